@@ -1,0 +1,165 @@
+"""CPU oracle for the mixed-precision iterative-refinement solve (arXiv 0808.2794, Alg. 1).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_0808_2794_b200``) never imports it and the
+two share no code.  The arithmetic lives in ``oracle/oracle.c`` (plain loops,
+fp32 / fp64, see its header for the passages each function follows); this
+module only builds that file with gcc and marshals numpy arrays through ctypes.
+
+Layout: matrices are numpy arrays in Fortran (column-major) order, exactly the
+C-ABI convention: A is n x n, B and X are n x nrhs with leading dimension n.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_CFLAGS = ["-O3", "-march=x86-64-v2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+           "-fPIC", "-shared", "-std=c11"]
+_lock = threading.Lock()
+_lib = None
+
+ITERMAX = 30
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            i64, p = ctypes.c_int64, ctypes.c_void_p
+            pint = ctypes.POINTER(ctypes.c_int)
+            lib.oracle_sgetf2.argtypes = [i64, p, i64, p]
+            lib.oracle_dgetf2.argtypes = [i64, p, i64, p]
+            lib.oracle_sgetrs.argtypes = [i64, i64, p, i64, p, p]
+            lib.oracle_dgetrs.argtypes = [i64, i64, p, i64, p, p]
+            lib.oracle_residual.argtypes = [i64, i64, p, i64, p, p, p]
+            lib.oracle_fro_norm.argtypes = [i64, p, i64]
+            lib.oracle_fro_norm.restype = ctypes.c_double
+            lib.oracle_dgesv.argtypes = [i64, i64, p, i64, p, p, pint]
+            lib.oracle_dsgesv_ex.argtypes = [i64, i64, p, i64, p, p, pint, pint, ctypes.c_int,
+                                             p, pint, ctypes.POINTER(ctypes.c_double)]
+            lib.oracle_num_threads.restype = ctypes.c_int
+            lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+            _lib = lib
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def _fortran(a, dtype):
+    return np.asfortranarray(np.asarray(a, dtype=dtype))
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def set_num_threads(t: int) -> None:
+    _load().oracle_set_num_threads(int(t))
+
+
+def sgetf2(A):
+    """Step 1 in binary32: returns (LU packed, ipiv 0-based, zero_pivot_info)."""
+    LU = _fortran(A, np.float32).copy(order="F")
+    n = LU.shape[0]
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = _load().oracle_sgetf2(n, _ptr(LU), max(1, n), _ptr(ipiv))
+    return LU, ipiv, int(info)
+
+
+def dgetf2(A):
+    LU = _fortran(A, np.float64).copy(order="F")
+    n = LU.shape[0]
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = _load().oracle_dgetf2(n, _ptr(LU), max(1, n), _ptr(ipiv))
+    return LU, ipiv, int(info)
+
+
+def sgetrs(LU, ipiv, B):
+    LU = _fortran(LU, np.float32)
+    n = LU.shape[0]
+    Bm = _fortran(B, np.float32).reshape(n, -1, order="F").copy(order="F")
+    _load().oracle_sgetrs(n, Bm.shape[1], _ptr(LU), max(1, n), _ptr(np.ascontiguousarray(ipiv, np.int32)), _ptr(Bm))
+    return Bm.reshape(np.shape(B), order="F")
+
+
+def dgetrs(LU, ipiv, B):
+    LU = _fortran(LU, np.float64)
+    n = LU.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F").copy(order="F")
+    _load().oracle_dgetrs(n, Bm.shape[1], _ptr(LU), max(1, n), _ptr(np.ascontiguousarray(ipiv, np.int32)), _ptr(Bm))
+    return Bm.reshape(np.shape(B), order="F")
+
+
+def residual(A, X, B):
+    """Step 4: R = B - A X in binary64 with the original A."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Xm = _fortran(X, np.float64).reshape(n, -1, order="F")
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    R = np.empty_like(Bm, order="F")
+    _load().oracle_residual(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(Xm), _ptr(R))
+    return R.reshape(np.shape(B), order="F")
+
+
+def fro_norm(A) -> float:
+    A = _fortran(A, np.float64)
+    return float(_load().oracle_fro_norm(A.shape[0], _ptr(A), max(1, A.shape[0])))
+
+
+def dgesv(A, B):
+    """Full binary64 GEPP solve (the fallback / mp_dgesv semantics). Returns (X, info)."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    X = np.zeros_like(Bm, order="F")
+    info = ctypes.c_int(0)
+    _load().oracle_dgesv(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), ctypes.byref(info))
+    return X.reshape(np.shape(B), order="F"), info.value
+
+
+class Result:
+    __slots__ = ("X", "iters", "info", "hist", "anrm")
+
+    def __init__(self, X, iters, info, hist, anrm):
+        self.X, self.iters, self.info, self.hist, self.anrm = X, iters, info, hist, anrm
+
+    def __iter__(self):  # allow  X, iters, info = dsgesv(...)
+        return iter((self.X, self.iters, self.info))
+
+
+def dsgesv(A, B, itermax: int = ITERMAX, lda: int | None = None) -> Result:
+    """Algorithm 1 with B:5's stop test, cap and fallback."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64)
+    Bm = Bm.reshape(n, Bm.size // n if n else (Bm.shape[1] if Bm.ndim > 1 else 1), order="F")
+    X = np.zeros_like(Bm, order="F")
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(itermax + 1, dtype=np.float64)
+    anrm = ctypes.c_double(0.0)
+    _load().oracle_dsgesv_ex(n, Bm.shape[1], _ptr(A), lda if lda is not None else max(1, n), _ptr(Bm), _ptr(X),
+                             ctypes.byref(iters), ctypes.byref(info), int(itermax), _ptr(hist),
+                             ctypes.byref(nh), ctypes.byref(anrm))
+    return Result(X.reshape(np.shape(B), order="F"), iters.value, info.value, hist[: nh.value].copy(), anrm.value)
