@@ -1,0 +1,309 @@
+#!/usr/bin/env python
+"""bench.py — FP64-accurate mixed-precision solve throughput on B200 (BASELINE.json metric).
+
+One "step" = one full mp_dsgesv solve (Alg. 1 of arXiv 0808.2794: demote, binary32
+blocked GEPP, x0, binary64 residual / binary32 correction loop until B:5's test)
+of the C3 workload: n = 16384, A i.i.d. N(0,1) fp64 (2.1 GB > L2), x_true U[-1,1],
+b = A x_true, nrhs = 1.  Inputs are resident in HBM when the timed region starts;
+A (2.1 GB) is larger than L2, so no flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mine|reference]
+
+value        = 2 n^3 / 3 flops per solve x solves (all ranks) / device time (max over ranks), GFLOP/s
+e2e          = same metric through the C-ABI with HOST buffers (H2D of A, b and D2H of x inside)
+speedup_vs_fp64 = t(mp_dgesv) / t(mp_dsgesv) on the same inputs (B:5; the paper's T3 analog)
+roofline     = dominant kernel class (CUDA events around each launch inside the timed region)
+cpu_baseline = the CPU oracle (oracle/oracle.c) on a bounded sample, rank 0, N = 1 only
+--impl reference: this tier's reference arm is the oracle itself (no reference package exists).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_0808_2794_b200 import inputs  # noqa: E402
+
+WORKLOAD = "C3: n=16384 dense nonsymmetric, A iid N(0,1) fp64, x_true U[-1,1], b=A x_true, nrhs=1"
+METRIC = "FP64-accurate solve GFLOP/s (2n^3/3 per solve), mixed fp32 LU + fp64 refinement"
+
+
+def flops(n: int) -> float:
+    return 2.0 * n ** 3 / 3.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- reference arm (the oracle)
+def cpu_oracle_sample(n_cpu: int, seed: int):
+    import oracle
+    oracle.build()
+    A, B, _ = inputs.gaussian(n_cpu, nrhs=1, seed=seed)
+    t0 = time.perf_counter()
+    r = oracle.dsgesv(A, B)
+    dt = time.perf_counter() - t0
+    return dt, r, oracle.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    n_cpu = args.cpu_n
+    times = []
+    for i in range(args.warmup + args.steps):
+        dt, r, threads = cpu_oracle_sample(n_cpu, inputs.BASE_SEED)
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    v = flops(n_cpu) / t / 1e9
+    out = {"metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": WORKLOAD, "n": args.n, "nrhs": 1, "sample_n": n_cpu},
+           "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                            "sample": f"one full oracle_dsgesv solve per step at n={n_cpu} (same generator), "
+                                      f"iters={r.iters}"},
+           "e2e": {"value": round(v, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--nb", type=int, default=0)
+    ap.add_argument("--variant", default="ffma", choices=["ffma", "3xtf32"])
+    ap.add_argument("--fp64-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-n", type=int, default=3072)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", local if world > 1 else 0)
+
+    from paper_0808_2794_b200 import binding as mp
+    variant = mp.MP_VARIANT_FFMA if args.variant == "ffma" else mp.MP_VARIANT_3XTF32
+    opts = mp.make_opts(nb=args.nb, variant=variant, flags=2)     # bit 1: per-kernel-class event timing
+    n, nrhs = args.n, args.nrhs
+
+    # inputs: one independent system per rank (weak scaling; replicas until the 1D block-cyclic path lands)
+    A, B, Xt = inputs.gaussian(n, nrhs=nrhs, seed=inputs.BASE_SEED + rank)
+    dA = torch.from_numpy(np.ascontiguousarray(A.T)).to(dev).t()
+    dB = torch.from_numpy(np.ascontiguousarray(B.T)).to(dev).t()
+    dX = torch.empty((nrhs, n), dtype=torch.float64, device=dev).t()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def solve():
+        _, it, info, rep = mp.mp_dsgesv_ex(dA, dB, dX, opts)
+        return it, info, rep
+
+    for _ in range(args.warmup):
+        it, info, rep = solve()
+    assert info == 0 and it >= 0, (it, info)
+
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            reps.append(solve())
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = flops(n) * args.steps * world / (ms_total / 1e3) / 1e9
+    iters = [r[0] for r in reps]
+
+    # per-kernel-class breakdown over the timed region (CUDA events on the launching stream)
+    kern = {}
+    launches = 0
+    for _, _, rep in reps:
+        launches += rep.kernel_launches
+        for name, d in rep.kernels().items():
+            k = kern.setdefault(name, {"ms": 0.0, "work": 0.0, "launches": 0})
+            k["ms"] += d["ms"]; k["work"] += d["work"]; k["launches"] += d["launches"]
+    pk, pk_src = peaks()
+    sm_max = pk.get("sm_max_mhz", 1965.0)
+    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12           # TFLOP/s, FP32 FMA lanes x clock
+    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])[0] if kern else None
+    roof = None
+    if dom:
+        d = kern[dom]
+        if dom in ("gemm", "trsm", "panel"):
+            ach = d["work"] / (d["ms"] / 1e3) / 1e12
+            roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(ffma_peak, 1),
+                    "unit": "TFLOP/s", "frac": round(ach / ffma_peak, 4), "traffic": None,
+                    "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",
+                    "launches": d["launches"] // args.steps, "avg_launch_us": round(d["ms"] * 1e3 / d["launches"], 2)}
+        else:
+            ach = d["work"] / (d["ms"] / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": pk_src}
+    breakdown = {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
+                     ("tflops" if k in ("gemm", "trsm", "panel") else "gbs"):
+                         round(v["work"] / (v["ms"] / 1e3) / (1e12 if k in ("gemm", "trsm", "panel") else 1e9), 2)
+                         if v["ms"] > 0 else None}
+                 for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
+
+    # FP64 path on the same inputs (speedup denominator, B:5)
+    fp64_ms = None
+    if args.fp64_steps > 0:
+        o64 = mp.make_opts(nb=args.nb)
+        Xd, info64, _ = mp.mp_dgesv_ex(dA, dB, None, o64)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.fp64_steps):
+            mp.mp_dgesv_ex(dA, dB, Xd, o64, report=False)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        fp64_ms = f0.elapsed_time(f1) / args.fp64_steps
+
+    # end-to-end through the C-ABI with pinned HOST buffers (copies inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        hA = torch.from_numpy(np.ascontiguousarray(A.T)).pin_memory()
+        hB = torch.from_numpy(np.ascontiguousarray(B.T)).pin_memory()
+        hX = torch.empty((nrhs, n), dtype=torch.float64).pin_memory()
+        nA, nB, nX = hA.numpy().T, hB.numpy().T, hX.numpy().T      # Fortran views of pinned memory
+        mp.mp_dsgesv_ex(nA, nB, nX, mp.make_opts(nb=args.nb, variant=variant), report=False)
+        barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.e2e_steps):
+            mp.mp_dsgesv_ex(nA, nB, nX, mp.make_opts(nb=args.nb, variant=variant), report=False)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = g0.elapsed_time(g1) / args.e2e_steps
+        if dist is not None:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": round(flops(n) * world / (e2e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": 8 * n * n + 8 * n * nrhs, "d2h_bytes_per_step": 8 * n * nrhs,
+               "ms_per_step": round(e2e_ms, 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        dt, r, threads = cpu_oracle_sample(args.cpu_n, inputs.BASE_SEED)
+        cpu = {"value": round(flops(args.cpu_n) / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
+               "kind": "oracle", "sample": f"one full oracle_dsgesv solve at n={args.cpu_n} (same generator, "
+                                           f"{dt:.1f} s, iters={r.iters}); the n=16384 solve is ~150x that work"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+               "config": {"workload": WORKLOAD, "n": n, "nrhs": nrhs, "nb": reps[-1][2].nb,
+                          "variant": args.variant, "iters": iters,
+                          "l2": "inputs larger than L2 (A fp64 = %.2f GB)" % (8 * n * n / 1e9),
+                          "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+               "speedup_vs_fp64": round(fp64_ms / ms_step, 3) if fp64_ms else None,
+               "fp64_ms_per_step": round(fp64_ms, 3) if fp64_ms else None,
+               "e2e": e2e, "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu,
+               "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,169 @@
+/*
+ * mp_solve.h — C-ABI of libmpsolve.so, the B200 (sm_100a) mixed-precision
+ * iterative-refinement dense solver of arXiv 0808.2794.
+ *
+ * Operation (Algorithm 1; BASELINE.json north_star B:5):
+ *   1  LU <- PA             binary32 blocked right-looking GEPP of fl32(A)
+ *   2-3 L y = P b; U x0 = y  binary32 substitution
+ *   loop k = 1, 2, ...
+ *   4  r_k <- b - A x_{k-1} binary64, with the ORIGINAL A
+ *   5-6 L y = P r_k; U z_k = y  binary32
+ *   7  x_k <- x_{k-1} + z_k binary64
+ *   check convergence: for every rhs column c
+ *        ||r_c||_2 < ||x_c||_2 * ||A||_F * 2^-53 * sqrt(n)   or  ||r_c||_2 == 0
+ *   (B:5 replaces the paper's spectral norm, by ||A||_F; readings
+ *   A-1..A-5 in DESIGN.md), at most 30 corrections, then the full
+ *   binary64 solver on a fresh copy of A.
+ *
+ * Layout: column-major.  A is n x n with leading dimension lda >= max(1,n),
+ * entry (i,j) at A[i + j*lda].  B and X are n x nrhs with leading dimension n.
+ *
+ * Pointers: every matrix/vector argument may be a CUDA device pointer (the
+ * device current on the calling thread) or a host pointer (pinned or
+ * pageable); the library detects which with cudaPointerGetAttributes and, for
+ * host buffers, stages the copies itself (H2D of A and B, D2H of X) on the
+ * library stream.  A host call is the "end-to-end" path.
+ *
+ * Ownership: the caller owns A, B, X.  A and B are read-only (never
+ * overwritten, unlike LAPACK DSGESV).  X is written.  The library allocates
+ * its workspace stream-ordered (cudaMallocAsync): a binary32 n x n working
+ * copy (the "+50 % memory" of P:145-146) plus O(n * nrhs) vectors; a binary64
+ * n x n copy only when the fallback runs.  Workspace is released before the
+ * call returns.
+ *
+ * Synchronisation: every solve call is synchronous with respect to the host
+ * (the convergence test reads one small status record per iteration).  Calls
+ * are not re-entrant for the same device from several threads.
+ *
+ * Return value: MP_OK (0), or a runtime failure code (MP_ERR_*): a CUDA error,
+ * an allocation failure, or an internal error; mp_last_error() describes it.
+ * Numerical outcomes go to *info / *iters, never to the return value.
+ *
+ * *info: 0 success; -i: the i-th argument is illegal (1 n < 0, 2 nrhs < 0,
+ *   3 A NULL / A has a NaN or Inf entry, 4 lda < max(1,n), 5 B NULL / B has a
+ *   NaN or Inf entry, 6 X NULL or X overlaps A or B); +i: U(i,i) (1-based) is
+ *   exactly zero in the binary64 factorisation, X is unspecified.
+ * *iters: >= 0 number of refinement corrections applied (0: x0 passed the
+ *   test); -2 a finite entry of A overflowed binary32 on demotion; -3 exact
+ *   zero pivot in the binary32 LU; -31 no convergence within itermax (30)
+ *   corrections, or a non-finite residual/solution norm.  iters < 0 means
+ *   the binary64 solver produced X.
+ * Quick return: n == 0 or nrhs == 0 -> info = 0, iters = 0, nothing touched.
+ */
+#ifndef MP_SOLVE_H
+#define MP_SOLVE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MP_OK            0
+#define MP_ERR_CUDA      1
+#define MP_ERR_NOMEM     2
+#define MP_ERR_INTERNAL  3
+#define MP_ERR_NCCL      4
+#define MP_ERR_UNSUPPORTED 5
+
+#define MP_ITERMAX_DEFAULT 30
+
+/* Trailing-update (Schur complement A22 -= L21 U12) variant of the binary32
+ * factorisation.  Both compute in binary32 precision; B:5 keeps a variant only
+ * if refinement still reaches the binary64 backward criterion. */
+#define MP_VARIANT_FFMA    0   /* FP32 FFMA SGEMM (CUDA cores) */
+#define MP_VARIANT_3XTF32  1   /* tcgen05 tensor cores, 3xTF32 split (hi*hi + hi*lo + lo*hi) */
+
+typedef struct mp_opts {
+    int32_t nb;        /* panel width; 0 = default (64 for n<=1024, 128 for n<=4096, else 256) */
+    int32_t itermax;   /* refinement cap; 0 = MP_ITERMAX_DEFAULT */
+    int32_t variant;   /* MP_VARIANT_* (default MP_VARIANT_FFMA) */
+    int32_t flags;     /* bit 0: force the binary64 fallback path after the binary32 factorisation (testing);
+                          bit 1: per-kernel-class CUDA-event timing into mp_report.k_* (measurement) */
+} mp_opts;
+
+#define MP_HIST_MAX 64
+
+typedef struct mp_report {
+    int32_t iters, info;        /* same values as the *iters / *info outputs */
+    int32_t nhist;              /* number of residual checks recorded in hist[] */
+    int32_t nb, variant, pad;   /* panel width / variant actually used */
+    double  anrm;               /* ||A||_F (binary64, computed once on device) */
+    double  hist[MP_HIST_MAX];  /* per residual check: max_c ||r_c|| / (||x_c|| * ||A||_F * 2^-53 * sqrt(n)) */
+    double  t_total_ms;         /* device time of the whole call (CUDA events) */
+    double  t_demote_ms;        /* K1: demote + ||A||_F */
+    double  t_factor_ms;        /* binary32 (or binary64 for mp_dgesv) factorisation */
+    double  t_refine_ms;        /* x0 + refinement loop */
+    double  t_fallback_ms;      /* binary64 fallback, if it ran */
+    double  t_copy_ms;          /* host<->device staging (host-pointer calls only) */
+    int64_t workspace_bytes;    /* peak bytes allocated by the library for this call */
+    int64_t kernel_launches;    /* number of library kernels launched by this call */
+    /* per kernel class (filled when opts.flags bit 1 is set), index = MP_KC_*:
+       summed device time of the launches (CUDA events on the launching stream),
+       number of launches, and their summed ALGORITHMIC work (flops for
+       MP_KC_GEMM / MP_KC_TRSM, bytes for the bandwidth-bound classes). */
+    double  k_ms[8];
+    double  k_work[8];
+    int64_t k_launches[8];
+} mp_report;
+
+#define MP_KC_DEMOTE   0   /* K1 demote + ||A||_F          work = bytes (12 n^2)          */
+#define MP_KC_PANEL    1   /* K2 panel factorisation       work = flops of the leaf       */
+#define MP_KC_LASWP    2   /* K3 row interchanges          work = bytes moved             */
+#define MP_KC_TRSM     3   /* K4 U12 <- L11^-1 A12         work = flops (w^2 N)           */
+#define MP_KC_GEMM     4   /* K5 Schur update              work = flops (2 M N K)         */
+#define MP_KC_SOLVE    5   /* K6/K7/K9 triangular solves   work = bytes of the factors    */
+#define MP_KC_RESIDUAL 6   /* K8/K10 residual + test       work = bytes (8 n^2 + vectors)  */
+#define MP_KC_OTHER    7
+
+/* Fill *o with the defaults above. */
+void mp_default_opts(mp_opts *o);
+
+/* Mixed-precision solve A X = B (Algorithm 1 + B:5 stop test + fallback). */
+int mp_dsgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+              const double *B, double *X, int *iters, int *info);
+
+/* Same, with options (NULL = defaults) and an optional report (NULL = none). */
+int mp_dsgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+                 const double *B, double *X, int *iters, int *info,
+                 const mp_opts *opts, mp_report *rep);
+
+/* Binary64 reference solver built the same way (DGETRF + DGETRS semantics,
+ * no refinement): the denominator of the speedup (B:5). */
+int mp_dgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+             const double *B, double *X, int *info);
+
+int mp_dgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+                const double *B, double *X, int *info,
+                const mp_opts *opts, mp_report *rep);
+
+/* Step 1 alone, for factor-level parity: demote A (RN-even),
+ * factor PA = LU in binary32 with the same kernels as mp_dsgesv, and return
+ * the packed factors LU (n x n column-major, leading dimension n, unit lower
+ * L below the diagonal, U on/above) and ipiv (0-based LAPACK-style sequential
+ * pivot list: at step k rows k and ipiv[k] were interchanged).  *info: as
+ * above for argument errors (-1 n, -3 A, -4 lda, -5 LU NULL, -6 ipiv NULL);
+ * +k when the first exact zero pivot is at column k (1-based); -2 when a
+ * finite entry of A overflowed binary32. */
+int mp_sgetrf(int64_t n, const double *A, int64_t lda, float *LU, int32_t *ipiv,
+              int *info, const mp_opts *opts);
+
+/* Same in binary64 (the fallback / mp_dgesv factorisation). */
+int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv,
+              int *info, const mp_opts *opts);
+
+/* Use this CUDA stream (a cudaStream_t, NULL = the legacy default stream) for
+ * all subsequent library work on the calling thread. */
+int mp_set_stream(void *stream);
+
+/* Human-readable description of the last runtime failure on this thread. */
+const char *mp_last_error(void);
+
+/* Library version / build string (arch, variant support). */
+const char *mp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MP_SOLVE_H */

@@ -5,15 +5,19 @@ stop test: FP32 blocked GEPP + FP32 triangular solves + FP64 residual/update on
 sm_100a, behind the C-ABI of include/mp_solve.h (libmpsolve.so).  This package
 is the thin Python binding (argument marshalling only) plus input generators.
 """
+import importlib
+
 from .inputs import BASE_SEED  # noqa: F401  (input generators carry no method arithmetic)
 
-__all__ = ["mp_dsgesv", "mp_dgesv", "mp_dsgesv_ex", "lib"]
+_SUBMODULES = {"binding", "build", "inputs"}
 
 
 def __getattr__(name):
     # lazy: importing the package (e.g. for inputs) must not require the CUDA library
-    if name in ("mp_dsgesv", "mp_dgesv", "mp_dsgesv_ex", "lib", "Report", "Opts", "MpError",
-                "mp_factor_f32", "mp_solve_f32", "mp_version"):
-        from . import binding
+    if name.startswith("_") or name in _SUBMODULES:
+        raise AttributeError(name)
+    binding = importlib.import_module(__name__ + ".binding")
+    try:
         return getattr(binding, name)
-    raise AttributeError(name)
+    except AttributeError:
+        raise AttributeError(name) from None

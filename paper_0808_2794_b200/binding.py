@@ -1,0 +1,206 @@
+"""Thin ctypes binding of libmpsolve.so (include/mp_solve.h) — argument marshalling only.
+
+Names mirror the C-ABI.  Matrices are column-major (Fortran order):
+* torch CUDA tensors: A of shape (n, n) with stride (1, lda); B, X of shape
+  (n, nrhs) with stride (1, n) — see ``colmajor_cuda`` to build them;
+* numpy arrays (host): Fortran-ordered float64 — the library stages the
+  host<->device copies itself (the end-to-end path).
+
+Every step of the solve runs in the CUDA kernels of libmpsolve.so.  If the
+library is missing this module raises at import time: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpsolve.so")
+
+MP_OK, MP_ERR_CUDA, MP_ERR_NOMEM, MP_ERR_INTERNAL, MP_ERR_NCCL, MP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4, 5
+MP_VARIANT_FFMA, MP_VARIANT_3XTF32 = 0, 1
+MP_HIST_MAX = 64
+KCLASSES = ("demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "other")
+
+
+class Opts(ctypes.Structure):
+    _fields_ = [("nb", ctypes.c_int32), ("itermax", ctypes.c_int32), ("variant", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("info", ctypes.c_int32), ("nhist", ctypes.c_int32),
+                ("nb", ctypes.c_int32), ("variant", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("anrm", ctypes.c_double), ("hist", ctypes.c_double * MP_HIST_MAX),
+                ("t_total_ms", ctypes.c_double), ("t_demote_ms", ctypes.c_double),
+                ("t_factor_ms", ctypes.c_double), ("t_refine_ms", ctypes.c_double),
+                ("t_fallback_ms", ctypes.c_double), ("t_copy_ms", ctypes.c_double),
+                ("workspace_bytes", ctypes.c_int64), ("kernel_launches", ctypes.c_int64),
+                ("k_ms", ctypes.c_double * 8), ("k_work", ctypes.c_double * 8), ("k_launches", ctypes.c_int64 * 8)]
+
+    def history(self):
+        return [self.hist[i] for i in range(self.nhist)]
+
+    def kernels(self):
+        return {KCLASSES[i]: {"ms": self.k_ms[i], "work": self.k_work[i], "launches": self.k_launches[i]}
+                for i in range(8) if self.k_launches[i]}
+
+
+class MpError(RuntimeError):
+    pass
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_0808_2794_b200.build` "
+                      "(there is no CPU fallback for the CUDA path)")
+
+lib = ctypes.CDLL(LIB_PATH)
+_i64, _p, _pi = ctypes.c_int64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)
+lib.mp_default_opts.argtypes = [ctypes.POINTER(Opts)]
+lib.mp_default_opts.restype = None
+lib.mp_dsgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, _pi]
+lib.mp_dsgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+lib.mp_dgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi]
+lib.mp_dgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+lib.mp_sgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_dgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_set_stream.argtypes = [_p]
+lib.mp_last_error.restype = ctypes.c_char_p
+lib.mp_version.restype = ctypes.c_char_p
+
+EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
+            "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version")
+
+
+def mp_version() -> str:
+    return lib.mp_version().decode()
+
+
+def _check(rc: int):
+    if rc != MP_OK:
+        raise MpError(f"libmpsolve error {rc}: {lib.mp_last_error().decode()}")
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr_ld(M, name: str, square: bool):
+    """Pointer and leading dimension of a column-major matrix (torch tensor or numpy array)."""
+    if _is_torch(M):
+        if M.dtype.is_floating_point and M.element_size() != 8:
+            raise TypeError(f"{name} must be float64")
+        if M.dim() == 1:
+            return M.data_ptr(), M.shape[0]
+        if M.stride(0) != 1:
+            raise ValueError(f"{name} must be column-major (stride(0) == 1); use colmajor_cuda()")
+        return M.data_ptr(), max(M.stride(1), 1)
+    A = np.asarray(M)
+    if A.dtype != np.float64:
+        raise TypeError(f"{name} must be float64")
+    if A.ndim == 2 and not A.flags.f_contiguous:
+        raise ValueError(f"{name} must be Fortran-ordered")
+    return A.ctypes.data, A.shape[0]
+
+
+def _stream_of(*ts):
+    for t in ts:
+        if _is_torch(t) and t.is_cuda:
+            import torch
+            return torch.cuda.current_stream(t.device).cuda_stream
+    return None
+
+
+def colmajor_cuda(M, device="cuda"):
+    """Fortran-ordered numpy (n, k) -> torch CUDA float64 tensor of shape (n, k), stride (1, n)."""
+    import torch
+    M = np.asfortranarray(np.asarray(M, dtype=np.float64))
+    if M.ndim == 1:
+        M = M[:, None]
+    return torch.from_numpy(np.ascontiguousarray(M.T)).to(device).t()
+
+
+def _alloc_like_X(B, n, nrhs):
+    if _is_torch(B):
+        import torch
+        return torch.empty((nrhs, n), dtype=torch.float64, device=B.device).t()
+    return np.zeros((n, nrhs), dtype=np.float64, order="F")
+
+
+def _nrhs(B, n):
+    return 1 if len(B.shape) == 1 else B.shape[1]
+
+
+def mp_dsgesv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
+    """Mixed-precision solve; returns (X, iters, info, Report|None)."""
+    n = A.shape[0]
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(B, "B", False)
+    px, _ = _ptr_ld(X, "X", False)
+    lib.mp_set_stream(_stream_of(A, B, X))
+    it, info = ctypes.c_int(0), ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_dsgesv_ex(n, nrhs, pa, lda, pb, px, ctypes.byref(it), ctypes.byref(info),
+                            ctypes.byref(opts) if opts is not None else None,
+                            ctypes.byref(rep) if rep is not None else None))
+    return X, it.value, info.value, rep
+
+
+def mp_dsgesv(A, B, X=None, opts: Opts | None = None):
+    X, it, info, _ = mp_dsgesv_ex(A, B, X, opts, report=False)
+    return X, it, info
+
+
+def mp_dgesv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
+    n = A.shape[0]
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(B, "B", False)
+    px, _ = _ptr_ld(X, "X", False)
+    lib.mp_set_stream(_stream_of(A, B, X))
+    info = ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_dgesv_ex(n, nrhs, pa, lda, pb, px, ctypes.byref(info),
+                           ctypes.byref(opts) if opts is not None else None,
+                           ctypes.byref(rep) if rep is not None else None))
+    return X, info.value, rep
+
+
+def mp_dgesv(A, B, X=None, opts: Opts | None = None):
+    X, info, _ = mp_dgesv_ex(A, B, X, opts, report=False)
+    return X, info
+
+
+def _getrf(fn, dtype, A, opts):
+    n = A.shape[0]
+    pa, lda = _ptr_ld(A, "A", True)
+    LU = np.zeros((n, n), dtype=dtype, order="F")
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = ctypes.c_int(0)
+    lib.mp_set_stream(_stream_of(A))
+    _check(fn(n, pa, lda, LU.ctypes.data, ipiv.ctypes.data, ctypes.byref(info),
+              ctypes.byref(opts) if opts is not None else None))
+    return LU, ipiv, info.value
+
+
+def mp_sgetrf(A, opts: Opts | None = None):
+    """Step 1 alone (binary32 GEPP of fl32(A)); returns host (LU float32 Fortran, ipiv 0-based, info)."""
+    return _getrf(lib.mp_sgetrf, np.float32, A, opts)
+
+
+def mp_dgetrf(A, opts: Opts | None = None):
+    return _getrf(lib.mp_dgetrf, np.float64, A, opts)
+
+
+def make_opts(nb: int = 0, itermax: int = 30, variant: int = MP_VARIANT_FFMA, flags: int = 0) -> Opts:
+    o = Opts()
+    lib.mp_default_opts(ctypes.byref(o))
+    o.nb, o.itermax, o.variant, o.flags = nb, itermax, variant, flags
+    return o

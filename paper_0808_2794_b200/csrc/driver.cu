@@ -1,0 +1,632 @@
+// driver.cu — host orchestration of the hot path and the C-ABI entry points of
+// include/mp_solve.h.
+//
+// mp_dsgesv  = PAPER.md Algorithm 1 with BASELINE.json B:5's stop
+//              test, 30-correction cap and binary64 fallback
+//              (P:603-605):
+//   K1 demote+||A||_F -> binary32 blocked GEPP (K2 panel / K3 laswp / K4 trsm /
+//   K5 Schur update) -> x0 (K6 + K7) -> loop { K8+K10 residual & test ->
+//   host reads one status record -> K7+K9 correction }.
+// mp_dgesv   = the same blocked GEPP and solves instantiated in binary64, no
+//              refinement (the "standard double precision solver").
+//
+// Every step runs in the kernels of this library; the host only sequences
+// launches and reads the per-iteration status.  There is no CPU fallback: a
+// missing GPU or a CUDA error is returned as MP_ERR_CUDA.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/mp_solve.h"
+#include "internal.h"
+
+namespace mp {
+
+thread_local int64_t g_launches = 0;
+static thread_local std::string g_err;
+static thread_local cudaStream_t g_stream = nullptr;
+
+struct NoMem {};
+
+// ------------------------------------------------------------------ per-class timing
+namespace {
+struct ProfRec { int cls, a, b; double work; };
+struct ProfState {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    int open[KC_COUNT] = {0};
+    std::vector<ProfRec> recs;
+    int take() {
+        if (used == ev.size()) {
+            cudaEvent_t e;
+            MP_CUDA(cudaEventCreate(&e));
+            ev.push_back(e);
+        }
+        return (int)used++;
+    }
+    void reset(bool enable) { on = enable; used = 0; recs.clear(); }
+};
+thread_local ProfState g_prof;
+}  // namespace
+
+void prof_begin(int cls, cudaStream_t s)
+{
+    if (!g_prof.on) return;
+    const int i = g_prof.take();
+    MP_CUDA(cudaEventRecord(g_prof.ev[i], s));
+    g_prof.open[cls] = i;
+}
+
+void prof_end(int cls, double work, cudaStream_t s)
+{
+    if (!g_prof.on) return;
+    const int i = g_prof.take();
+    MP_CUDA(cudaEventRecord(g_prof.ev[i], s));
+    g_prof.recs.push_back({cls, g_prof.open[cls], i, work});
+}
+
+static void prof_collect(mp_report *rep)
+{
+    if (!g_prof.on || !rep) return;
+    for (const ProfRec &r : g_prof.recs) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, g_prof.ev[r.a], g_prof.ev[r.b]) != cudaSuccess) { cudaGetLastError(); t = 0.f; }
+        rep->k_ms[r.cls] += t;
+        rep->k_work[r.cls] += r.work;
+        rep->k_launches[r.cls] += 1;
+    }
+}
+
+namespace {
+
+// ------------------------------------------------------------------ memory
+struct Pool {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    int64_t bytes = 0;
+    explicit Pool(cudaStream_t st) : s(st) {}
+    ~Pool() { release(); }
+    void release() {
+        for (void *p : ptrs) cudaFreeAsync(p, s);
+        ptrs.clear();
+    }
+    template <typename T>
+    T *get(size_t count) {
+        if (count == 0) count = 1;
+        void *p = nullptr;
+        const size_t b = round_up((int64_t)(count * sizeof(T)), 256);
+        cudaError_t e = cudaMallocAsync(&p, b, s);
+        if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw NoMem{}; }
+        MP_CUDA(e);
+        ptrs.push_back(p);
+        bytes += (int64_t)b;
+        return static_cast<T *>(p);
+    }
+};
+
+void configure_mempool_once()
+{
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    if (done_dev == dev) return;
+    cudaMemPool_t pool;
+    MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = UINT64_MAX;                 // keep freed workspace cached between calls
+    MP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done_dev = dev;
+}
+
+bool is_device_ptr(const void *p)
+{
+    if (!p) return false;
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) { cudaGetLastError(); return false; }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+bool overlaps(const void *a, size_t ab, const void *b, size_t bb)
+{
+    const char *pa = static_cast<const char *>(a), *pb = static_cast<const char *>(b);
+    return pa < pb + bb && pb < pa + ab;
+}
+
+int num_sms()
+{
+    int dev = 0, sms = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return std::min(sms, kMaxSMs);
+}
+
+int default_nb(int64_t n) { return n <= 1024 ? 64 : (n <= 4096 ? 128 : 256); }
+
+struct Timer {
+    cudaEvent_t e[12];
+    int k = 0;
+    cudaStream_t s;
+    explicit Timer(cudaStream_t st) : s(st) {
+        for (auto &x : e) MP_CUDA(cudaEventCreate(&x));
+    }
+    ~Timer() { for (auto &x : e) cudaEventDestroy(x); }
+    int mark() { MP_CUDA(cudaEventRecord(e[k], s)); return k++; }
+    double ms(int a, int b) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, e[a], e[b]) != cudaSuccess) { cudaGetLastError(); return 0.0; }
+        return (double)t;
+    }
+};
+
+// ------------------------------------------------------------------ blocked GEPP
+template <typename T>
+struct Factor {
+    T *W;
+    int64_t n, ldw;
+    int32_t *ipiv, *perm;
+    PanelScratch ps;
+    DevStatus *st;
+    int sms;
+    cudaStream_t s;
+
+    void leaf(int64_t c0, int w) {
+        const double m = (double)(n - c0);
+        prof_begin(KC_PANEL, s);
+        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, sms, s);
+        prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, s);
+        // the leaf interchanged full rows inside its own columns; apply the same
+        // interchanges to every other column (left factors and trailing matrix)
+        prof_begin(KC_LASWP, s);
+        launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, 0, n, c0, c0 + w, perm, s);
+        prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
+    }
+    void trsm(int64_t r0, int w, int64_t c_lo, int64_t c_hi) {
+        prof_begin(KC_TRSM, s);
+        launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, s);
+        prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), s);
+    }
+    void gemm(int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K) {
+        prof_begin(KC_GEMM, s);
+        launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+        prof_end(KC_GEMM, 2.0 * M * N * K, s);
+    }
+    // recursive panel: columns [c0, c0+w), rows [c0, n)
+    void panel(int64_t c0, int w) {
+        if (w <= 8 || panel_leaf_fits<T>(n - c0, w, sms)) { leaf(c0, w); return; }
+        const int w1 = (int)round_up(w / 2, 8);
+        panel(c0, w1);
+        trsm(c0, w1, c0 + w1, c0 + w);
+        gemm(c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1);
+        panel(c0 + w1, w - w1);
+    }
+    void run(int nb) {
+        launch_init_perm(perm, n, s);
+        for (int64_t k = 0; k < n; k += nb) {
+            const int w = (int)std::min<int64_t>(nb, n - k);
+            panel(k, w);
+            if (k + w < n) {
+                trsm(k, w, k + w, n);                                     // U12 <- L11^-1 A12
+                gemm(k + w, k + w, k, n - k - w, n - k - w, w);           // A22 -= L21 U12
+            }
+        }
+    }
+};
+
+template <typename T>
+void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
+                cudaStream_t s)
+{
+    Factor<T> f;
+    f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.sms = num_sms(); f.s = s;
+    void *scratch = pool.get<unsigned char>(panel_scratch_bytes(nb, sizeof(T)));
+    panel_scratch_carve(f.ps, scratch, nb, sizeof(T));
+    f.run(nb);
+}
+
+struct Args {
+    int64_t n, nrhs, lda;
+    const double *A, *B;
+    double *X;
+};
+
+// Staged device views of the caller's buffers (host pointers are copied in/out).
+struct Views {
+    const double *A, *B;
+    double *X;
+    int64_t lda;
+    bool x_host;
+};
+
+Views stage_in(const Args &a, Pool &pool, cudaStream_t s, bool need_b)
+{
+    Views v{a.A, a.B, a.X, a.lda, false};
+    if (!is_device_ptr(a.A)) {
+        double *d = pool.get<double>((size_t)a.n * a.n);
+        MP_CUDA(cudaMemcpy2DAsync(d, a.n * sizeof(double), a.A, a.lda * sizeof(double), a.n * sizeof(double),
+                                  a.n, cudaMemcpyHostToDevice, s));
+        v.A = d;
+        v.lda = a.n;
+    }
+    if (need_b && !is_device_ptr(a.B)) {
+        double *d = pool.get<double>((size_t)a.n * a.nrhs);
+        MP_CUDA(cudaMemcpyAsync(d, a.B, (size_t)a.n * a.nrhs * sizeof(double), cudaMemcpyHostToDevice, s));
+        v.B = d;
+    }
+    if (a.X && !is_device_ptr(a.X)) {
+        v.X = pool.get<double>((size_t)a.n * std::max<int64_t>(a.nrhs, 1));
+        v.x_host = true;
+    }
+    return v;
+}
+
+int check_args(const Args &a, int *info)
+{
+    const int64_t mx = std::max<int64_t>(1, a.n);
+    if (a.n < 0) return *info = -1, 1;
+    if (a.nrhs < 0) return *info = -2, 1;
+    if (a.n > 0 && !a.A) return *info = -3, 1;
+    if (a.lda < mx) return *info = -4, 1;
+    if (a.n > 0 && a.nrhs > 0 && !a.B) return *info = -5, 1;
+    if (a.n > 0 && a.nrhs > 0 && !a.X) return *info = -6, 1;
+    if (a.n > 0 && a.nrhs > 0) {
+        const size_t xb = (size_t)a.n * a.nrhs * sizeof(double);
+        const size_t ab = (size_t)((a.n - 1) * a.lda + a.n) * sizeof(double);
+        if (overlaps(a.X, xb, a.A, ab) || overlaps(a.X, xb, a.B, xb)) return *info = -6, 1;
+    }
+    return 0;
+}
+
+struct StatusIO {
+    DevStatus *d;
+    DevStatus *h;   // pinned
+    cudaStream_t s;
+    StatusIO(Pool &pool, cudaStream_t st) : s(st) {
+        d = pool.get<DevStatus>(1);
+        MP_CUDA(cudaMallocHost(&h, sizeof(DevStatus)));
+        std::memset(h, 0, sizeof(DevStatus));
+        h->zero_col = INT_MAX;
+        MP_CUDA(cudaMemcpyAsync(d, h, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+    }
+    ~StatusIO() { cudaFreeHost(h); }
+    const DevStatus &read() {
+        MP_CUDA(cudaMemcpyAsync(h, d, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        return *h;
+    }
+};
+
+// binary64 GEPP + substitution on a fresh working copy (reading A-11).
+// Returns info (0, or the 1-based column of the first exact zero pivot).
+int fp64_solve(const Views &v, int64_t n, int64_t nrhs, int nb, Pool &pool, StatusIO &sio, cudaStream_t s)
+{
+    const int64_t ldw = round_up(n, 64);
+    double *W = pool.get<double>((size_t)n * ldw);
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
+    double *Y = pool.get<double>((size_t)n * nrhs);
+    const int nblk = (int)ceil_div(n, solve_block_rows());
+    SolveScratch ss{pool.get<unsigned>(2 * (size_t)nblk), pool.get<unsigned>(2)};
+    launch_demote_transpose<double>(v.A, v.lda, n, W, ldw, nullptr, nullptr, sio.d, s);
+    run_factor<double>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
+    const DevStatus &st = sio.read();
+    if (st.flags & ST_A_NONFINITE) return -3;
+    if (st.flags & ST_ZERO_PIVOT) return st.zero_col;
+    launch_invert_perm(perm, pinv, n, s);
+    launch_permute_demote_rhs<double>(v.B, n, nrhs, pinv, Y, sio.d, s);
+    launch_lu_solve<double>(W, ldw, n, nrhs, Y, v.X, 0, ss, s);
+    return 0;
+}
+
+void finish_copy_out(const Args &a, const Views &v, cudaStream_t s)
+{
+    if (v.x_host)
+        MP_CUDA(cudaMemcpyAsync(a.X, v.X, (size_t)a.n * a.nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+}
+
+int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0; *iters = 0;
+    if (rep) { std::memset(rep, 0, sizeof(*rep)); }
+    if (check_args(a, info)) { if (rep) rep->info = *info; return MP_OK; }
+    if (a.n == 0 || a.nrhs == 0) return MP_OK;
+
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int nb = o.nb > 0 ? o.nb : default_nb(a.n);
+    const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    if (o.variant != MP_VARIANT_FFMA) throw std::runtime_error("variant not available in this build");
+    const int64_t n = a.n, nrhs = a.nrhs;
+    cudaStream_t s = g_stream;
+    configure_mempool_once();
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0);
+    Timer tm(s);
+    const int t0 = tm.mark();
+
+    Pool pool(s);
+    Views v = stage_in(a, pool, s, true);
+    const int t_staged = tm.mark();
+    StatusIO sio(pool, s);
+    const int sms = num_sms();
+    const int64_t ldw = round_up(n, 64);
+    float *W = pool.get<float>((size_t)n * ldw);                   // the +50 % of P:145-146
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
+    float *Y = pool.get<float>((size_t)n * nrhs);
+    double *R = pool.get<double>((size_t)n * nrhs);
+    ResidualScratch rs;
+    rs.partial = pool.get<double>(residual_partial_elems(n, nrhs, sms));
+    rs.blocksums = pool.get<double>((size_t)ceil_div(n, 256) * 2 * nrhs);
+    rs.counter = pool.get<unsigned>(1);
+    const int nblk = (int)ceil_div(n, solve_block_rows());
+    SolveScratch ss{pool.get<unsigned>(2 * (size_t)nblk), pool.get<unsigned>(2)};
+    double *dpart = pool.get<double>((size_t)sms * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+
+    // ---- K1: demote + ||A||_F; B finiteness (identity scatter into Y, discarded)
+    prof_begin(KC_DEMOTE, s);
+    launch_demote_transpose<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);
+    prof_end(KC_DEMOTE, 12.0 * n * n, s);
+    launch_init_perm(perm, n, s);
+    launch_permute_demote_rhs<float>(v.B, n, nrhs, perm, Y, sio.d, s);
+    const int t_dem = tm.mark();
+    DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) { *info = -3; if (rep) rep->info = -3; return MP_OK; }
+    if (st0.flags & ST_B_NONFINITE) { *info = -5; if (rep) rep->info = -5; return MP_OK; }
+    const double anrm = std::sqrt(st0.anrm2);
+    const double cte = anrm * std::ldexp(1.0, -53) * std::sqrt((double)n);   // A-1, A-2
+    int code = 0;
+    int t_fac = t_dem, t_ref = t_dem;
+    int nhist = 0;
+    double hist[MP_HIST_MAX] = {0};
+
+    if (st0.flags & ST_OVERFLOW) code = -2;
+    if (!code) {
+        // ---- step 1: binary32 blocked GEPP
+        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
+        t_fac = tm.mark();
+        const DevStatus &st1 = sio.read();
+        if (st1.flags & ST_ZERO_PIVOT) code = -3;
+    }
+    if (!code && (o.flags & 1)) code = -31;
+    if (!code) {
+        // ---- steps 2-3: x0 = LUsolve(fl32(P b))
+        launch_invert_perm(perm, pinv, n, s);
+        launch_permute_demote_rhs<float>(v.B, n, nrhs, pinv, Y, sio.d, s);
+        prof_begin(KC_SOLVE, s);
+        launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 0, ss, s);
+        prof_end(KC_SOLVE, 4.0 * n * n, s);
+        code = -31;
+        for (int it = 0; it <= itermax; ++it) {
+            // ---- step 4 + check: r = b - A x (binary64), norms, verdict; y = fl32(P r)
+            prof_begin(KC_RESIDUAL, s);
+            launch_residual<float>(v.A, v.lda, n, nrhs, v.B, v.X, R, pinv, Y, cte, rs, sio.d, sms, s);
+            prof_end(KC_RESIDUAL, 8.0 * n * n + 8.0 * 4 * n * nrhs, s);
+            const DevStatus &st = sio.read();
+            if (st.flags & ST_NORM_NONFINITE) break;
+            hist[nhist++] = st.ratio;
+            if (st.converged) { *iters = it; code = 0; break; }
+            if (it == itermax) break;
+            // ---- steps 5-7: z = LUsolve(y) (binary32), x += z (binary64)
+            prof_begin(KC_SOLVE, s);
+            launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 1, ss, s);
+            prof_end(KC_SOLVE, 4.0 * n * n, s);
+        }
+        t_ref = tm.mark();
+    }
+    int t_fb = tm.mark();
+    if (code) {
+        *iters = code;
+        *info = fp64_solve(v, n, nrhs, nb, pool, sio, s);
+        t_fb = tm.mark();
+    }
+    finish_copy_out(a, v, s);
+    const int t_end = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = nb; rep->variant = o.variant;
+        rep->anrm = anrm;
+        for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
+        rep->t_total_ms = tm.ms(t0, t_end);
+        rep->t_copy_ms = tm.ms(t0, t_staged);
+        rep->t_demote_ms = tm.ms(t_staged, t_dem);
+        rep->t_factor_ms = (t_fac != t_dem) ? tm.ms(t_dem, t_fac) : 0.0;
+        rep->t_refine_ms = (t_ref != t_dem) ? tm.ms(t_fac, t_ref) : 0.0;
+        rep->t_fallback_ms = code ? tm.ms(t_ref, t_fb) : 0.0;
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        prof_collect(rep);
+    }
+    g_prof.reset(false);
+    return MP_OK;
+}
+
+int dgesv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    if (check_args(a, info)) { if (rep) rep->info = *info; return MP_OK; }
+    if (a.n == 0 || a.nrhs == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int nb = o.nb > 0 ? o.nb : default_nb(a.n);
+    cudaStream_t s = g_stream;
+    configure_mempool_once();
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0);
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    Views v = stage_in(a, pool, s, true);
+    const int t1 = tm.mark();
+    StatusIO sio(pool, s);
+    {   // B finiteness (identity scatter into a scratch vector)
+        int32_t *idp = pool.get<int32_t>(a.n);
+        double *Yd = pool.get<double>((size_t)a.n * a.nrhs);
+        launch_init_perm(idp, a.n, s);
+        launch_permute_demote_rhs<double>(v.B, a.n, a.nrhs, idp, Yd, sio.d, s);
+    }
+    *info = fp64_solve(v, a.n, a.nrhs, nb, pool, sio, s);
+    const DevStatus &st = sio.read();
+    if (*info != -3 && (st.flags & ST_B_NONFINITE)) *info = -5;
+    finish_copy_out(a, v, s);
+    const int t2 = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->info = *info; rep->nb = nb;
+        rep->t_total_ms = tm.ms(t0, t2);
+        rep->t_copy_ms = tm.ms(t0, t1);
+        rep->t_factor_ms = tm.ms(t1, t2);
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        prof_collect(rep);
+    }
+    g_prof.reset(false);
+    return MP_OK;
+}
+
+template <typename T>
+int getrf_impl(int64_t n, const double *A, int64_t lda, T *LU, int32_t *ipiv_out, int *info, const mp_opts *opts)
+{
+    *info = 0;
+    if (n < 0) return *info = -1, MP_OK;
+    if (n > 0 && !A) return *info = -3, MP_OK;
+    if (lda < std::max<int64_t>(1, n)) return *info = -4, MP_OK;
+    if (n > 0 && !LU) return *info = -5, MP_OK;
+    if (n > 0 && !ipiv_out) return *info = -6, MP_OK;
+    if (n == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int nb = o.nb > 0 ? o.nb : default_nb(n);
+    cudaStream_t s = g_stream;
+    configure_mempool_once();
+    g_launches = 0;
+    Pool pool(s);
+    Args a{n, 0, lda, A, nullptr, nullptr};
+    Views v = stage_in(a, pool, s, false);
+    StatusIO sio(pool, s);
+    const int64_t ldw = round_up(n, 64);
+    T *W = pool.get<T>((size_t)n * ldw);
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n);
+    const int sms = num_sms();
+    double *dpart = pool.get<double>((size_t)sms * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    launch_demote_transpose<T>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);
+    const DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) return *info = -3, MP_OK;
+    if (st0.flags & ST_OVERFLOW) return *info = -2, MP_OK;
+    run_factor<T>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
+    const DevStatus &st = sio.read();
+    if (st.flags & ST_ZERO_PIVOT) *info = st.zero_col;
+    // packed factors back to column-major (leading dimension n)
+    const bool lu_dev = is_device_ptr(LU), ip_dev = is_device_ptr(ipiv_out);
+    T *dLU = lu_dev ? LU : pool.get<T>((size_t)n * n);
+    launch_transpose_out<T>(W, ldw, n, dLU, s);
+    if (!lu_dev) MP_CUDA(cudaMemcpyAsync(LU, dLU, (size_t)n * n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaMemcpyAsync(ipiv_out, ipiv, (size_t)n * sizeof(int32_t),
+                            ip_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    return MP_OK;
+}
+
+template <typename F>
+int guarded(F &&f)
+{
+    try {
+        return f();
+    } catch (const CudaError &e) {
+        char buf[512];
+        std::snprintf(buf, sizeof(buf), "CUDA error %d (%s) at driver/kernels line %d: %s", (int)e.err,
+                      cudaGetErrorString(e.err), e.line, e.what);
+        g_err = buf;
+        return e.err == cudaErrorMemoryAllocation ? MP_ERR_NOMEM : MP_ERR_CUDA;
+    } catch (const NoMem &) {
+        g_err = "device workspace allocation failed";
+        return MP_ERR_NOMEM;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return MP_ERR_UNSUPPORTED;
+    } catch (...) {
+        g_err = "unknown internal error";
+        return MP_ERR_INTERNAL;
+    }
+}
+
+}  // namespace
+}  // namespace mp
+
+using namespace mp;
+
+extern "C" {
+
+void mp_default_opts(mp_opts *o)
+{
+    if (!o) return;
+    o->nb = 0;
+    o->itermax = MP_ITERMAX_DEFAULT;
+    o->variant = MP_VARIANT_FFMA;
+    o->flags = 0;
+}
+
+int mp_dsgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *iters,
+                 int *info, const mp_opts *opts, mp_report *rep)
+{
+    if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return dsgesv_impl(Args{n, nrhs, lda, A, B, X}, iters, info, opts, rep); });
+}
+
+int mp_dsgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *iters,
+              int *info)
+{
+    return mp_dsgesv_ex(n, nrhs, A, lda, B, X, iters, info, nullptr, nullptr);
+}
+
+int mp_dgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *info,
+                const mp_opts *opts, mp_report *rep)
+{
+    if (!info) { g_err = "info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return dgesv_impl(Args{n, nrhs, lda, A, B, X}, info, opts, rep); });
+}
+
+int mp_dgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *info)
+{
+    return mp_dgesv_ex(n, nrhs, A, lda, B, X, info, nullptr, nullptr);
+}
+
+int mp_sgetrf(int64_t n, const double *A, int64_t lda, float *LU, int32_t *ipiv, int *info, const mp_opts *opts)
+{
+    if (!info) { g_err = "info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return getrf_impl<float>(n, A, lda, LU, ipiv, info, opts); });
+}
+
+int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv, int *info, const mp_opts *opts)
+{
+    if (!info) { g_err = "info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return getrf_impl<double>(n, A, lda, LU, ipiv, info, opts); });
+}
+
+int mp_set_stream(void *stream)
+{
+    g_stream = static_cast<cudaStream_t>(stream);
+    return MP_OK;
+}
+
+const char *mp_last_error(void) { return g_err.c_str(); }
+
+const char *mp_version(void)
+{
+    return "libmpsolve 0.1 (sm_100a; variants: ffma; blocked right-looking GEPP, row-major working copy)";
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+// internal.h — shared declarations of the sm_100a kernels (K1..K11) and the
+// host driver of libmpsolve.so.  Not part of the public ABI (include/mp_solve.h).
+//
+// Working-copy layout: the binary32 (or, for
+// the binary64 path, binary64) working copy W is ROW-major, n rows x ldw
+// columns, ldw = round_up(n, 64): W[i*ldw + j] = fl(A(i,j)).  Row interchanges
+// are then contiguous 1 KB+ row segments, panel rows are contiguous,
+// and the Schur update C -= L21*U12 reads both operands with unit stride.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mp {
+
+constexpr int kMaxSMs = 256;
+
+// ---------------------------------------------------------------- errors
+struct CudaError {
+    cudaError_t err;
+    const char *what;
+    int line;
+};
+
+#define MP_CUDA(call)                                                         \
+    do {                                                                      \
+        cudaError_t e_ = (call);                                              \
+        if (e_ != cudaSuccess) throw ::mp::CudaError{e_, #call, __LINE__};    \
+    } while (0)
+
+#define MP_LAUNCH_CHECK() MP_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- small helpers
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+
+// Status record written by the device, read by the host once per iteration.
+struct DevStatus {
+    int32_t flags;        // bit0 A non-finite, bit1 demotion overflow, bit2 B non-finite,
+                          // bit3 zero pivot seen, bit4 norms non-finite
+    int32_t zero_col;     // 1-based column of the first exact zero pivot (0 = none)
+    int32_t converged;    // residual check verdict
+    int32_t pad;
+    double anrm2;         // sum of squares of A (binary64)
+    double ratio;         // max_c ||r_c|| / (||x_c|| cte)
+    double rn[16];
+    double xn[16];
+};
+
+enum : int32_t {
+    ST_A_NONFINITE = 1,
+    ST_OVERFLOW = 2,
+    ST_B_NONFINITE = 4,
+    ST_ZERO_PIVOT = 8,
+    ST_NORM_NONFINITE = 16,
+};
+
+// Per-launch counters (how many library kernels ran), read by the report.
+extern thread_local int64_t g_launches;
+
+// Optional per-kernel-class timing (mp_opts.flags bit 1): CUDA events recorded
+// on the launching stream around every launch of a class, summed after the
+// call.  Classes follow DESIGN.md's kernel list.
+enum KClass : int { KC_DEMOTE = 0, KC_PANEL, KC_LASWP, KC_TRSM, KC_GEMM, KC_SOLVE, KC_RESIDUAL, KC_OTHER, KC_COUNT };
+void prof_begin(int cls, cudaStream_t s);
+void prof_end(int cls, double work, cudaStream_t s);   // work: algorithmic flops (or bytes) of the launch
+
+// ---------------------------------------------------------------- K1 demote (k_demote.cu)
+// W[i*ldw + j] = (T)A[i + j*lda] for i,j < n; zero for j in [n, ldw).
+// For T=float also: sum of squares (binary64) into st->anrm2 (deterministic
+// two-level reduction), ST_A_NONFINITE / ST_OVERFLOW flags.
+template <typename T>
+void launch_demote_transpose(const double *A, int64_t lda, int64_t n, T *W, int64_t ldw,
+                             double *partials, unsigned *counter, DevStatus *st, cudaStream_t s);
+
+// LU[i + j*n] = W[i*ldw + j]: packed factors back to the column-major ABI layout.
+template <typename T>
+void launch_transpose_out(const T *W, int64_t ldw, int64_t n, T *LU, cudaStream_t s);
+
+// B non-finite check + y[pinv[i]] = (T)B[i + c*n] (demote + permute the rhs, K6).
+template <typename T>
+void launch_permute_demote_rhs(const double *B, int64_t n, int64_t nrhs, const int32_t *pinv,
+                               T *Y, DevStatus *st, cudaStream_t s);
+
+// ---------------------------------------------------------------- K2 panel (k_panel.cu)
+struct PanelScratch {
+    void *cand_rows;      // [2][kMaxSMs][w] T
+    void *diag_rows;      // [2][w] T
+    double *cand_val;     // [2][kMaxSMs]
+    int32_t *cand_pos;    // [2][kMaxSMs]
+    int32_t *cand_orig;   // [2][kMaxSMs]
+    int32_t *diag_orig;   // [2]
+    unsigned *barrier;    // grid barrier counter (zeroed before each launch)
+    int32_t *pairs;       // [2*w][2] (position, original row)
+    int32_t *npairs;      // 1
+};
+size_t panel_scratch_bytes(int wmax, size_t elem);
+void panel_scratch_carve(PanelScratch &ps, void *base, int wmax, size_t elem);
+
+// Largest leaf width that fits the panel rows [r0, n) in the SMs' shared memory.
+template <typename T>
+int panel_leaf_fits(int64_t m, int w, int num_sms);
+
+// Factor the leaf panel: rows [c0, n), columns [c0, c0+w) of W (GEPP, binary T).
+// Writes ipiv[c0 .. c0+w) (0-based global rows), the (position, origin) pairs
+// of this leaf's row permutation, zero-pivot status.
+template <typename T>
+void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv,
+                       PanelScratch &ps, DevStatus *st, int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- K3 laswp (k_laswp.cu)
+// Apply a (position <- origin row) pair list to columns [c_lo, c_hi) minus
+// [x_lo, x_hi); optionally also perm[pos] <- perm[orig] (perm != nullptr).
+template <typename T>
+void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *npairs, int max_pairs,
+                        int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm,
+                        cudaStream_t s);
+void launch_init_perm(int32_t *perm, int64_t n, cudaStream_t s);
+void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- K4 trsm (k_trsm.cu)
+// U12 <- L11^{-1} A12: rows [r0, r0+w), columns [c_lo, c_hi), L11 = unit lower of W[r0.., r0..].
+template <typename T>
+void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi,
+                            cudaStream_t s);
+
+// ---------------------------------------------------------------- K5 Schur update (k_gemm.cu)
+// C[M x N] -= A[M x K] * B[K x N], all row-major views into W with stride ldw:
+//   A at W[r0*ldw + k0], B at W[k0*ldw + c0], C at W[r0*ldw + c0].
+template <typename T>
+void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                        int64_t K, cudaStream_t s);
+
+// ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
+struct SolveScratch {
+    unsigned *flags;      // [2][nblk] ready flags (forward / backward), zeroed per solve
+    unsigned *tickets;    // [2] dynamic block tickets
+};
+// Forward (unit L) then backward (U) substitution on Y (n x nrhs, T, column-major
+// with ld n) with the packed LU in W; then X (double, ld n) = (mode 0) or += (mode 1) Y.
+template <typename T>
+void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
+                     SolveScratch &ss, cudaStream_t s);
+int solve_block_rows();
+
+// ---------------------------------------------------------------- K8/K10 residual (k_residual.cu)
+// R = B - A X (binary64, original A, column-major), then Y[pinv[i]] = (T)R[i],
+// per-column norms and the B:5 convergence verdict into *st.
+struct ResidualScratch {
+    double *partial;      // [splits][n][nrhs]
+    double *blocksums;    // [nblocks][2*nrhs]
+    unsigned *counter;    // last-block ticket
+};
+int64_t residual_splits(int64_t n, int num_sms);
+size_t residual_partial_elems(int64_t n, int64_t nrhs, int num_sms);
+template <typename T>
+void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,
+                     double *R, const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
+                     int num_sms, cudaStream_t s);
+
+}  // namespace mp

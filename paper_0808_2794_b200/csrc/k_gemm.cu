@@ -1,0 +1,190 @@
+// k_gemm.cu — K5a: trailing (Schur complement) update  A22 <- A22 - L21 * U12.
+//
+// "the only operation with computational complexity of
+// O(n^3) is handled in single precision"; SGETRF's trailing update
+// (P:366).  This is the FFMA variant (binary32 CUDA-core FMAs; the binary64
+// instantiation is the DGEMM of the mp_dgesv path and of the fallback).
+//
+// All three operands are row-major views into the working copy W (stride
+// ldw): L21 rows are K-contiguous, U12 rows are N-contiguous, so both tiles
+// are read with 128-bit unit-stride loads.  Classic register-blocked SGEMM:
+// BM x BN block tile, BK-deep k-slices double-buffered in shared memory
+// (register-staged prefetch of slice t+1 while slice t is consumed), TM x TN
+// micro-tile per thread split in two halves to keep LDS.128 conflict-free.
+// Algorithmic work 2*M*N*K flops; C is read and written once (8 M N bytes).
+#include <algorithm>
+
+#include "internal.h"
+
+namespace mp {
+
+namespace {
+
+template <typename T, int N> struct Vec;
+template <> struct Vec<float, 4> { using type = float4; };
+template <> struct Vec<float, 2> { using type = float2; };
+template <> struct Vec<double, 2> { using type = double2; };
+template <> struct Vec<double, 4> { using type = double4; };
+
+template <typename T, int BM, int BN, int BK, int TM, int TN>
+struct Cfg {
+    static constexpr int NT = (BM / TM) * (BN / TN);
+    static constexpr int A_PER = BM * BK / NT;       // elements of the A slice per thread (along k)
+    static constexpr int B_PER = BK * BN / NT;       // elements of the B slice per thread (along n)
+    static constexpr int A_TPR = BK / A_PER;         // threads per A row
+    static constexpr int B_TPR = BN / B_PER;         // threads per B row
+    static_assert(BK % A_PER == 0 && BN % B_PER == 0, "tile split");
+};
+
+template <typename T, int BM, int BN, int BK, int TM, int TN, bool VEC>
+__global__ void __launch_bounds__(Cfg<T, BM, BN, BK, TM, TN>::NT)
+gemm_update_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                   int64_t K)
+{
+    using C = Cfg<T, BM, BN, BK, TM, TN>;
+    constexpr int NT = C::NT;
+    __shared__ __align__(16) T As[2][BK][BM];
+    __shared__ __align__(16) T Bs[2][BK][BN];
+    const int tid = threadIdx.x;
+    const int64_t bm0 = (int64_t)blockIdx.y * BM, bn0 = (int64_t)blockIdx.x * BN;
+    const T *Ag = W + (r0 + bm0) * ldw + k0;          // L21 block rows
+    const T *Bg = W + k0 * ldw + c0 + bn0;            // U12 block columns
+    T *Cg = W + (r0 + bm0) * ldw + c0 + bn0;
+
+    // loader coordinates
+    const int a_row = tid / C::A_TPR, a_k = (tid % C::A_TPR) * C::A_PER;
+    const int b_k = tid / C::B_TPR, b_n = (tid % C::B_TPR) * C::B_PER;
+    T ra[C::A_PER], rb[C::B_PER];
+
+    auto load_slice = [&](int64_t kk) {
+        const bool arow_ok = bm0 + a_row < M;
+        if (VEC && arow_ok && kk + a_k + C::A_PER <= K) {
+            using V = typename Vec<T, C::A_PER>::type;
+            V v = *reinterpret_cast<const V *>(Ag + a_row * ldw + kk + a_k);
+            const T *pv = reinterpret_cast<const T *>(&v);
+#pragma unroll
+            for (int e = 0; e < C::A_PER; ++e) ra[e] = pv[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < C::A_PER; ++e)
+                ra[e] = (arow_ok && kk + a_k + e < K) ? Ag[a_row * ldw + kk + a_k + e] : T(0);
+        }
+        const bool bk_ok = kk + b_k < K;
+        if (VEC && bk_ok && bn0 + b_n + C::B_PER <= N) {
+            using V = typename Vec<T, C::B_PER>::type;
+            V v = *reinterpret_cast<const V *>(Bg + (kk + b_k) * ldw + b_n);
+            const T *pv = reinterpret_cast<const T *>(&v);
+#pragma unroll
+            for (int e = 0; e < C::B_PER; ++e) rb[e] = pv[e];
+        } else {
+#pragma unroll
+            for (int e = 0; e < C::B_PER; ++e)
+                rb[e] = (bk_ok && bn0 + b_n + e < N) ? Bg[(kk + b_k) * ldw + b_n + e] : T(0);
+        }
+    };
+    auto store_slice = [&](int buf) {
+#pragma unroll
+        for (int e = 0; e < C::A_PER; ++e) As[buf][a_k + e][a_row] = ra[e];
+#pragma unroll
+        for (int e = 0; e < C::B_PER; ++e) Bs[buf][b_k][b_n + e] = rb[e];
+    };
+
+    constexpr int TX = BN / TN;                       // threads along n
+    const int ty = tid / TX, tx = tid % TX;
+    constexpr int HM = TM / 2, HN = TN / 2;
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+
+    const int nslices = (int)ceil_div(K, BK);
+    load_slice(0);
+    store_slice(0);
+    __syncthreads();
+    for (int t = 0; t < nslices; ++t) {
+        const int buf = t & 1;
+        if (t + 1 < nslices) load_slice((int64_t)(t + 1) * BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            T a[TM], b[TN];
+#pragma unroll
+            for (int i = 0; i < HM; ++i) {
+                a[i] = As[buf][kk][ty * HM + i];
+                a[HM + i] = As[buf][kk][BM / 2 + ty * HM + i];
+            }
+#pragma unroll
+            for (int j = 0; j < HN; ++j) {
+                b[j] = Bs[buf][kk][tx * HN + j];
+                b[HN + j] = Bs[buf][kk][BN / 2 + tx * HN + j];
+            }
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        if (t + 1 < nslices) {
+            store_slice(buf ^ 1);
+            __syncthreads();
+        }
+    }
+
+    // epilogue: C <- C - acc
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int row = (i < HM) ? ty * HM + i : BM / 2 + ty * HM + (i - HM);
+        if (bm0 + row >= M) continue;
+        T *crow = Cg + (int64_t)row * ldw;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int col = (h == 0) ? tx * HN : BN / 2 + tx * HN;
+            if (VEC && bn0 + col + HN <= N) {
+                using V = typename Vec<T, HN>::type;
+                V v = *reinterpret_cast<V *>(crow + col);
+                T *pv = reinterpret_cast<T *>(&v);
+#pragma unroll
+                for (int j = 0; j < HN; ++j) pv[j] -= acc[i][h * HN + j];
+                *reinterpret_cast<V *>(crow + col) = v;
+            } else {
+#pragma unroll
+                for (int j = 0; j < HN; ++j)
+                    if (bn0 + col + j < N) crow[col + j] -= acc[i][h * HN + j];
+            }
+        }
+    }
+}
+
+template <typename T, int BM, int BN, int BK, int TM, int TN>
+void launch_tiles(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
+                  cudaStream_t s)
+{
+    using C = Cfg<T, BM, BN, BK, TM, TN>;
+    dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
+    const bool vec = ((uintptr_t)W % 32 == 0) && (ldw % 8 == 0) && (k0 % 4 == 0) && (c0 % 4 == 0);
+    if (vec)
+        gemm_update_kernel<T, BM, BN, BK, TM, TN, true><<<grid, C::NT, 0, s>>>(W, ldw, r0, c0, k0, M, N, K);
+    else
+        gemm_update_kernel<T, BM, BN, BK, TM, TN, false><<<grid, C::NT, 0, s>>>(W, ldw, r0, c0, k0, M, N, K);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
+}  // namespace
+
+template <>
+void launch_gemm_update<float>(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                               int64_t K, cudaStream_t s)
+{
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    launch_tiles<float, 128, 128, 8, 8, 8>(W, ldw, r0, c0, k0, M, N, K, s);
+}
+
+template <>
+void launch_gemm_update<double>(double *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                                int64_t K, cudaStream_t s)
+{
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    launch_tiles<double, 128, 64, 8, 8, 4>(W, ldw, r0, c0, k0, M, N, K, s);
+}
+
+}  // namespace mp

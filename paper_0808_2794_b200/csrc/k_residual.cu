@@ -1,0 +1,216 @@
+// k_residual.cu — K8 + K10: binary64 residual with the original A, the
+// demoted/permuted correction right-hand side, and the convergence test.
+//
+// PAPER.md Alg. 1 step 4: r_k <- b - A x_{k-1} in double precision,
+// "using the original double precision coefficients".  Step 5's
+// right-hand side P r_k is demoted to binary32 here (reading A-10: RN, no
+// scaling) and scattered through pinv, so the solve kernels read it directly.
+// "check convergence" with B:5's test (readings A-1..A-5):
+//   converged  <=>  for all c:  ||r_c||_2 < ||x_c||_2 * cte  or  ||r_c||_2 == 0,
+//   cte = ||A||_F * 2^-53 * sqrt(n); any non-finite norm -> ST_NORM_NONFINITE.
+//
+// HBM-bound: A (8 n^2 bytes, column-major, the caller's layout) is streamed
+// once per iteration with coalesced 128-bit loads; the column range is split
+// over `splits` CTAs per row tile (split-K) and the partial sums are reduced
+// in a fixed order by the finalize kernel (deterministic).
+#include <algorithm>
+
+#include "internal.h"
+
+namespace mp {
+
+namespace {
+
+constexpr int RT = 256;              // threads per CTA (2 rows each)
+constexpr int ROWS = 2 * RT;         // rows per row tile
+constexpr int MAXR = 16;
+constexpr int JU = 8;                // column unroll (loads in flight per thread)
+
+template <bool VEC>
+__global__ void __launch_bounds__(RT)
+residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int nrhs,
+                        const double *__restrict__ X, double *__restrict__ partial, int64_t cols_per_split,
+                        int c_off, int nrhs_total)
+{
+    extern __shared__ __align__(16) double xs[];        // [cols_per_split][MAXR]
+    const int s = blockIdx.y;
+    const int64_t j0 = (int64_t)s * cols_per_split;
+    const int64_t j1 = (n < j0 + cols_per_split) ? n : j0 + cols_per_split;
+    const int64_t i = (int64_t)blockIdx.x * ROWS + 2 * threadIdx.x;
+    for (int64_t idx = threadIdx.x; idx < (j1 - j0) * nrhs; idx += RT) {
+        const int64_t jj = idx / nrhs;
+        const int c = (int)(idx - jj * nrhs);
+        xs[jj * MAXR + c] = X[c * n + j0 + jj];
+    }
+    __syncthreads();
+    double acc0[MAXR], acc1[MAXR];
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
+    const bool r0 = i < n, r1 = i + 1 < n;
+    int64_t j = j0;
+    if (VEC && r1) {
+        for (; j + JU <= j1; j += JU) {
+            double2 a[JU];
+#pragma unroll
+            for (int u = 0; u < JU; ++u) a[u] = __ldcs(reinterpret_cast<const double2 *>(A + (j + u) * lda + i));
+#pragma unroll
+            for (int u = 0; u < JU; ++u) {
+                const double *xj = xs + (j + u - j0) * MAXR;
+#pragma unroll
+                for (int c = 0; c < MAXR; ++c)
+                    if (c < nrhs) {
+                        acc0[c] = fma(a[u].x, xj[c], acc0[c]);
+                        acc1[c] = fma(a[u].y, xj[c], acc1[c]);
+                    }
+            }
+        }
+    }
+    for (; j < j1; ++j) {
+        const double *col = A + j * lda;
+        const double a0 = r0 ? __ldcs(col + i) : 0.0, a1 = r1 ? __ldcs(col + i + 1) : 0.0;
+        const double *xj = xs + (j - j0) * MAXR;
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c)
+            if (c < nrhs) {
+                acc0[c] = fma(a0, xj[c], acc0[c]);
+                acc1[c] = fma(a1, xj[c], acc1[c]);
+            }
+    }
+    double *ps = partial + ((int64_t)s * nrhs_total + c_off) * n;
+#pragma unroll
+    for (int c = 0; c < MAXR; ++c)
+        if (c < nrhs) {
+            if (r0) ps[c * n + i] = acc0[c];
+            if (r1) ps[c * n + i + 1] = acc1[c];
+        }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RT)
+residual_finalize_kernel(int64_t n, int nrhs, int splits, const double *__restrict__ B, const double *__restrict__ X,
+                         const double *__restrict__ partial, double *__restrict__ R, const int32_t *__restrict__ pinv,
+                         T *__restrict__ Y, double cte, double *blocksums, unsigned *counter, DevStatus *st)
+{
+    __shared__ double red[RT / 32][2 * MAXR];
+    __shared__ bool last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = (int64_t)blockIdx.x * RT + threadIdx.x;
+    const int32_t pi = i < n ? pinv[i] : 0;
+    for (int cb = 0; cb < nrhs; cb += MAXR) {
+        const int nc = (nrhs - cb < MAXR) ? (nrhs - cb) : MAXR;
+        for (int cc = 0; cc < nc; ++cc) {
+            const int c = cb + cc;
+            double rr = 0.0, xx = 0.0;
+            if (i < n) {
+                double sum = 0.0;
+                for (int s = 0; s < splits; ++s) sum += partial[((int64_t)s * nrhs + c) * n + i];
+                const double r = B[c * n + i] - sum;
+                R[c * n + i] = r;
+                Y[c * n + pi] = (T)r;                  // y = fl32(P r)   (A-10)
+                const double x = X[c * n + i];
+                rr = r * r;
+                xx = x * x;
+            }
+            for (int o = 16; o; o >>= 1) {
+                rr += __shfl_xor_sync(0xffffffffu, rr, o);
+                xx += __shfl_xor_sync(0xffffffffu, xx, o);
+            }
+            if (lane == 0) { red[warp][2 * cc] = rr; red[warp][2 * cc + 1] = xx; }
+        }
+        __syncthreads();
+        if (threadIdx.x < 2 * nc) {
+            double v = 0.0;
+            for (int w = 0; w < RT / 32; ++w) v += red[w][threadIdx.x];
+            blocksums[(int64_t)blockIdx.x * 2 * nrhs + 2 * cb + threadIdx.x] = v;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    __shared__ int s_conv, s_bad;
+    __shared__ double s_worst;
+    if (threadIdx.x == 0) { s_conv = 1; s_bad = 0; s_worst = 0.0; }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nrhs; c += RT) {     // fixed-order sums over blocks, one column per thread
+        double r2 = 0.0, x2 = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) {
+            r2 += __ldcg(blocksums + (int64_t)b * 2 * nrhs + 2 * c);
+            x2 += __ldcg(blocksums + (int64_t)b * 2 * nrhs + 2 * c + 1);
+        }
+        const double rn = sqrt(r2), xn = sqrt(x2);
+        if (c < MAXR) { st->rn[c] = rn; st->xn[c] = xn; }
+        if (!isfinite(rn) || !isfinite(xn)) { atomicOr(&s_bad, 1); continue; }
+        const double ratio = rn == 0.0 ? 0.0 : rn / (xn * cte);
+        atomicMax(reinterpret_cast<unsigned long long *>(&s_worst), (unsigned long long)__double_as_longlong(ratio));
+        if (!(rn < xn * cte || rn == 0.0)) atomicAnd(&s_conv, 0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int conv = s_conv;
+        if (s_bad) { atomicOr(&st->flags, (int)ST_NORM_NONFINITE); conv = 0; }
+        st->converged = conv;
+        st->ratio = s_worst;                          // non-negative doubles order like their bit patterns
+        *counter = 0u;
+    }
+}
+
+}  // namespace
+
+int64_t residual_splits(int64_t n, int num_sms)
+{
+    const int64_t tiles = ceil_div(n, ROWS);
+    int64_t s = ceil_div((int64_t)num_sms * 8, tiles);
+    s = std::max<int64_t>(1, std::min<int64_t>(s, ceil_div(n, 64)));
+    return s;
+}
+
+size_t residual_partial_elems(int64_t n, int64_t nrhs, int num_sms)
+{
+    return (size_t)residual_splits(n, num_sms) * (size_t)nrhs * (size_t)n;
+}
+
+template <typename T>
+void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,
+                     double *R, const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
+                     int num_sms, cudaStream_t s)
+{
+    const int nr = (int)nrhs;
+    const int64_t splits = residual_splits(n, num_sms);
+    const int64_t cps = ceil_div(n, splits);
+    const int64_t real_splits = ceil_div(n, cps);
+    dim3 g1((unsigned)ceil_div(n, ROWS), (unsigned)real_splits);
+    const size_t smem = (size_t)cps * MAXR * sizeof(double);
+    const bool vec = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
+    if (vec) {
+        if (smem > 48 * 1024)
+            MP_CUDA(cudaFuncSetAttribute(residual_partial_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        for (int c0 = 0; c0 < nr; c0 += MAXR)
+            residual_partial_kernel<true><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
+                                                               rs.partial, cps, c0, nr);
+    } else {
+        if (smem > 48 * 1024)
+            MP_CUDA(cudaFuncSetAttribute(residual_partial_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        for (int c0 = 0; c0 < nr; c0 += MAXR)
+            residual_partial_kernel<false><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
+                                                                rs.partial, cps, c0, nr);
+    }
+    MP_LAUNCH_CHECK();
+    const int g2 = (int)ceil_div(n, RT);
+    residual_finalize_kernel<T><<<g2, RT, 0, s>>>(n, nr, (int)real_splits, B, X, rs.partial, R, pinv, Y, cte,
+                                                  rs.blocksums, rs.counter, st);
+    MP_LAUNCH_CHECK();
+    g_launches += 1 + ceil_div(nr, MAXR);
+}
+
+template void launch_residual<float>(const double *, int64_t, int64_t, int64_t, const double *, const double *,
+                                     double *, const int32_t *, float *, double, ResidualScratch &, DevStatus *, int,
+                                     cudaStream_t);
+
+}  // namespace mp
