@@ -18,6 +18,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <set>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -28,6 +31,33 @@
 namespace mp {
 
 thread_local int64_t g_launches = 0;
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void *, int>, size_t> g_attr_smem;
+std::set<std::pair<const void *, int>> g_attr_cl16;
+}  // namespace
+
+void func_smem_once(const void *fn, size_t bytes)
+{
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t &cur = g_attr_smem[{fn, dev}];
+    if (bytes > cur) {
+        MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        cur = bytes;
+    }
+}
+
+void func_cluster16_once(const void *fn)
+{
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (g_attr_cl16.insert({fn, dev}).second)
+        MP_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
 static thread_local std::string g_err;
 static thread_local cudaStream_t g_stream = nullptr;
 
@@ -165,6 +195,10 @@ struct Timer {
 };
 
 // ------------------------------------------------------------------ blocked GEPP
+// Right-looking blocked LU (SGETRF's structure): for every panel of nb
+// columns — recursive panel factorisation (cluster leaves K2 + in-panel K3/K4/K5),
+// the panel's interchanges applied once to every other column (K3), U12 (K4),
+// Schur update of the trailing matrix (K5).
 template <typename T>
 struct Factor {
     T *W;
@@ -172,19 +206,19 @@ struct Factor {
     int32_t *ipiv, *perm;
     PanelScratch ps;
     DevStatus *st;
-    int sms;
+    int nb;
     cudaStream_t s;
 
-    void leaf(int64_t c0, int w) {
+    void leaf(int64_t c0, int w, int64_t klo, int64_t khi) {
         const double m = (double)(n - c0);
         prof_begin(KC_PANEL, s);
-        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, sms, s);
+        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, s);
         prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, s);
-        // the leaf interchanged full rows inside its own columns; apply the same
-        // interchanges to every other column (left factors and trailing matrix)
-        prof_begin(KC_LASWP, s);
-        launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, 0, n, c0, c0 + w, perm, s);
-        prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
+        if (khi - klo > w) {   // the leaf's interchanges, on the rest of its panel
+            prof_begin(KC_LASWP, s);
+            launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, klo, khi, c0, c0 + w, nullptr, s);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(khi - klo - w) * sizeof(T), s);
+        }
     }
     void trsm(int64_t r0, int w, int64_t c_lo, int64_t c_hi) {
         prof_begin(KC_TRSM, s);
@@ -196,20 +230,29 @@ struct Factor {
         launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
         prof_end(KC_GEMM, 2.0 * M * N * K, s);
     }
-    // recursive panel: columns [c0, c0+w), rows [c0, n)
-    void panel(int64_t c0, int w) {
-        if (w <= 8 || panel_leaf_fits<T>(n - c0, w, sms)) { leaf(c0, w); return; }
-        const int w1 = (int)round_up(w / 2, 8);
-        panel(c0, w1);
+    // recursive panel: columns [c0, c0+w) of the panel [klo, khi), rows [c0, n)
+    void panel(int64_t c0, int w, int64_t klo, int64_t khi) {
+        const int wl = panel_leaf_width<T>(n - c0);
+        if (wl <= 0) throw std::runtime_error("matrix too tall for one panel cluster");
+        if (w <= wl) { leaf(c0, w, klo, khi); return; }
+        int w1 = (int)round_up(w / 2, 8);
+        if (w1 > wl && w1 % wl) w1 = (int)round_up(w1, wl);
+        panel(c0, w1, klo, khi);
         trsm(c0, w1, c0 + w1, c0 + w);
         gemm(c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1);
-        panel(c0 + w1, w - w1);
+        panel(c0 + w1, w - w1, klo, khi);
     }
-    void run(int nb) {
+    void run() {
         launch_init_perm(perm, n, s);
         for (int64_t k = 0; k < n; k += nb) {
             const int w = (int)std::min<int64_t>(nb, n - k);
-            panel(k, w);
+            launch_orig_init(ps.orig, k, n, s);
+            panel(k, w, k, k + w);
+            // the panel's interchanges on every other column (left factors + trailing matrix)
+            launch_emit_pairs(ps.orig, k, n, ps.ppairs, ps.nppairs, s);
+            prof_begin(KC_LASWP, s);
+            launch_laswp_pairs<T>(W, ldw, ps.ppairs, ps.nppairs, 2 * w, 0, n, k, k + w, perm, s);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
             if (k + w < n) {
                 trsm(k, w, k + w, n);                                     // U12 <- L11^-1 A12
                 gemm(k + w, k + w, k, n - k - w, n - k - w, w);           // A22 -= L21 U12
@@ -223,10 +266,13 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
                 cudaStream_t s)
 {
     Factor<T> f;
-    f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.sms = num_sms(); f.s = s;
-    void *scratch = pool.get<unsigned char>(panel_scratch_bytes(nb, sizeof(T)));
-    panel_scratch_carve(f.ps, scratch, nb, sizeof(T));
-    f.run(nb);
+    f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
+    f.ps.orig = pool.get<int32_t>(n);
+    f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
+    f.ps.npairs = pool.get<int32_t>(1);
+    f.ps.ppairs = pool.get<int32_t>(4 * (size_t)nb);
+    f.ps.nppairs = pool.get<int32_t>(1);
+    f.run();
 }
 
 struct Args {
@@ -294,6 +340,12 @@ struct StatusIO {
         MP_CUDA(cudaMemcpyAsync(d, h, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
     }
     ~StatusIO() { cudaFreeHost(h); }
+    void reset() {
+        MP_CUDA(cudaStreamSynchronize(s));
+        std::memset(h, 0, sizeof(DevStatus));
+        h->zero_col = INT_MAX;
+        MP_CUDA(cudaMemcpyAsync(d, h, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
+    }
     const DevStatus &read() {
         MP_CUDA(cudaMemcpyAsync(h, d, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
@@ -311,6 +363,7 @@ int fp64_solve(const Views &v, int64_t n, int64_t nrhs, int nb, Pool &pool, Stat
     double *Y = pool.get<double>((size_t)n * nrhs);
     const int nblk = (int)ceil_div(n, solve_block_rows());
     SolveScratch ss{pool.get<unsigned>(2 * (size_t)nblk), pool.get<unsigned>(2)};
+    sio.reset();                                   // fresh status: the binary32 attempt may have flagged a zero pivot
     launch_demote_transpose<double>(v.A, v.lda, n, W, ldw, nullptr, nullptr, sio.d, s);
     run_factor<double>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
     const DevStatus &st = sio.read();

@@ -55,6 +55,12 @@ enum : int32_t {
     ST_NORM_NONFINITE = 16,
 };
 
+// Raise a kernel's dynamic shared-memory limit / allow non-portable cluster sizes,
+// once per (kernel, device): the attribute calls cost microseconds and must stay off
+// the per-launch path (thousands of launches per factorisation).
+void func_smem_once(const void *fn, size_t bytes);
+void func_cluster16_once(const void *fn);
+
 // Per-launch counters (how many library kernels ran), read by the report.
 extern thread_local int64_t g_launches;
 
@@ -84,29 +90,23 @@ void launch_permute_demote_rhs(const double *B, int64_t n, int64_t nrhs, const i
 
 // ---------------------------------------------------------------- K2 panel (k_panel.cu)
 struct PanelScratch {
-    void *cand_rows;      // [2][kMaxSMs][w] T
-    void *diag_rows;      // [2][w] T
-    double *cand_val;     // [2][kMaxSMs]
-    int32_t *cand_pos;    // [2][kMaxSMs]
-    int32_t *cand_orig;   // [2][kMaxSMs]
-    int32_t *diag_orig;   // [2]
-    unsigned *barrier;    // grid barrier counter (zeroed before each launch)
-    int32_t *pairs;       // [2*w][2] (position, original row)
+    int32_t *orig;        // [n] panel-level origin of the row at each position
+    int32_t *pairs;       // leaf-level (position, origin) pairs [2*nbmax][2]
     int32_t *npairs;      // 1
+    int32_t *ppairs;      // panel-level pairs [2*nbmax][2]
+    int32_t *nppairs;     // 1
 };
-size_t panel_scratch_bytes(int wmax, size_t elem);
-void panel_scratch_carve(PanelScratch &ps, void *base, int wmax, size_t elem);
-
-// Largest leaf width that fits the panel rows [r0, n) in the SMs' shared memory.
+// Widest leaf one thread-block cluster can hold for m = n - c0 rows (0: too tall).
 template <typename T>
-int panel_leaf_fits(int64_t m, int w, int num_sms);
-
-// Factor the leaf panel: rows [c0, n), columns [c0, c0+w) of W (GEPP, binary T).
-// Writes ipiv[c0 .. c0+w) (0-based global rows), the (position, origin) pairs
-// of this leaf's row permutation, zero-pivot status.
+int panel_leaf_width(int64_t m);
+// Factor the leaf rows [c0, n) x columns [c0, c0+w) of W in place (GEPP, binary T).
+// Writes ipiv[c0 .. c0+w) (0-based global rows), updates ps.orig for the rows,
+// and emits the leaf's (position <- position-at-leaf-start) pairs.
 template <typename T>
-void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv,
-                       PanelScratch &ps, DevStatus *st, int num_sms, cudaStream_t s);
+void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
+                       DevStatus *st, cudaStream_t s);
+void launch_orig_init(int32_t *orig, int64_t k, int64_t n, cudaStream_t s);
+void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 laswp (k_laswp.cu)
 // Apply a (position <- origin row) pair list to columns [c_lo, c_hi) minus

@@ -37,7 +37,7 @@ struct Cfg {
 };
 
 template <typename T, int BM, int BN, int BK, int TM, int TN, bool VEC>
-__global__ void __launch_bounds__(Cfg<T, BM, BN, BK, TM, TN>::NT)
+__global__ void __launch_bounds__(Cfg<T, BM, BN, BK, TM, TN>::NT, 2)
 gemm_update_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                    int64_t K)
 {

@@ -74,8 +74,7 @@ void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *
     if (grid == 0) return;
     const size_t smem = std::max<size_t>((size_t)max_pairs * STRIP * sizeof(T), (size_t)max_pairs * 4);
     auto kern = laswp_pairs_kernel<T>;
-    if (smem > 48 * 1024)
-        MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
     kern<<<grid, LT, smem, s>>>(W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm, nstrips);
     MP_LAUNCH_CHECK();
     ++g_launches;

@@ -187,16 +187,12 @@ void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, cons
     const size_t smem = (size_t)cps * MAXR * sizeof(double);
     const bool vec = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
     if (vec) {
-        if (smem > 48 * 1024)
-            MP_CUDA(cudaFuncSetAttribute(residual_partial_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+        if (smem > 48 * 1024) func_smem_once((const void *)residual_partial_kernel<true>, smem);
         for (int c0 = 0; c0 < nr; c0 += MAXR)
             residual_partial_kernel<true><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
                                                                rs.partial, cps, c0, nr);
     } else {
-        if (smem > 48 * 1024)
-            MP_CUDA(cudaFuncSetAttribute(residual_partial_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem));
+        if (smem > 48 * 1024) func_smem_once((const void *)residual_partial_kernel<false>, smem);
         for (int c0 = 0; c0 < nr; c0 += MAXR)
             residual_partial_kernel<false><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
                                                                 rs.partial, cps, c0, nr);

@@ -26,10 +26,10 @@ constexpr int ST = 256;           // threads per CTA
 constexpr int MAXR = 16;          // right-hand sides per launch
 constexpr int LDD = BS + 1;       // smem stride of the transposed diagonal block
 
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p)
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p)
 {
     unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v)
@@ -64,17 +64,41 @@ tri_solve_kernel(const T *__restrict__ W, int64_t ldw, int64_t n, int nrhs, T *Y
     const int64_t i0 = (int64_t)I * BS;
     const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
 
+    // stage the diagonal block transposed (Ld[j][i] = Tri(i0+i, i0+j)) and this block's
+    // right-hand side first: neither depends on other blocks, so this overlaps the waits.
+    // Warp-per-row, lanes along j: coalesced 128 B reads, conflict-free transposed stores.
+    for (int i = warp; i < BS; i += ST / 32) {
+#pragma unroll
+        for (int k = 0; k < BS / 32; ++k) {
+            const int j = lane + 32 * k;
+            Ld[j * LDD + i] = (i < nr && j < nr) ? W[(i0 + i) * ldw + i0 + j] : T(0);
+        }
+    }
+    T rhs[MAXR];
+    {
+        const int rr = tid >> 1;
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c) rhs[c] = (c < nrhs && rr < nr && (tid & 1) == 0) ? Y[c * ldy + i0 + rr] : T(0);
+    }
+
     // ---- off-diagonal GEMV part: 2 threads per row, each half of every tile
     const int r = tid >> 1, half = tid & 1;
     T psum[MAXR];
 #pragma unroll
     for (int c = 0; c < MAXR; ++c) psum[c] = T(0);
-    const int jb_begin = LOWER ? 0 : I + 1, jb_end = LOWER ? I : nblk;
-    for (int J = jb_begin; J < jb_end; ++J) {
+    // visit the off-diagonal blocks in the order they become ready: increasing J for
+    // the forward sweep, DECREASING J for the backward sweep (block nblk-1 is published first)
+    const int ntiles = LOWER ? I : nblk - 1 - I;
+    for (int t = 0; t < ntiles; ++t) {
+        const int J = LOWER ? t : nblk - 1 - t;
         const int64_t j0 = (int64_t)J * BS;
         const int nc = (int)((n - j0 < (int64_t)BS) ? (n - j0) : (int64_t)BS);
-        if (tid == 0)
-            while (ld_acquire_u32(flags + J) == 0u) { }
+        if (tid == 0) {
+            // relaxed polling (an acquire load per poll would invalidate L1 every time),
+            // then one acquire fence once the flag is seen
+            while (ld_relaxed_u32(flags + J) == 0u) { }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
         __syncthreads();
         for (int idx = tid; idx < nc * nrhs; idx += ST) {
             const int j = idx % nc, c = idx / nc;
@@ -115,65 +139,69 @@ tri_solve_kernel(const T *__restrict__ W, int64_t ldw, int64_t n, int nrhs, T *Y
     // combine the two halves; rhs block I minus the off-diagonal sums -> ys[r][c]
 #pragma unroll
     for (int c = 0; c < MAXR; ++c) psum[c] += __shfl_xor_sync(0xffffffffu, psum[c], 1);
-    if (half == 0 && r < nr)
-        for (int c = 0; c < nrhs; ++c) ys[r * MAXR + c] = Y[c * ldy + i0 + r] - psum[c];
-    // stage the diagonal block transposed: Ld[j][i] = Tri(i0+i, i0+j)
-    for (int idx = tid; idx < nr * nr; idx += ST) {
-        const int i = idx / nr, j = idx - i * nr;
-        Ld[j * LDD + i] = W[(i0 + i) * ldw + i0 + j];
+    if (half == 0 && r < nr) {
+#pragma unroll
+        for (int c = 0; c < MAXR; ++c)
+            if (c < nrhs) ys[r * MAXR + c] = rhs[c] - psum[c];
     }
     __syncthreads();
 
-    // ---- substitution on the diagonal block: warp w handles rhs c = w, w+8
-    for (int c = warp; c < nrhs; c += ST / 32) {
-        T xr[BS / 32];
+    // ---- substitution on the diagonal block, in 32-row sub-blocks (forward: top-down,
+    //      backward: bottom-up).  The 32 x 32 triangle: lane i keeps row i of the triangle in
+    //      registers and its rhs b_i; a fully unrolled chain x_j = shfl(b, j), b_i -= t_ij x_j
+    //      (one warp per right-hand side).  The rows of the block not yet solved then get the
+    //      sub-block's contribution from all 256 threads.
+#pragma unroll 1
+    for (int sbi = 0; sbi < BS / 32; ++sbi) {
+        const int sb = LOWER ? sbi : BS / 32 - 1 - sbi;
+        const int s0 = sb * 32;
+        if (s0 >= nr) continue;
+        const int i = s0 + lane;                           // this lane's row
+        for (int c = warp; c < nrhs; c += ST / 32) {
+            T trow[32];
 #pragma unroll
-        for (int q = 0; q < BS / 32; ++q) {
-            const int i = lane + 32 * q;
-            xr[q] = i < nr ? ys[i * MAXR + c] : T(0);
-        }
-        if (LOWER) {
+            for (int j = 0; j < 32; ++j) trow[j] = Ld[(s0 + j) * LDD + i];
+            T b = i < nr ? ys[i * MAXR + c] : T(0);
+            if (LOWER) {
 #pragma unroll
-            for (int q = 0; q < BS / 32; ++q) {
-                for (int jj = 0; jj < 32; ++jj) {
-                    const int j = q * 32 + jj;
-                    if (j >= nr) break;
-                    const T xj = __shfl_sync(0xffffffffu, xr[q], jj);
-                    const T *lj = Ld + j * LDD;
+                for (int j = 0; j < 32; ++j) {
+                    const T xj = __shfl_sync(0xffffffffu, b, j);
+                    if (lane > j && s0 + j < nr) b = fma(-trow[j], xj, b);
+                }
+            } else {
 #pragma unroll
-                    for (int qq = q; qq < BS / 32; ++qq) {
-                        const int i = lane + 32 * qq;
-                        if (i > j) xr[qq] = fma(-lj[i], xj, xr[qq]);
+                for (int j = 31; j >= 0; --j) {
+                    if (s0 + j < nr) {
+                        if (lane == j) b = b / trow[j];        // U(j, j): non-unit diagonal
+                        const T xj = __shfl_sync(0xffffffffu, b, j);
+                        if (lane < j) b = fma(-trow[j], xj, b);
                     }
                 }
             }
-        } else {
-#pragma unroll
-            for (int q = BS / 32 - 1; q >= 0; --q) {
-                for (int jj = 31; jj >= 0; --jj) {
-                    const int j = q * 32 + jj;
-                    if (j >= nr) continue;
-                    const T *uj = Ld + j * LDD;
-                    if (lane == jj) xr[q] = xr[q] / uj[j];
-                    const T xj = __shfl_sync(0xffffffffu, xr[q], jj);
-#pragma unroll
-                    for (int qq = 0; qq <= q; ++qq) {
-                        const int i = lane + 32 * qq;
-                        if (i < j) xr[qq] = fma(-uj[i], xj, xr[qq]);
-                    }
-                }
-            }
+            if (i < nr) ys[i * MAXR + c] = b;
         }
-#pragma unroll
-        for (int q = 0; q < BS / 32; ++q) {
-            const int i = lane + 32 * q;
-            if (i < nr) {
-                Y[c * ldy + i0 + i] = xr[q];
-                if (!LOWER) {
-                    double *xp = X + c * ldy + i0 + i;
-                    *xp = accumulate ? *xp + (double)xr[q] : (double)xr[q];   // step 7 (binary64)
-                }
-            }
+        __syncthreads();
+        // contribution of the 32 solved rows to the block rows still to be solved
+        const int rlo = LOWER ? s0 + 32 : 0, rhi = LOWER ? nr : s0;
+        const int nrem = rhi > rlo ? rhi - rlo : 0;
+        for (int idx = tid; idx < nrem * nrhs; idx += ST) {
+            const int r = rlo + idx % nrem, c = idx / nrem;
+            T acc = ys[r * MAXR + c];
+#pragma unroll 8
+            for (int j = 0; j < 32; ++j)
+                if (s0 + j < nr) acc = fma(-Ld[(s0 + j) * LDD + r], ys[(s0 + j) * MAXR + c], acc);
+            ys[r * MAXR + c] = acc;
+        }
+        __syncthreads();
+    }
+    // publish the solved block (and, backward, x += z in binary64: step 7)
+    for (int idx = tid; idx < nr * nrhs; idx += ST) {
+        const int r = idx % nr, c = idx / nr;
+        const T v = ys[r * MAXR + c];
+        Y[c * ldy + i0 + r] = v;
+        if (!LOWER) {
+            double *xp = X + c * ldy + i0 + r;
+            *xp = accumulate ? *xp + (double)v : (double)v;
         }
     }
     __syncthreads();
@@ -198,8 +226,8 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     const size_t smem = tri_smem<T>();
     auto kl = tri_solve_kernel<T, true>;
     auto ku = tri_solve_kernel<T, false>;
-    MP_CUDA(cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    MP_CUDA(cudaFuncSetAttribute(ku, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    func_smem_once((const void *)kl, smem);
+    func_smem_once((const void *)ku, smem);
     for (int64_t c0 = 0; c0 < nrhs; c0 += MAXR) {
         const int nc = (int)std::min<int64_t>(MAXR, nrhs - c0);
         MP_CUDA(cudaMemsetAsync(ss.flags, 0, sizeof(unsigned) * (2 * (size_t)nblk), s));

