@@ -167,7 +167,8 @@ def main():
 
     from paper_0808_2794_b200 import binding as mp
     variant = mp.MP_VARIANT_FFMA if args.variant == "ffma" else mp.MP_VARIANT_3XTF32
-    opts = mp.make_opts(nb=args.nb, variant=variant, flags=2)     # bit 1: per-kernel-class event timing
+    # bit 1: per-kernel-class CUDA events around every launch; bit 2: resolved after the timed region
+    opts = mp.make_opts(nb=args.nb, variant=variant, flags=2 | 4)
     n, nrhs = args.n, args.nrhs
 
     # inputs: one independent system per rank (weak scaling; replicas until the 1D block-cyclic path lands)
@@ -188,16 +189,20 @@ def main():
     for _ in range(args.warmup):
         it, info, rep = solve()
     assert info == 0 and it >= 0, (it, info)
+    mp.mp_profile_collect()                                         # drop the warm-up records
 
     stream = torch.cuda.current_stream(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = []
     barrier()
     torch.cuda.synchronize()
+    walls = []
     with ClockSampler(dev.index) as clk:
         e0.record(stream)
         for _ in range(args.steps):
+            w0 = time.perf_counter()
             reps.append(solve())
+            walls.append(time.perf_counter() - w0)
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -211,13 +216,8 @@ def main():
     iters = [r[0] for r in reps]
 
     # per-kernel-class breakdown over the timed region (CUDA events on the launching stream)
-    kern = {}
-    launches = 0
-    for _, _, rep in reps:
-        launches += rep.kernel_launches
-        for name, d in rep.kernels().items():
-            k = kern.setdefault(name, {"ms": 0.0, "work": 0.0, "launches": 0})
-            k["ms"] += d["ms"]; k["work"] += d["work"]; k["launches"] += d["launches"]
+    kern = mp.mp_profile_collect().kernels()
+    launches = sum(r[2].kernel_launches for r in reps)
     pk, pk_src = peaks()
     sm_max = pk.get("sm_max_mhz", 1965.0)
     ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12           # TFLOP/s, FP32 FMA lanes x clock
@@ -298,7 +298,12 @@ def main():
                "speedup_vs_fp64": round(fp64_ms / ms_step, 3) if fp64_ms else None,
                "fp64_ms_per_step": round(fp64_ms, 3) if fp64_ms else None,
                "e2e": e2e, "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches}
+               "clocks": clk.summary(), "gpu_launches": launches,
+               "phases_ms": {"wall": round(1e3 * sum(walls) / len(walls), 3),
+                             "call_device": round(sum(r[2].t_total_ms for r in reps) / len(reps), 3),
+                             "demote": round(sum(r[2].t_demote_ms for r in reps) / len(reps), 3),
+                             "factor": round(sum(r[2].t_factor_ms for r in reps) / len(reps), 3),
+                             "refine": round(sum(r[2].t_refine_ms for r in reps) / len(reps), 3)}}
         print(json.dumps(out), flush=True)
     if dist is not None:
         dist.destroy_process_group()

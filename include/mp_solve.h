@@ -79,7 +79,9 @@ typedef struct mp_opts {
     int32_t itermax;   /* refinement cap; 0 = MP_ITERMAX_DEFAULT */
     int32_t variant;   /* MP_VARIANT_* (default MP_VARIANT_FFMA) */
     int32_t flags;     /* bit 0: force the binary64 fallback path after the binary32 factorisation (testing);
-                          bit 1: per-kernel-class CUDA-event timing into mp_report.k_* (measurement) */
+                          bit 1: per-kernel-class CUDA-event timing into mp_report.k_* (measurement);
+                          bit 2: with bit 1, keep the events of successive calls and resolve them only in
+                                 mp_profile_collect() (keeps event queries out of timed loops) */
 } mp_opts;
 
 #define MP_HIST_MAX 64
@@ -151,6 +153,11 @@ int mp_sgetrf(int64_t n, const double *A, int64_t lda, float *LU, int32_t *ipiv,
 /* Same in binary64 (the fallback / mp_dgesv factorisation). */
 int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv,
               int *info, const mp_opts *opts);
+
+/* Resolve the per-launch events recorded by calls made with opts.flags = 2|4 since the
+ * last collection: fills rep->k_ms / k_work / k_launches (summed over those calls, all
+ * other fields untouched) and clears the records.  Synchronises the device. */
+int mp_profile_collect(mp_report *rep);
 
 /* Use this CUDA stream (a cudaStream_t, NULL = the legacy default stream) for
  * all subsequent library work on the calling thread. */

@@ -66,12 +66,15 @@ lib.mp_dgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi]
 lib.mp_dgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
 lib.mp_sgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_dgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_kernel_schur_update.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_set_stream.argtypes = [_p]
+lib.mp_profile_collect.argtypes = [ctypes.POINTER(Report)]
 lib.mp_last_error.restype = ctypes.c_char_p
 lib.mp_version.restype = ctypes.c_char_p
 
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
-            "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version")
+            "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
+            "mp_profile_collect")
 
 
 def mp_version() -> str:
@@ -197,6 +200,21 @@ def mp_sgetrf(A, opts: Opts | None = None):
 
 def mp_dgetrf(A, opts: Opts | None = None):
     return _getrf(lib.mp_dgetrf, np.float64, A, opts)
+
+
+def mp_kernel_schur_update(W, r0: int, c0: int, k0: int, M: int, N: int, K: int, variant: int = MP_VARIANT_FFMA):
+    """K5 alone on a row-major float32 CUDA tensor W (in place): W[r0:r0+M, c0:c0+N] -= W[r0:, k0:k0+K] @ W[k0:k0+K, c0:]."""
+    if not (_is_torch(W) and W.is_cuda and W.element_size() == 4 and W.stride(1) == 1):
+        raise TypeError("W must be a row-major float32 CUDA tensor")
+    lib.mp_set_stream(_stream_of(W))
+    _check(lib.mp_kernel_schur_update(W.data_ptr(), W.stride(0), r0, c0, k0, M, N, K, variant))
+
+
+def mp_profile_collect() -> Report:
+    """Per-kernel-class totals of the calls made with flags 2|4 since the last collection."""
+    rep = Report()
+    _check(lib.mp_profile_collect(ctypes.byref(rep)))
+    return rep
 
 
 def make_opts(nb: int = 0, itermax: int = 30, variant: int = MP_VARIANT_FFMA, flags: int = 0) -> Opts:

@@ -17,6 +17,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -26,6 +27,7 @@
 #include <vector>
 
 #include "../../include/mp_solve.h"
+#include "../../include/mp_kernels.h"
 #include "internal.h"
 
 namespace mp {
@@ -80,7 +82,12 @@ struct ProfState {
         }
         return (int)used++;
     }
-    void reset(bool enable) { on = enable; used = 0; recs.clear(); }
+    bool deferred = false;       // keep records across calls until mp_profile_collect()
+    void reset(bool enable, bool defer) {
+        on = enable;
+        if (!(deferred && defer)) { used = 0; recs.clear(); }
+        deferred = defer;
+    }
 };
 thread_local ProfState g_prof;
 }  // namespace
@@ -103,7 +110,21 @@ void prof_end(int cls, double work, cudaStream_t s)
 
 static void prof_collect(mp_report *rep)
 {
-    if (!g_prof.on || !rep) return;
+    if (!rep || g_prof.recs.empty()) return;
+    if (const char *path = std::getenv("MP_TIMELINE")) {        // debug: per-launch device timeline
+        if (FILE *f = std::fopen(path, "a")) {
+            static const char *names[] = {"demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "other"};
+            std::fprintf(f, "# call\n");
+            for (const ProfRec &r : g_prof.recs) {
+                float t0 = 0.f, t1 = 0.f;
+                cudaEventElapsedTime(&t0, g_prof.ev[g_prof.recs[0].a], g_prof.ev[r.a]);
+                cudaEventElapsedTime(&t1, g_prof.ev[g_prof.recs[0].a], g_prof.ev[r.b]);
+                std::fprintf(f, "%s %.4f %.4f\n", names[r.cls], t0, t1);
+            }
+            std::fclose(f);
+        }
+        cudaGetLastError();
+    }
     for (const ProfRec &r : g_prof.recs) {
         float t = 0.f;
         if (cudaEventElapsedTime(&t, g_prof.ev[r.a], g_prof.ev[r.b]) != cudaSuccess) { cudaGetLastError(); t = 0.f; }
@@ -179,13 +200,18 @@ int num_sms()
 int default_nb(int64_t n) { return n <= 1024 ? 64 : (n <= 4096 ? 128 : 256); }
 
 struct Timer {
-    cudaEvent_t e[12];
+    cudaEvent_t *e;
     int k = 0;
     cudaStream_t s;
     explicit Timer(cudaStream_t st) : s(st) {
-        for (auto &x : e) MP_CUDA(cudaEventCreate(&x));
+        static thread_local cudaEvent_t pool[12];
+        static thread_local bool made = false;
+        if (!made) {
+            for (auto &x : pool) MP_CUDA(cudaEventCreate(&x));
+            made = true;
+        }
+        e = pool;
     }
-    ~Timer() { for (auto &x : e) cudaEventDestroy(x); }
     int mark() { MP_CUDA(cudaEventRecord(e[k], s)); return k++; }
     double ms(int a, int b) {
         float t = 0.f;
@@ -207,6 +233,9 @@ struct Factor {
     PanelScratch ps;
     DevStatus *st;
     int nb;
+    int variant = MP_VARIANT_FFMA;
+    float *tf32 = nullptr;     // 3xTF32 split scratch (variant 1)
+    int sms = 148;
     cudaStream_t s;
 
     void leaf(int64_t c0, int w, int64_t klo, int64_t khi) {
@@ -225,9 +254,16 @@ struct Factor {
         launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, s);
         prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), s);
     }
-    void gemm(int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K) {
+    void gemm(int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool trailing = false) {
         prof_begin(KC_GEMM, s);
-        launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+        if constexpr (sizeof(T) == 4) {
+            if (trailing && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, tf32, sms, s);
+            else
+                launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+        } else {
+            launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+        }
         prof_end(KC_GEMM, 2.0 * M * N * K, s);
     }
     // recursive panel: columns [c0, c0+w) of the panel [klo, khi), rows [c0, n)
@@ -255,7 +291,7 @@ struct Factor {
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
             if (k + w < n) {
                 trsm(k, w, k + w, n);                                     // U12 <- L11^-1 A12
-                gemm(k + w, k + w, k, n - k - w, n - k - w, w);           // A22 -= L21 U12
+                gemm(k + w, k + w, k, n - k - w, n - k - w, w, true);     // A22 -= L21 U12
             }
         }
     }
@@ -263,10 +299,13 @@ struct Factor {
 
 template <typename T>
 void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
-                cudaStream_t s)
+                cudaStream_t s, int variant = MP_VARIANT_FFMA)
 {
     Factor<T> f;
     f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
+    f.sms = num_sms();
+    f.variant = variant;
+    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) f.tf32 = pool.get<float>(tf32_scratch_floats(n, nb));
     f.ps.orig = pool.get<int32_t>(n);
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
@@ -330,16 +369,17 @@ int check_args(const Args &a, int *info)
 
 struct StatusIO {
     DevStatus *d;
-    DevStatus *h;   // pinned
+    DevStatus *h;   // pinned, allocated once per thread (cudaFreeHost would synchronise the device)
     cudaStream_t s;
     StatusIO(Pool &pool, cudaStream_t st) : s(st) {
+        static thread_local DevStatus *pinned = nullptr;
+        if (!pinned) MP_CUDA(cudaMallocHost(&pinned, sizeof(DevStatus)));
+        h = pinned;
         d = pool.get<DevStatus>(1);
-        MP_CUDA(cudaMallocHost(&h, sizeof(DevStatus)));
         std::memset(h, 0, sizeof(DevStatus));
         h->zero_col = INT_MAX;
         MP_CUDA(cudaMemcpyAsync(d, h, sizeof(DevStatus), cudaMemcpyHostToDevice, s));
     }
-    ~StatusIO() { cudaFreeHost(h); }
     void reset() {
         MP_CUDA(cudaStreamSynchronize(s));
         std::memset(h, 0, sizeof(DevStatus));
@@ -394,12 +434,12 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     if (opts) o = *opts;
     const int nb = o.nb > 0 ? o.nb : default_nb(a.n);
     const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
-    if (o.variant != MP_VARIANT_FFMA) throw std::runtime_error("variant not available in this build");
+    if (o.variant != MP_VARIANT_FFMA && o.variant != MP_VARIANT_3XTF32) throw std::runtime_error("unknown variant");
     const int64_t n = a.n, nrhs = a.nrhs;
     cudaStream_t s = g_stream;
     configure_mempool_once();
     g_launches = 0;
-    g_prof.reset((o.flags & 2) != 0);
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
     Timer tm(s);
     const int t0 = tm.mark();
 
@@ -444,7 +484,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     if (st0.flags & ST_OVERFLOW) code = -2;
     if (!code) {
         // ---- step 1: binary32 blocked GEPP
-        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
+        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant);
         t_fac = tm.mark();
         const DevStatus &st1 = sio.read();
         if (st1.flags & ST_ZERO_PIVOT) code = -3;
@@ -496,9 +536,10 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         rep->t_fallback_ms = code ? tm.ms(t_ref, t_fb) : 0.0;
         rep->workspace_bytes = pool.bytes;
         rep->kernel_launches = g_launches;
-        prof_collect(rep);
+        if (!g_prof.deferred) prof_collect(rep);
     }
-    g_prof.reset(false);
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
     return MP_OK;
 }
 
@@ -515,7 +556,7 @@ int dgesv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
     cudaStream_t s = g_stream;
     configure_mempool_once();
     g_launches = 0;
-    g_prof.reset((o.flags & 2) != 0);
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
     Timer tm(s);
     const int t0 = tm.mark();
     Pool pool(s);
@@ -541,9 +582,10 @@ int dgesv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
         rep->t_factor_ms = tm.ms(t1, t2);
         rep->workspace_bytes = pool.bytes;
         rep->kernel_launches = g_launches;
-        prof_collect(rep);
+        if (!g_prof.deferred) prof_collect(rep);
     }
-    g_prof.reset(false);
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
     return MP_OK;
 }
 
@@ -579,7 +621,7 @@ int getrf_impl(int64_t n, const double *A, int64_t lda, T *LU, int32_t *ipiv_out
     const DevStatus st0 = sio.read();
     if (st0.flags & ST_A_NONFINITE) return *info = -3, MP_OK;
     if (st0.flags & ST_OVERFLOW) return *info = -2, MP_OK;
-    run_factor<T>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
+    run_factor<T>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, sizeof(T) == 4 ? o.variant : MP_VARIANT_FFMA);
     const DevStatus &st = sio.read();
     if (st.flags & ST_ZERO_PIVOT) *info = st.zero_col;
     // packed factors back to column-major (leading dimension n)
@@ -669,6 +711,37 @@ int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv
     return guarded([&] { return getrf_impl<double>(n, A, lda, LU, ipiv, info, opts); });
 }
 
+int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                           int64_t K, int variant)
+{
+    return guarded([&] {
+        cudaStream_t s = g_stream;
+        if (variant == MP_VARIANT_3XTF32) {
+            float *scratch = nullptr;
+            const size_t bytes = ((size_t)2 * M * round_up(K, 4) + (size_t)2 * N * round_up(K, 4) + 4096) * 4;
+            MP_CUDA(cudaMallocAsync((void **)&scratch, bytes, s));
+            launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, num_sms(), s);
+            MP_CUDA(cudaFreeAsync(scratch, s));
+        } else {
+            launch_gemm_update<float>(W, ldw, r0, c0, k0, M, N, K, s);
+        }
+        MP_CUDA(cudaStreamSynchronize(s));
+        return MP_OK;
+    });
+}
+
+int mp_profile_collect(mp_report *rep)
+{
+    return guarded([&] {
+        if (!rep) return MP_OK;
+        for (int i = 0; i < 8; ++i) { rep->k_ms[i] = 0; rep->k_work[i] = 0; rep->k_launches[i] = 0; }
+        prof_collect(rep);
+        g_prof.deferred = false;
+        g_prof.reset(false, false);
+        return MP_OK;
+    });
+}
+
 int mp_set_stream(void *stream)
 {
     g_stream = static_cast<cudaStream_t>(stream);
@@ -679,7 +752,8 @@ const char *mp_last_error(void) { return g_err.c_str(); }
 
 const char *mp_version(void)
 {
-    return "libmpsolve 0.1 (sm_100a; variants: ffma; blocked right-looking GEPP, row-major working copy)";
+    return "libmpsolve 0.2 (sm_100a; variants: ffma, 3xtf32-tcgen05; blocked right-looking GEPP, cluster panel, "
+           "row-major working copy)";
 }
 
 }  // extern "C"

@@ -131,6 +131,12 @@ template <typename T>
 void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                         int64_t K, cudaStream_t s);
 
+// 3xTF32 tcgen05 variant (k_gemm_tf32.cu): same operation, binary32 W; scratch holds the
+// hi/lo splits of L21 and U12^T (tf32_scratch_floats(n, nb) floats).
+size_t tf32_scratch_floats(int64_t n, int nbmax);
+void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s);
+
 // ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
 struct SolveScratch {
     unsigned *flags;      // [2][nblk] ready flags (forward / backward), zeroed per solve

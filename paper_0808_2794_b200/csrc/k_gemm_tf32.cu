@@ -1,0 +1,355 @@
+// k_gemm_tf32.cu — K5b: the trailing (Schur complement) update A22 <- A22 - L21 U12
+// on the 5th-generation tensor cores, 3xTF32 (B:5's second variant).
+//
+// the O(n^3) step is the one that runs in single precision.
+// Every operand x is split x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi);
+// the product L21 U12 is formed as Lhi Uhi + Lhi Ulo + Llo Uhi with FP32 accumulation
+// in TMEM (the lo*lo term, ~2^-22 relative, is dropped), which keeps the update at
+// binary32-level accuracy so refinement still reaches the binary64 criterion.
+//
+// Orientation: D^T = U12^T L21^T.  The MMA's M dimension (TMEM lanes) runs over the
+// COLUMNS j of the row-major trailing matrix and its N dimension over the ROWS i, so in
+// the epilogue each thread owns one column and a warp reads / writes 128 contiguous
+// bytes per row: the read-modify-write of C is fully coalesced.
+//
+// Kernel structure (persistent, one CTA per SM, 256 threads):
+//   warp 0     TMA producer: per 32-deep K chunk, 4 boxes (Uhi, Ulo 128x32; Lhi, Llo 256x32)
+//              SWIZZLE_128B into a 2-stage shared-memory ring, mbarrier expect_tx
+//   warp 1     MMA issuer (one thread): 4 k-steps x 3 tcgen05.mma.cta_group::1.kind::tf32
+//              (M=128, N=256, K=8) per chunk, tcgen05.commit -> ring slot free / accumulator full
+//   warp 2     TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7 epilogue: tcgen05.ld 32x32b.x32 -> C -= D (coalesced RMW), accumulator free
+// Two accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+
+#include "internal.h"
+
+namespace mp {
+
+namespace {
+
+constexpr int TM_COLS = 128;      // C columns per tile (MMA M, TMEM lanes)
+constexpr int TM_ROWS = 256;      // C rows per tile (MMA N)
+constexpr int KC = 32;            // K chunk: 32 tf32 = 128 B rows (one SWIZZLE_128B atom)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = TM_COLS * KC * 4;     // 16 KB
+constexpr int B_BYTES = TM_ROWS * KC * 4;     // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 96 KB
+constexpr int GT = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major operand, SWIZZLE_128B, 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr)
+{
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFFu);          // start address
+    d |= (uint64_t)1u << 16;                          // leading byte offset (unused for SW128 K-major)
+    d |= (uint64_t)(1024u >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+    d |= (uint64_t)1u << 46;                          // descriptor version (sm_100)
+    d |= (uint64_t)2u << 61;                          // layout: SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: kind::tf32, D fp32, A/B tf32 K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TM_ROWS >> 3) << 17) |
+                            ((uint32_t)(TM_COLS >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(GT, 1)
+gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_constant__ CUtensorMap tmUl,
+                   const __grid_constant__ CUtensorMap tmLh, const __grid_constant__ CUtensorMap tmLl,
+                   float *__restrict__ C, int64_t ldc, int M, int N, int K)
+{
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte aligned ring (SWIZZLE_128B atoms)
+    unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base_sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles_n = (N + TM_COLS - 1) / TM_COLS, tiles_m = (M + TM_ROWS - 1) / TM_ROWS;
+    const int ntiles = tiles_n * tiles_m;
+    const int nk = (K + KC - 1) / KC;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = tmem_base_sh;
+
+    if (warp == 0) {
+        // ================= TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int tn = t % tiles_n, tm = t / tiles_n;
+                for (int kc = 0; kc < nk; ++kc) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    unsigned char *st = smem + stage * STAGE_BYTES;
+                    mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+                    tma_load_2d(st, &tmUh, &full_bar[stage], kc * KC, tn * TM_COLS);
+                    tma_load_2d(st + A_BYTES, &tmUl, &full_bar[stage], kc * KC, tn * TM_COLS);
+                    tma_load_2d(st + 2 * A_BYTES, &tmLh, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmLl, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ================= MMA issuer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t acc_phase[2] = {0, 0};
+            int a = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(&acc_empty[a], acc_phase[a] ^ 1);           // epilogue drained this accumulator
+                tc_fence_after();
+                const uint32_t tacc = tmem_base + (uint32_t)(a * TM_ROWS);
+                for (int kc = 0; kc < nk; ++kc) {
+                    mbar_wait(&full_bar[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + stage * STAGE_BYTES);
+                    const uint32_t sAh = sa, sAl = sa + A_BYTES, sBh = sa + 2 * A_BYTES, sBl = sa + 2 * A_BYTES + B_BYTES;
+#pragma unroll
+                    for (int ks = 0; ks < KC / 8; ++ks) {
+                        const uint32_t off = ks * 32;                  // 8 tf32 = 32 B along the swizzled row
+                        const uint64_t dAh = umma_desc_sw128(sAh + off), dAl = umma_desc_sw128(sAl + off);
+                        const uint64_t dBh = umma_desc_sw128(sBh + off), dBl = umma_desc_sw128(sBl + off);
+                        umma_tf32(tacc, dAl, dBh, (kc | ks) ? 1u : 0u);  // small terms first
+                        umma_tf32(tacc, dAh, dBl, 1u);
+                        umma_tf32(tacc, dAh, dBh, 1u);
+                    }
+                    umma_commit(&empty_bar[stage]);                    // ring slot free when these MMAs finish
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                umma_commit(&acc_full[a]);                             // accumulator ready for the epilogue
+                acc_phase[a] ^= 1;
+                a ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ================= epilogue: C[i][j] -= D^T[j][i]
+        const int ew = warp - 4;                                       // TMEM lanes 32*ew .. 32*ew+31
+        uint32_t acc_phase[2] = {0, 0};
+        int a = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int tn = t % tiles_n, tm = t / tiles_n;
+            const int j = tn * TM_COLS + ew * 32 + lane;
+            mbar_wait(&acc_full[a], acc_phase[a]);
+            acc_phase[a] ^= 1;
+            tc_fence_after();
+            const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(a * TM_ROWS);
+            const int i0 = tm * TM_ROWS;
+            for (int r0 = 0; r0 < TM_ROWS; r0 += 32) {
+                float v[32];
+                tmem_ld32(tacc + (uint32_t)r0, v);
+                if (j < N) {
+                    float c[32];
+#pragma unroll
+                    for (int rr = 0; rr < 32; ++rr) {
+                        const int i = i0 + r0 + rr;
+                        c[rr] = i < M ? __ldcs(C + (int64_t)i * ldc + j) : 0.f;
+                    }
+#pragma unroll
+                    for (int rr = 0; rr < 32; ++rr) {
+                        const int i = i0 + r0 + rr;
+                        if (i < M) __stcs(C + (int64_t)i * ldc + j, c[rr] - v[rr]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[a]);
+            a ^= 1;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
+// ---- split: Lh/Ll[i][k] = split(L21(i, k)),  Uh/Ul[j][k] = split(U12(k, j)) (transposed)
+__device__ __forceinline__ float rna_tf32(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+__global__ void split_rows_kernel(const float *__restrict__ W, int64_t ldw, int64_t r0, int64_t k0, int M, int K,
+                                  float *__restrict__ hi, float *__restrict__ lo, int kp)
+{
+    const int64_t tot = (int64_t)M * kp;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / kp;
+        const int k = (int)(t - i * kp);
+        const float x = k < K ? W[(r0 + i) * ldw + k0 + k] : 0.f;
+        const float h = rna_tf32(x);
+        hi[t] = h;
+        lo[t] = rna_tf32(x - h);
+    }
+}
+
+__global__ void split_cols_T_kernel(const float *__restrict__ W, int64_t ldw, int64_t k0, int64_t c0, int N, int K,
+                                    float *__restrict__ hi, float *__restrict__ lo, int kp)
+{
+    __shared__ float tile[32][33];
+    const int jb = blockIdx.x * 32, kb = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {               // read U12(kb + r, jb + tx): coalesced
+        const int k = kb + r, j = jb + threadIdx.x;
+        tile[r][threadIdx.x] = (k < K && j < N) ? W[(k0 + k) * ldw + c0 + j] : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {               // write [j][k]: coalesced along k
+        const int j = jb + r, k = kb + threadIdx.x;
+        if (j < N && k < kp) {
+            const float x = tile[threadIdx.x][r];
+            const float h = rna_tf32(x);
+            hi[(int64_t)j * kp + k] = h;
+            lo[(int64_t)j * kp + k] = rna_tf32(x - h);
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+void encode_kmajor(CUtensorMap *map, const float *base, int rows, int kdim, int kp, int box_rows)
+{
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        MP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled", __LINE__};
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)kp * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), gdim, gstride, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled failed", __LINE__};
+}
+
+}  // namespace
+
+size_t tf32_scratch_floats(int64_t n, int nbmax)
+{
+    const int64_t kp = round_up(nbmax, 4);
+    return (size_t)4 * (size_t)n * (size_t)kp + 4096;
+}
+
+void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s)
+{
+    if (M <= 0 || N <= 0 || K <= 0) return;
+    const int kp = (int)round_up(K, 4);
+    float *Lh = scratch, *Ll = Lh + (size_t)M * kp;
+    float *Uh = Ll + (size_t)M * kp, *Ul = Uh + (size_t)N * kp;
+    {
+        const int64_t tot = M * kp;
+        split_rows_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 4096), 256, 0, s>>>(W, ldw, r0, k0, (int)M, (int)K,
+                                                                                              Lh, Ll, kp);
+        MP_LAUNCH_CHECK();
+        dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(kp, 32));
+        split_cols_T_kernel<<<g, dim3(32, 8), 0, s>>>(W, ldw, k0, c0, (int)N, (int)K, Uh, Ul, kp);
+        MP_LAUNCH_CHECK();
+    }
+    CUtensorMap mUh, mUl, mLh, mLl;
+    encode_kmajor(&mUh, Uh, (int)N, (int)K, kp, TM_COLS);
+    encode_kmajor(&mUl, Ul, (int)N, (int)K, kp, TM_COLS);
+    encode_kmajor(&mLh, Lh, (int)M, (int)K, kp, TM_ROWS);
+    encode_kmajor(&mLl, Ll, (int)M, (int)K, kp, TM_ROWS);
+    const int ntiles = (int)(ceil_div(N, TM_COLS) * ceil_div(M, TM_ROWS));
+    const int grid = std::min(ntiles, num_sms);
+    const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
+    func_smem_once((const void *)gemm_3xtf32_kernel, smem);
+    gemm_3xtf32_kernel<<<grid, GT, smem, s>>>(mUh, mUl, mLh, mLl, W + r0 * ldw + c0, ldw, (int)M, (int)N, (int)K);
+    MP_LAUNCH_CHECK();
+    g_launches += 3;
+}
+
+}  // namespace mp

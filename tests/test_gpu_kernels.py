@@ -1,0 +1,71 @@
+"""Kernel-level parity (`-m gpu`): the Schur update K5 (FFMA and tcgen05 3xTF32) through
+the C-ABI test hook include/mp_kernels.h, against an fp64 reference of the same op."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mp():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_0808_2794_b200 import build
+    build.build()
+    from paper_0808_2794_b200 import binding
+    return binding
+
+
+def run(mp, W0, r0, c0, k0, M, N, K, variant):
+    import torch
+    ldw = W0.shape[1]
+    W = torch.from_numpy(W0.copy()).cuda()
+    mp.mp_kernel_schur_update(W, r0, c0, k0, M, N, K, variant)
+    torch.cuda.synchronize()
+    assert W.stride(0) == ldw
+    return W.cpu().numpy()
+
+
+def reference(W0, r0, c0, k0, M, N, K):
+    W = W0.astype(np.float64)
+    R = W.copy()
+    R[r0:r0 + M, c0:c0 + N] -= W[r0:r0 + M, k0:k0 + K] @ W[k0:k0 + K, c0:c0 + N]
+    return R
+
+
+SHAPES = [(64, 64, 0, 256, 128, 64), (300, 200, 7, 512, 333, 32), (1000, 700, 16, 1400, 1200, 256),
+          (256, 128, 0, 300, 400, 100), (513, 129, 40, 700, 700, 200), (2048, 2048, 256, 2304, 2304, 256)]
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_schur_update_exact_integers(mp, variant, shape):
+    """Small integers: every product and partial sum is exact in fp32 (and tf32 hi, lo = 0)."""
+    M, N, k0, rows, cols, K = shape
+    rng = np.random.default_rng(M + N + K)
+    ldw = ((cols + 63) // 64) * 64
+    W0 = rng.integers(-8, 9, size=(rows, ldw)).astype(np.float32)
+    r0, c0 = k0 + K, k0 + K
+    M, N = min(M, rows - r0), min(N, cols - c0)
+    got = run(mp, W0, r0, c0, k0, M, N, K, variant)
+    ref = reference(W0, r0, c0, k0, M, N, K)
+    assert np.array_equal(got.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_schur_update_gaussian_accuracy(mp, variant):
+    rng = np.random.default_rng(5)
+    rows = cols = 1536
+    W0 = rng.standard_normal((rows, cols)).astype(np.float32)
+    k0, K = 256, 256
+    r0 = c0 = k0 + K
+    M, N = rows - r0, cols - c0
+    got = run(mp, W0, r0, c0, k0, M, N, K, variant)
+    ref = reference(W0, r0, c0, k0, M, N, K)
+    scale = np.abs(W0[r0:, k0:k0 + K]).astype(np.float64) @ np.abs(W0[k0:k0 + K, c0:]).astype(np.float64)
+    err = np.abs(got[r0:, c0:] - ref[r0:, c0:]) / (scale + np.abs(ref[r0:, c0:]))
+    # fp32 accumulation over K terms: ~K * 2^-24; 3xTF32 adds the dropped lo*lo term and tf32 rounding of lo
+    assert err.max() <= K * 2.0 ** -24 * 4, err.max()
+    # untouched regions stay bitwise
+    assert np.array_equal(got[:r0], W0[:r0]) and np.array_equal(got[:, :c0], W0[:, :c0])

@@ -275,3 +275,34 @@ def test_lda_larger_than_n(mp, orc):
     Xg, it, info, _ = mp.mp_dsgesv_ex(dA, mp.colmajor_cuda(B))
     torch.cuda.synchronize()
     assert info == 0 and certificate_ok(A, Xg.cpu().numpy(), B)
+
+
+# --------------------------------------------------------------------------- 3xTF32 tcgen05 variant (B:5)
+@pytest.mark.parametrize("n", [700, 2100])
+def test_exact_lu_factors_bitwise_3xtf32(mp, orc, n):
+    A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n + 5)
+    LU, ipiv, info = mp.mp_sgetrf(A, mp.make_opts(variant=mp.MP_VARIANT_3XTF32))
+    assert info == 0
+    assert np.array_equal(perm_from_ipiv(ipiv), perm)
+    assert np.array_equal(np.tril(LU, -1).astype(np.float64), np.tril(L, -1))
+    assert np.array_equal(np.triu(LU).astype(np.float64), U)
+    Xg, it, info, _ = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_3XTF32)
+    assert (it, info) == (0, 0) and np.array_equal(Xg, X)
+
+
+@pytest.mark.parametrize("n,nrhs,seed", [(1024, 1, 4), (1500, 5, 5), (2600, 1, 6)])
+def test_criterion_parity_3xtf32(mp, orc, n, nrhs, seed):
+    A, B, X = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+    ro = orc.dsgesv(A, B)
+    Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_3XTF32)
+    assert info == ro.info == 0
+    assert it >= 0 and abs(it - ro.iters) <= 1, (it, ro.iters, rep.history(), list(ro.hist))
+    assert certificate_ok(A, Xg, B)
+
+
+def test_strict_parity_3xtf32(mp, orc):
+    A, B, X = inputs.conditioned(1024, 1.0, seed=2)
+    ro = orc.dsgesv(A, B)
+    Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_3XTF32)
+    assert info == 0 and abs(it - ro.iters) <= 1
+    assert np.abs(Xg - ro.X).max() / np.abs(ro.X).max() <= 1e-12
