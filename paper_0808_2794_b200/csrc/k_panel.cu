@@ -9,19 +9,33 @@
 // recorded (ST_ZERO_PIVOT, first column) and elimination continues without
 // scaling; the driver then takes the binary64 fallback (iters -3).
 //
-// B200 design — one THREAD-BLOCK CLUSTER of CL = 16 CTAs (non-portable size;
-// 8 if the device refuses 16) owns the whole leaf, held in REGISTERS: thread t
-// of CTA g keeps RPT rows x W columns (rows g*R + t + NT*q).  Per column there
-// is exactly ONE cluster barrier (barrier.cluster, ~0.2 us) instead of a
-// grid-wide barrier: before it every CTA writes its (|a|, position) candidate
-// into every CTA's shared-memory slot (DSMEM stores) and leaves its candidate
-// row (and row kc, if owned) in its own shared memory; after it every CTA
-// reduces the CL slots identically, pulls the winning row (one warp, 128 B of
-// DSMEM loads), installs the interchange in registers and applies the rank-1
-// update, fusing the arg-max of the next column into it.  Double-buffered
-// slots (by column parity) make the next column's writes safe without a second
-// barrier.  Latency-bound: n cluster barriers per factorisation.  The rest of
-// the GPU stays free for the trailing update (look-ahead).
+// B200 design.  The pivot search is the method's serial critical path (n
+// dependent arg-max decisions per factorisation), so a column step must cost
+// a few hundred cycles, not microseconds:
+//
+//  * the leaf lives in REGISTERS of one thread-block cluster of CL <= 16 CTAs
+//    (non-portable size; CL = ceil(m / rows-per-CTA), so short leaves use
+//    fewer SMs): thread t of CTA g holds the rows loaded from positions
+//    c0 + g*R + t + NT*q;
+//  * rows never move between threads: the interchanges are tracked
+//    logically (every row carries its current position) and rows are stored
+//    at their final positions when the leaf is done;
+//  * the column loop is unrolled in groups of UG columns over a rotating
+//    register frame (static register indices, small code: the fully
+//    unrolled loop was instruction-fetch bound);
+//  * the cross-CTA exchange of a column is one-sided: after the CTA-level
+//    arg-max, the warp holding the CTA's candidate row pushes (record, row)
+//    with st.async into a slot of EVERY CTA's shared memory, completing bytes
+//    on that CTA's mbarrier.  Each CTA then waits on its own mbarrier only
+//    (no cluster barrier, no fence on global memory, no global atomics inside
+//    the column loop) and reduces the CL candidate records locally — every
+//    CTA reaches the same pivot and applies the rank-1 update, fused with the
+//    next column's local arg-max.  Slots and mbarriers alternate by column
+//    parity; a CTA cannot push column c+2 before every CTA has pushed column
+//    c+1, which each CTA does only after it has consumed column c's slots, so
+//    the double buffer is race-free without extra synchronisation;
+//  * global memory is touched only at the start (load the leaf) and the end
+//    (store the leaf, orig[] and the leaf's row pairs), plus ipiv.
 #include <cooperative_groups.h>
 
 #include "internal.h"
@@ -34,40 +48,133 @@ namespace {
 
 constexpr int CLMAX = 16;
 
-// Order-preserving key of |a| for the arg-max (non-negative IEEE values order like their
-// bit patterns; NaN is mapped to 0 so it never wins against a finite entry).
-__device__ __forceinline__ void abs_key(float v, unsigned &hi, unsigned &lo)
-{
-    const float a = fabsf(v);
-    hi = (a == a) ? __float_as_uint(a) : 0u;
-    lo = 0u;
-}
-__device__ __forceinline__ void abs_key(double v, unsigned &hi, unsigned &lo)
-{
-    const double a = fabs(v);
-    const unsigned long long b = (a == a) ? (unsigned long long)__double_as_longlong(a) : 0ull;
-    hi = (unsigned)(b >> 32);
-    lo = (unsigned)b;
-}
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-// Warp arg-max of (key, position): largest key, ties to the smallest position.
-// Three redux.sync instructions instead of a shuffle tree.  Inactive lanes pass pos = INT_MAX.
-__device__ __forceinline__ void warp_argmax(unsigned &hi, unsigned &lo, int &pos)
-{
-    const unsigned full = 0xffffffffu;
-    const unsigned h = __reduce_max_sync(full, hi);
-    const unsigned l = __reduce_max_sync(full, hi == h ? lo : 0u);
-    const unsigned pm = __reduce_min_sync(full, (hi == h && lo == l) ? (unsigned)pos : 0x7fffffffu);
-    hi = h;
-    lo = l;
-    pos = (int)pm;
-}
-
-struct __align__(16) Cand {
-    unsigned hi, lo;
-    int pos, pad;
-    int org, lorg, pad1, pad2;
+// Candidate keys for the arg-max (largest |a| wins, ties to the smallest position,
+// reading A-6).  Non-negative IEEE values order like their bit patterns; NaN maps to
+// key 0 so it never beats a finite entry.
+//   binary32: one 64-bit word k = (|a| bits << 32) | (0x7fffffff - pos); k = 0: none.
+//   binary64: 64-bit |a| bits + np = 0x7fffffff - pos (np = -1: none).
+struct __align__(16) Rec {
+    unsigned a, b, c, d;
 };
+
+template <typename T> struct Key;
+
+template <> struct Key<float> {
+    unsigned long long k;
+    __device__ static Key none() { return Key{0ull}; }
+    __device__ static Key make(float x, int pos)
+    {
+        const float v = fabsf(x);
+        const unsigned bits = (v == v) ? __float_as_uint(v) : 0u;
+        return Key{((unsigned long long)bits << 32) | (unsigned)(0x7fffffff - pos)};
+    }
+    __device__ void take(const Key &o) { if (o.k > k) k = o.k; }
+    __device__ bool valid() const { return k != 0ull; }
+    __device__ bool zero_value() const { return (k >> 32) == 0ull; }
+    __device__ int pos() const { return k ? 0x7fffffff - (int)(unsigned)k : 0x7fffffff; }
+    __device__ void warp_max()
+    {
+        const unsigned h = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32));
+        const unsigned l = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32) == h ? (unsigned)k : 0u);
+        k = ((unsigned long long)h << 32) | l;
+    }
+    __device__ bool operator==(const Key &o) const { return k == o.k; }
+    __device__ void store(Rec &r) const { r.a = (unsigned)(k >> 32); r.b = (unsigned)k; r.c = 0u; r.d = 0u; }
+    __device__ static Key load(const Rec &r) { return Key{((unsigned long long)r.a << 32) | r.b}; }
+};
+
+template <> struct Key<double> {
+    unsigned long long key;
+    int np;
+    __device__ static Key none() { return Key{0ull, -1}; }
+    __device__ static Key make(double x, int pos)
+    {
+        const double v = fabs(x);
+        return Key{(v == v) ? (unsigned long long)__double_as_longlong(v) : 0ull, 0x7fffffff - pos};
+    }
+    __device__ void take(const Key &o) { if (o.key > key || (o.key == key && o.np > np)) *this = o; }
+    __device__ bool valid() const { return np >= 0; }
+    __device__ bool zero_value() const { return key == 0ull; }
+    __device__ int pos() const { return np >= 0 ? 0x7fffffff - np : 0x7fffffff; }
+    __device__ void warp_max()
+    {
+        const unsigned hk = (unsigned)(key >> 32), lk = (unsigned)key;
+        const unsigned h = __reduce_max_sync(0xffffffffu, hk);
+        const unsigned l = __reduce_max_sync(0xffffffffu, hk == h ? lk : 0u);
+        np = __reduce_max_sync(0xffffffffu, (hk == h && lk == l) ? np : -1);
+        key = ((unsigned long long)h << 32) | l;
+    }
+    __device__ bool operator==(const Key &o) const { return key == o.key && np == o.np; }
+    __device__ void store(Rec &r) const { r.a = (unsigned)(key >> 32); r.b = (unsigned)key; r.c = (unsigned)np; r.d = 0u; }
+    __device__ static Key load(const Rec &r) { return Key{((unsigned long long)r.a << 32) | r.b, (int)r.c}; }
+};
+
+// Reciprocal for the multipliers l = x / piv (reading A-7): hardware approximation +
+// one Newton step, then per row q = x*r corrected once with the residual fma(-piv,q,x).
+// Equal to the IEEE quotient except in rare double-rounding cases (<= 1 ulp).
+__device__ __forceinline__ float recip(float v)
+{
+    float r;
+    asm("rcp.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+    return fmaf(r, fmaf(-v, r, 1.0f), r);
+}
+__device__ __forceinline__ double recip(double v) { return 1.0 / v; }
+
+
+template <typename T, int W>
+struct __align__(16) Slot {
+    Rec rec;
+    T row[W];
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int count)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count)
+{
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, int rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async16(uint32_t raddr, uint4 v, uint32_t rbar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                     raddr),
+                 "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(rbar)
+                 : "memory");
+}
+
+#ifdef MP_PANEL_TRACE
+__device__ long long g_trace[64][8];
+#define TRACE(c, k) do { if (tid == 0 && g == 0 && (c) < 64) g_trace[(c)][(k)] = clock64(); } while (0)
+#else
+#define TRACE(c, k) do { } while (0)
+#endif
 
 template <typename T>
 struct LeafArgs {
@@ -81,217 +188,260 @@ struct LeafArgs {
     DevStatus *st;
 };
 
-template <typename T, int NT, int RPT, int W>
-__global__ void __launch_bounds__(NT, 1) panel_cluster_kernel(LeafArgs<T> a)
+// RPT rows per thread, leaf width W, column loop unrolled in groups of UG columns.
+//
+// Rows never move between threads inside the leaf: every row carries its CURRENT
+// position cur (LAPACK's sequential interchanges, tracked logically): at
+// column c the winner (position p) gets position kc and retires, the row at position
+// kc gets position p.  Rows are stored at their final positions at the end.
+//
+// Register frame: at the start of group o, slot s holds leaf column (o*UG + s) mod W;
+// the frame is rotated by UG after every group (W/UG rotations = identity at the end).
+// Slots s >= W - o*UG hold multipliers of earlier columns ("dead"); the staged pivot
+// row has them zeroed so the rank-1 update leaves them unchanged.
+template <typename T, int NT, int RPT, int W, int UG, bool MULTI>
+__global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 {
-    // Register frame: every active row keeps its W leaf values ROTATED by the number of
-    // columns eliminated so far: slot s holds column (c + s) for s < W - c and the
-    // multiplier l of column (s - (W - c)) for s >= W - c.  All active rows share the
-    // frame, so a column step is a constant-size body (update slots 1..W-1 with the
-    // pivot row, consumed slots masked to zero, then rotate by one) and the column loop
-    // stays rolled: small code, no instruction-cache misses, no dynamic indexing.
-    //
-    // Per column: one __syncthreads (warp candidates -> CTA candidate) and ONE cluster
-    // barrier.  Before the barrier the winning warp of every CTA pushes its candidate
-    // record and candidate row into every CTA's shared memory, and the warp owning row
-    // kc pushes row kc: afterwards everything is local.  All shared buffers touched
-    // across the barrier are double-buffered by column parity.
     constexpr int NWP = NT / 32;
+    static_assert(W % UG == 0, "group size must divide the leaf width");
+    using SlotT = Slot<T, W>;
+    using K = Key<T>;
+    static_assert(sizeof(SlotT) % 16 == 0, "slot must be 16-byte chunks");
+    constexpr int CH = (int)(sizeof(SlotT) / 16);
+    constexpr int EPC = 16 / (int)sizeof(T);     // elements per 16-byte chunk
     cg::cluster_group cluster = cg::this_cluster();
     const int g = (int)cluster.block_rank();
     const int CL = (int)cluster.num_blocks();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const unsigned full = 0xffffffffu;
 
-    __shared__ __align__(16) T cand_rows[2][CLMAX][W];   // pushed by every CTA
-    __shared__ __align__(16) T diag_rows[2][W];          // pushed by the owner of row kc
-    __shared__ Cand slot[2][CLMAX];                       // pushed by every CTA
-    __shared__ int diag_org[2], diag_lorg[2];
-    __shared__ unsigned whi[2][NWP], wlo[2][NWP];
-    __shared__ int wpos[2][NWP];
+    __shared__ SlotT slots[2][CLMAX];     // incoming CTA candidates, by source CTA
+    __shared__ SlotT wstage[2][NWP];      // per-warp candidates, by column parity
+    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ int s_p[2], s_ww[2];       // single-CTA leaves: pivot position, winning warp
 
     const long long n = a.n, c0 = a.c0, ldw = a.ldw;
     const int w = a.w;
     constexpr int R = NT * RPT;                  // rows per CTA
     const long long base = c0 + (long long)g * R;
     const int nn = (int)(n - base);              // rows of this CTA that exist: local index < nn
+    const unsigned bytes_per_col = (unsigned)(CL * sizeof(SlotT));
+
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (g == 0) *a.npairs = 0;
+    }
+    // every CTA's mbarriers must be initialised before anyone pushes into them
+    cluster.sync();
 
     T x[RPT][W];
-    int org[RPT], lorg[RPT];
+    int org[RPT], cur[RPT];
+    bool act[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
         const bool valid = li < nn;
         const T *row = a.W + (base + li) * ldw + c0;
+        if (valid && w == W && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
-        for (int s = 0; s < W; ++s) x[q][s] = (valid && s < w) ? row[s] : T(0);
+            for (int s = 0; s < W; s += EPC) {
+                const uint4 v = *reinterpret_cast<const uint4 *>(row + s);
+                const T *pv = reinterpret_cast<const T *>(&v);
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) x[q][s + e] = pv[e];
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < W; ++s) x[q][s] = (valid && s < w) ? row[s] : T(0);
+        }
         org[q] = valid ? a.orig[base + li] : -1;
-        lorg[q] = (int)(base + li);
+        cur[q] = (int)(base + li);
+        act[q] = valid;
     }
+
+    // this thread's candidate for column 0
+    K ck = K::none();
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+        if (act[q]) ck.take(K::make(x[q][0], cur[q]));
 
 #pragma unroll 1
-    for (int c = 0; c < w; ++c) {
-        const int par = c & 1;
-        const long long kc = c0 + c;
-        const int kl = (int)(kc - base);          // local index of row kc (may be out of range)
-        // ---- this thread's candidate for column c (slot 0 of the frame), then warp / CTA arg-max
-        unsigned hi = 0u, lo = 0u;
-        int pos = 0x7fffffff;
+    for (int o = 0; o < W / UG; ++o) {
+        const int live = W - o * UG;             // slots >= live are dead (multipliers)
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const int li = tid + NT * q;
-            if (li < nn && li >= kl) {
-                unsigned h, l;
-                abs_key(x[q][0], h, l);
-                if (pos == 0x7fffffff || h > hi || (h == hi && l > lo)) { hi = h; lo = l; pos = (int)(base + li); }
-            }
-        }
-        warp_argmax(hi, lo, pos);
-        if (lane == 0) { whi[par][warp] = hi; wlo[par][warp] = lo; wpos[par][warp] = pos; }
-        __syncthreads();
-        {
-            unsigned h = lane < NWP ? whi[par][lane] : 0u;
-            unsigned l = lane < NWP ? wlo[par][lane] : 0u;
-            int ps = lane < NWP ? wpos[par][lane] : 0x7fffffff;
-            warp_argmax(h, l, ps);
-            hi = h; lo = l; pos = ps;             // CTA candidate, known to every warp
-        }
-        // ---- the warp holding the CTA candidate pushes record + row into every CTA
-        if (pos != 0x7fffffff) {
-            const int li = (int)(pos - base);
-            if ((li % NT) / 32 == warp) {
-                const int src = li % 32, qq = li / NT;
-                T v = T(0);
-                int o = 0, lo_ = 0;
+        for (int u = 0; u < UG; ++u) {
+            const int c = o * UG + u;
+            if (c < w) {
+                const int par = c & 1;
+                const long long kc = c0 + c;
+                TRACE(c, 0);
+                // ---- warp arg-max; the lane holding the warp's candidate stages (record, row)
+                {
+                    K wk = ck;
+                    wk.warp_max();
+                    const int wp = wk.pos();
+                    int qs = -1;
+#pragma unroll
+                    for (int q = RPT - 1; q >= 0; --q)
+                        if (act[q] && cur[q] == wp) qs = q;
+                    if (qs >= 0) {                       // one lane per warp: a divergent, short branch
+#pragma unroll
+                        for (int q = 0; q < RPT; ++q)
+                            if (q == qs) {
+#pragma unroll
+                                for (int s = 0; s < W; s += EPC) {
+                                    uint4 v;
+                                    T *pv = reinterpret_cast<T *>(&v);
+#pragma unroll
+                                    for (int e = 0; e < EPC; ++e) pv[e] = s + e < live ? x[q][s + e] : T(0);
+                                    *reinterpret_cast<uint4 *>(&wstage[par][warp].row[s]) = v;
+                                }
+                            }
+                    }
+                    if (lane == 0) wk.store(wstage[par][warp].rec);
+                }
+                const SlotT *win;
+                int p;
+                K pk;                                     // the pivot's key (thread 0 only needs it)
+                if constexpr (!MULTI) {
+                    // ---- single-CTA leaf: the CTA arg-max is the pivot; no exchange
+                    if (warp == 0) {
+                        named_bar_sync(1, NT);           // every warp has staged
+                        TRACE(c, 1);
+                        K bk = lane < NWP ? K::load(wstage[par][lane].rec) : K::none();
+                        const K mine = bk;
+                        bk.warp_max();
+                        const int ww = __ffs(__ballot_sync(0xffffffffu, mine == bk && lane < NWP)) - 1;
+                        if (lane == 0) { s_p[par] = bk.pos(); s_ww[par] = ww; }
+                        pk = bk;
+                        TRACE(c, 2);
+                        named_bar_sync(2, NT);
+                    } else {
+                        named_bar_arrive(1, NT);
+                        named_bar_sync(2, NT);
+                    }
+                    p = s_p[par];
+                    win = &wstage[par][s_ww[par]];
+                    TRACE(c, 3);
+                } else {
+                    // ---- leader warp: CTA arg-max and push (record, row) into every CTA
+                    if (warp == 0) {
+                        named_bar_sync(1, NT);           // every warp has staged
+                        TRACE(c, 1);
+                        K bk = lane < NWP ? K::load(wstage[par][lane].rec) : K::none();
+                        const K mine = bk;
+                        bk.warp_max();
+                        const int ww = __ffs(__ballot_sync(0xffffffffu, mine == bk && lane < NWP)) - 1;
+                        if (lane == 0) mbar_arm(&mbar[par], bytes_per_col);
+                        const uint4 *s4 = reinterpret_cast<const uint4 *>(&wstage[par][ww]);
+                        const uint32_t dst = smem_u32(&slots[par][g]), b = smem_u32(&mbar[par]);
+                        for (int idx = lane; idx < CL * CH; idx += 32) {
+                            const int r = idx / CH, ch = idx - r * CH;
+                            const uint4 v = s4[ch];
+                            st_async16(mapa(dst + 16u * ch, r), v, mapa(b, r));
+                        }
+                        TRACE(c, 2);
+                    } else {
+                        named_bar_arrive(1, NT);
+                    }
+                    // ---- every warp: wait for the CL candidates, identical cluster arg-max
+                    mbar_wait_cluster(&mbar[par], (unsigned)((c >> 1) & 1));
+                    TRACE(c, 3);
+                    K gk = lane < CL ? K::load(slots[par][lane].rec) : K::none();
+                    const K mine = gk;
+                    gk.warp_max();
+                    const int gw = __ffs(__ballot_sync(0xffffffffu, mine == gk && lane < CL)) - 1;
+                    p = gk.pos();
+                    pk = gk;
+                    win = &slots[par][gw];
+                }
+                TRACE(c, 4);
+                if (g == 0 && tid == 0) {
+                    a.ipiv[kc] = (int32_t)p;
+                    if (pk.zero_value()) {               // exact zero pivot (or all NaN)
+                        atomicOr(&a.st->flags, (int)ST_ZERO_PIVOT);
+                        atomicMin(&a.st->zero_col, (int)(kc + 1));
+                    }
+                }
+
+                // ---- logical interchange, scale, rank-1 update; next column's candidate.
+                // Branch-free per row (predicated selects): rows that are not updated use l = 0.
+                const T piv = win->row[u];
+                const bool scale = piv != T(0);
+                // subnormal pivots: scale numerator and pivot by the same power of two
+                const T sc = fabs(piv) < (sizeof(T) == 4 ? T(1e-30) : T(1e-300)) ? T(sizeof(T) == 4 ? 0x1p64 : 0x1p512) : T(1);
+                const T ps = piv * sc;
+                const T rinv = scale ? recip(ps) : T(0);
+                ck = K::none();
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
+                    const bool is_piv = act[q] && cur[q] == p;
+                    const bool upd = act[q] && cur[q] != p;
+                    cur[q] = is_piv ? (int)kc : ((upd && cur[q] == (int)kc) ? p : cur[q]);
+                    act[q] = upd;
+                    const T xv = x[q][u];
+                    const T xs = xv * sc;
+                    T l = xs * rinv;
+                    l = fma(fma(-ps, l, xs), rinv, l);
+                    l = scale ? l : xv;
+                    l = upd ? l : T(0);
+                    x[q][u] = upd ? l : xv;
 #pragma unroll
-                    for (int s = 0; s < W; ++s) {
-                        const T t = __shfl_sync(full, x[q][s], src);
-                        if (q == qq && s == (lane % W)) v = t;
+                    for (int s2 = u + 1; s2 < W; ++s2) x[q][s2] = fma(-l, win->row[s2], x[q][s2]);
+                    if (u + 1 < W) {
+                        const K kq = K::make(x[q][(u + 1) % W], cur[q]);
+                        ck.take(upd ? kq : K::none());
                     }
-                    const int to = __shfl_sync(full, org[q], src);
-                    const int tl = __shfl_sync(full, lorg[q], src);
-                    if (q == qq) { o = to; lo_ = tl; }
-                }
-                // lanes 0..W-1 push element lane to CTAs r = 0.. (32/W lanes per element cover CTAs)
-                for (int r = lane / W; r < CL; r += 32 / W)
-                    *cluster.map_shared_rank(&cand_rows[par][g][lane % W], r) = v;
-                if (lane < CL) {
-                    Cand rec;
-                    rec.hi = hi; rec.lo = lo; rec.pos = pos; rec.pad = 0;
-                    rec.org = o; rec.lorg = lo_; rec.pad1 = rec.pad2 = 0;
-                    *cluster.map_shared_rank(&slot[par][g], lane) = rec;
                 }
             }
-        } else if (warp == 0 && lane < CL) {
-            Cand rec = {0u, 0u, 0x7fffffff, 0, -1, -1, 0, 0};
-            *cluster.map_shared_rank(&slot[par][g], lane) = rec;
         }
-        // ---- the warp holding row kc pushes it (the owner of p needs it after the barrier)
-        if (kl >= 0 && kl < R && kl < nn && (kl % NT) / 32 == warp) {
-            const int src = kl % 32, qq = kl / NT;
-            T v = T(0);
-            int o = 0, lo_ = 0;
+        // ---- rotate the frame by UG
+        if constexpr (UG < W) {
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
+                T t[UG];
 #pragma unroll
-                for (int s = 0; s < W; ++s) {
-                    const T t = __shfl_sync(full, x[q][s], src);
-                    if (q == qq && s == (lane % W)) v = t;
-                }
-                const int to = __shfl_sync(full, org[q], src);
-                const int tl = __shfl_sync(full, lorg[q], src);
-                if (q == qq) { o = to; lo_ = tl; }
-            }
-            for (int r = lane / W; r < CL; r += 32 / W)
-                *cluster.map_shared_rank(&diag_rows[par][lane % W], r) = v;
-            if (lane < CL) {
-                *cluster.map_shared_rank(&diag_org[par], lane) = o;
-                *cluster.map_shared_rank(&diag_lorg[par], lane) = lo_;
-            }
-        }
-        cluster.sync();                                   // the one cluster barrier of this column
-
-        // ---- every warp: identical arg-max over the CL slots (all local now)
-        unsigned ph = lane < CL ? slot[par][lane].hi : 0u;
-        unsigned pl = lane < CL ? slot[par][lane].lo : 0u;
-        int p = lane < CL ? slot[par][lane].pos : 0x7fffffff;
-        const int myp = p;
-        warp_argmax(ph, pl, p);
-        const int gw = __ffs(__ballot_sync(full, myp == p && lane < CL)) - 1;
-        const T *prow = &cand_rows[par][gw][0];
-        const T *drow = &diag_rows[par][0];
-        const bool zero_piv = (ph == 0u && pl == 0u);
-        // row kc is final: its owner CTA writes it out (un-rotating through shared memory)
-        if (kl >= 0 && kl < R) {
-            if (tid < w) a.W[kc * ldw + c0 + tid] = prow[(tid - c + W) % W];
-            if (tid == 0) {
-                a.orig[kc] = slot[par][gw].org;
-                const int plorg = slot[par][gw].lorg;
-                if (plorg != (int)kc) {
-                    const int si = atomicAdd(a.npairs, 1);
-                    a.pairs[2 * si] = (int32_t)kc;
-                    a.pairs[2 * si + 1] = plorg;
-                }
-            }
-        }
-        if (g == 0 && tid == 0) {
-            a.ipiv[kc] = (int32_t)p;
-            if (zero_piv) {                               // exact zero pivot
-                atomicOr(&a.st->flags, (int)ST_ZERO_PIVOT);
-                atomicMin(&a.st->zero_col, (int)(kc + 1));
-            }
-        }
-
-        // ---- install the interchange, scale, rank-1 update, rotate
-        const T piv = prow[0];
-        const bool scale = piv != T(0);
-        T pu[W];
+                for (int s = 0; s < UG; ++s) t[s] = x[q][s];
 #pragma unroll
-        for (int s = 1; s < W; ++s) pu[s] = (s < W - c) ? prow[s] : T(0);
+                for (int s = 0; s < W - UG; ++s) x[q][s] = x[q][s + UG];
 #pragma unroll
-        for (int q = 0; q < RPT; ++q) {
-            const int li = tid + NT * q;
-            if (p != (int)kc && base + li == p) {
-#pragma unroll
-                for (int s = 0; s < W; ++s) x[q][s] = drow[s];
-                org[q] = diag_org[par];
-                lorg[q] = diag_lorg[par];
-            }
-            if (li > kl && li < nn) {
-                const T l = scale ? x[q][0] / piv : x[q][0];
-#pragma unroll
-                for (int s = 1; s < W; ++s) x[q][s] = fma(-l, pu[s], x[q][s]);
-#pragma unroll
-                for (int s = 0; s < W - 1; ++s) x[q][s] = x[q][s + 1];
-                x[q][W - 1] = l;
+                for (int s = 0; s < UG; ++s) x[q][W - UG + s] = t[s];
             }
         }
     }
 
-    // ---- write back the rows below the leaf's diagonal block (rotated by w: column j
-    //      lives in slot j + W - w); rows c0 .. c0+w-1 were written when they became final
+    // ---- store every row at its final position, orig[] and the leaf pairs
+    cluster.sync();   // orders the npairs reset before the pair emission below
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
-        const long long pos = base + li;
-        if (pos >= c0 + w && li < nn) {
+        if (li < nn) {
+            const long long pos = cur[q];
             T *row = a.W + pos * ldw + c0;
+            if (w == W && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
-            for (int s = 0; s < W; ++s) {
-                const int j = s - (W - w);
-                if (j >= 0) row[j] = x[q][s];
+                for (int s = 0; s < W; s += EPC) {
+                    uint4 v;
+                    T *pv = reinterpret_cast<T *>(&v);
+#pragma unroll
+                    for (int e = 0; e < EPC; ++e) pv[e] = x[q][s + e];
+                    *reinterpret_cast<uint4 *>(row + s) = v;
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < W; ++s)
+                    if (s < w) row[s] = x[q][s];
             }
             a.orig[pos] = org[q];
-            if (lorg[q] != (int)pos) {
+            const int lorg = (int)(base + li);
+            if (lorg != (int)pos) {
                 const int si = atomicAdd(a.npairs, 1);
                 a.pairs[2 * si] = (int32_t)pos;
-                a.pairs[2 * si + 1] = lorg[q];
+                a.pairs[2 * si + 1] = lorg;
             }
         }
     }
-    cluster.sync();   // no CTA may exit while others can still write into its shared memory
 }
 
 __global__ void orig_init_kernel(int32_t *orig, int64_t k, int64_t n)
@@ -313,18 +463,25 @@ __global__ void emit_pairs_kernel(const int32_t *orig, int64_t k, int64_t n, int
 }
 
 // ---------------------------------------------------------------- host side
+// Configurations (threads per CTA, rows per thread, leaf width).  Four rows per thread
+// amortise the per-column protocol (arg-max, barriers) over several rows; data registers
+// RPT * W * sizeof(T) / 4 <= 128.  Capacity per cluster = CLMAX * NT * RPT rows; the
+// cluster uses ceil(m / (NT * RPT)) CTAs.
 struct LeafCfg { int nt, rpt, w; };
+constexpr LeafCfg kCfgF[] = {{128, 4, 32}, {256, 4, 32}, {512, 4, 16}, {512, 8, 8}};
+constexpr LeafCfg kCfgD[] = {{128, 4, 16}, {256, 4, 16}, {512, 4, 8}, {512, 8, 4}};
+constexpr int kNumCfg = 4;
 
-// capacity per cluster = CL * nt * rpt rows; data registers rpt * w * sizeof(T) / 4 <= 64
-constexpr LeafCfg kCfgF[] = {{256, 1, 32}, {512, 2, 32}, {512, 4, 16}, {512, 8, 8}};
-constexpr LeafCfg kCfgD[] = {{256, 1, 32}, {512, 2, 16}, {512, 4, 8}, {512, 8, 4}};
+int g_cluster = 0;   // largest cluster size the device accepts (16, else 8)
 
-int g_cluster = 0;   // cluster size chosen at first use (16, else 8)
-
+#ifndef MP_PANEL_UG
+#define MP_PANEL_UG 4
+#endif
 template <typename T, int NT, int RPT, int W>
 void launch_cfg(const LeafArgs<T> &a, int cl, cudaStream_t s)
 {
-    auto kern = panel_cluster_kernel<T, NT, RPT, W>;
+    constexpr int UG = W > MP_PANEL_UG ? MP_PANEL_UG : W;
+    auto kern = cl > 1 ? panel_leaf_kernel<T, NT, RPT, W, UG, true> : panel_leaf_kernel<T, NT, RPT, W, UG, false>;
     if (cl > 8) func_cluster16_once((const void *)kern);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cl, 1, 1);
@@ -345,7 +502,7 @@ int cluster_size()
 {
     if (g_cluster) return g_cluster;
     // can a 16-CTA cluster of the widest configuration be resident?
-    auto kern = panel_cluster_kernel<float, 512, 2, 32>;
+    auto kern = panel_leaf_kernel<float, 512, 8, 8, 8, true>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int nclusters = 0;
     if (e == cudaSuccess) {
@@ -369,7 +526,7 @@ int cluster_size()
 int select_cfg(size_t elem, int64_t m, int cl)
 {
     const LeafCfg *c = elem == 4 ? kCfgF : kCfgD;
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < kNumCfg; ++i)
         if ((int64_t)cl * c[i].nt * c[i].rpt >= m) return i;
     return -1;
 }
@@ -388,25 +545,27 @@ template <typename T>
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
                        DevStatus *st, cudaStream_t s)
 {
-    const int cl = cluster_size();
-    const int sel = select_cfg(sizeof(T), n - c0, cl);
-    if (sel < 0 || w > (sizeof(T) == 4 ? kCfgF : kCfgD)[sel].w)
+    const int clmax = cluster_size();
+    const int64_t m = n - c0;
+    const int sel = select_cfg(sizeof(T), m, clmax);
+    const LeafCfg *cfgs = sizeof(T) == 4 ? kCfgF : kCfgD;
+    if (sel < 0 || w > cfgs[sel].w)
         throw CudaError{cudaErrorInvalidValue, "panel leaf does not fit one cluster", __LINE__};
+    const int cl = (int)std::max<int64_t>(1, ceil_div(m, (int64_t)cfgs[sel].nt * cfgs[sel].rpt));
     LeafArgs<T> a;
     a.W = W; a.ldw = ldw; a.n = n; a.c0 = c0; a.w = w; a.ipiv = ipiv;
     a.orig = ps.orig; a.pairs = ps.pairs; a.npairs = ps.npairs; a.st = st;
-    MP_CUDA(cudaMemsetAsync(ps.npairs, 0, sizeof(int32_t), s));
     if constexpr (sizeof(T) == 4) {
         switch (sel) {
-        case 0: launch_cfg<T, 256, 1, 32>(a, cl, s); break;
-        case 1: launch_cfg<T, 512, 2, 32>(a, cl, s); break;
+        case 0: launch_cfg<T, 128, 4, 32>(a, cl, s); break;
+        case 1: launch_cfg<T, 256, 4, 32>(a, cl, s); break;
         case 2: launch_cfg<T, 512, 4, 16>(a, cl, s); break;
         default: launch_cfg<T, 512, 8, 8>(a, cl, s); break;
         }
     } else {
         switch (sel) {
-        case 0: launch_cfg<T, 256, 1, 32>(a, cl, s); break;
-        case 1: launch_cfg<T, 512, 2, 16>(a, cl, s); break;
+        case 0: launch_cfg<T, 128, 4, 16>(a, cl, s); break;
+        case 1: launch_cfg<T, 256, 4, 16>(a, cl, s); break;
         case 2: launch_cfg<T, 512, 4, 8>(a, cl, s); break;
         default: launch_cfg<T, 512, 8, 4>(a, cl, s); break;
         }
