@@ -401,8 +401,8 @@ int fp64_solve(const Views &v, int64_t n, int64_t nrhs, int nb, Pool &pool, Stat
     double *W = pool.get<double>((size_t)n * ldw);
     int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
     double *Y = pool.get<double>((size_t)n * nrhs);
-    const int nblk = (int)ceil_div(n, solve_block_rows());
-    SolveScratch ss{pool.get<unsigned>(2 * (size_t)nblk), pool.get<unsigned>(2)};
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<double>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
     sio.reset();                                   // fresh status: the binary32 attempt may have flagged a zero pivot
     launch_demote_transpose<double>(v.A, v.lda, n, W, ldw, nullptr, nullptr, sio.d, s);
     run_factor<double>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);
@@ -457,8 +457,8 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     rs.partial = pool.get<double>(residual_partial_elems(n, nrhs, sms));
     rs.blocksums = pool.get<double>((size_t)ceil_div(n, 256) * 2 * nrhs);
     rs.counter = pool.get<unsigned>(1);
-    const int nblk = (int)ceil_div(n, solve_block_rows());
-    SolveScratch ss{pool.get<unsigned>(2 * (size_t)nblk), pool.get<unsigned>(2)};
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<float>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
     double *dpart = pool.get<double>((size_t)sms * 8);
     unsigned *dcnt = pool.get<unsigned>(1);
     MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));

@@ -139,14 +139,16 @@ void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, in
 
 // ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
 struct SolveScratch {
-    unsigned *flags;      // [2][nblk] ready flags (forward / backward), zeroed per solve
-    unsigned *tickets;    // [2] dynamic block tickets
+    unsigned *flags;      // [4][nblk] y / F ready flags (forward, backward), epoch-tagged, zeroed once
+    void *F;              // [min(nrhs,16)][n] far partial sums (element type of the solve)
+    unsigned epoch;       // last epoch used (incremented per sweep)
 };
 // Forward (unit L) then backward (U) substitution on Y (n x nrhs, T, column-major
 // with ld n) with the packed LU in W; then X (double, ld n) = (mode 0) or += (mode 1) Y.
 template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
                      SolveScratch &ss, cudaStream_t s);
+size_t solve_flag_words(int64_t n);
 int solve_block_rows();
 
 // ---------------------------------------------------------------- K8/K10 residual (k_residual.cu)

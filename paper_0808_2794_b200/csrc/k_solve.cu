@@ -1,18 +1,38 @@
-// k_solve.cu — K7 + K9: the binary32 triangular solves with the packed LU and
+// k_solve.cu — K7 + K9: the triangular solves with the packed LU factors and
 // the binary64 update of the solution.
 //
 // PAPER.md Alg. 1 steps 2-3 / 5-6: "solve L y = P r_k",
-// "solve U z_k = y" in single precision; step 7: x_k <- x_{k-1} + z_k
-// in double (fused into the backward solve's write-back).  The permutation P
-// was already applied when y was demoted (K6 / the residual epilogue).
+// "solve U z_k = y" in the factorisation precision; step 7:
+// x_k <- x_{k-1} + z_k in double (fused into the backward sweep's write-back).
+// The permutation P was already applied when y was demoted (K6 / the residual
+// epilogue).
 //
-// One kernel per triangle.  The n rows are cut into BS-row block rows; CTAs
-// take block rows in dependency order from an atomic ticket and chain on
-// per-block ready flags (no grid barrier, no per-block launches).  CTA I
-// streams the off-diagonal tiles L(I, J) (or U(I, J)) as soon as block J is
-// published — the GEMV part, HBM-bound, 4 n^2 bytes per forward+backward pair
-// — then one warp per right-hand side runs the BS-step substitution of the
-// diagonal block (latency-bound), publishes its block and sets its flag.
+// One sweep = one cooperative kernel.  The n rows are cut into BS = 64-row
+// blocks, visited in dependency order (top-down for L, bottom-up for U).
+//
+//   * The CHAIN CTA (block 0) runs the whole dependent substitution on ONE SM,
+//     so the serial chain never pays a cross-SM hand-off: for every block it
+//     forms r_I = b_I - F_I - sum_{d=1..DN} T(I, I-d) y_{I-d} (the DN "near"
+//     tiles from shared memory), then warp c solves the 64 x 64 diagonal block
+//     for right-hand side c: lanes own two rows each; rows are finished in
+//     8-row chunks whose 8 x 8 triangle every lane solves redundantly (no
+//     shuffle chain), followed by 8 FMAs per owned row.
+//   * The HELPER CTAs accumulate the "far" part F_I = sum_{J older than I-DN}
+//     T(I, J) y_J as soon as the y_J are published (flags with an epoch), and
+//     publish F_I with a flag; they run DN blocks ahead of the chain.
+//   * Every tile is streamed HBM -> shared memory by a producer warp with TMA
+//     (2D tensor map over the row-major working copy, out-of-range rows and
+//     columns zero-filled), through an mbarrier ring, ahead of its use.
+//
+// Unit lower L (forward) uses no division.  The upper sweep computes
+// x_i = b_i / u_ii as q = b*r, r = 1/u_ii correctly rounded, with one residual
+// correction q += (b - u q) r: the IEEE quotient except in rare double-rounding
+// cases, <= 1 ulp (reading A-7, extended to the substitution; exact whenever
+// u_ii is a power of two, as in the exact-LU pin P2).
+// HBM traffic: 2 n^2 sizeof(T) per sweep (each factor read once), plus O(n).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 
 #include "internal.h"
@@ -21,11 +41,102 @@ namespace mp {
 
 namespace {
 
-constexpr int BS = 128;           // block-row height
-constexpr int ST = 256;           // threads per CTA
-constexpr int MAXR = 16;          // right-hand sides per launch
-constexpr int LDD = BS + 1;       // smem stride of the transposed diagonal block
+constexpr int BS = 64;                 // block rows
+constexpr int NCW = 8;                 // compute warps per CTA
+constexpr int WPUB = NCW;              // chain CTA: publisher warp (fence + y flag)
+constexpr int WPREP = NCW + 1;         // chain CTA: prepares the next block (rhs, F, diagonal copy)
+constexpr int WPROD = NCW + 2;         // TMA producer warp
+constexpr int NTH = (NCW + 3) * 32;
+constexpr int MAXR = 16;               // right-hand sides per launch
 
+template <typename T> struct SCfg;
+template <> struct SCfg<float> {
+    static constexpr int DN = 4;                  // near tiles handled by the chain CTA
+    static constexpr int CHB = 2;                 // chain ring: blocks in flight
+    static constexpr int HS = 8;                  // helper ring stages
+    static constexpr int YB = 8;                  // y blocks fetched per helper batch
+    static constexpr int MAXOWN = 12;             // far blocks owned by one helper CTA
+};
+template <> struct SCfg<double> {
+    static constexpr int DN = 2;
+    static constexpr int CHB = 1;
+    static constexpr int HS = 3;
+    static constexpr int YB = 4;
+    static constexpr int MAXOWN = 8;
+};
+
+template <typename T>
+constexpr size_t tile_bytes() { return (size_t)BS * BS * sizeof(T); }
+
+// Tiles land in shared memory through TMA with SWIZZLE_128B: a 64 x 64 tile is NBOX boxes
+// of 64 rows x 128 bytes; inside a box the 16-byte chunk c of row r is stored at chunk
+// c ^ (r & 7).  Rows read by consecutive lanes then fall in different banks.
+template <typename T> struct Sw {
+    static constexpr int EPB = 128 / (int)sizeof(T);     // elements per 128-byte box row
+    static constexpr int NBOX = BS / EPB;
+    static constexpr int EPC = 16 / (int)sizeof(T);      // elements per 16-byte chunk
+    __device__ __forceinline__ static int off(int r, int c)
+    {
+        const int h = c / EPB, cc = c - h * EPB;
+        const int ch = cc / EPC, w = cc - ch * EPC;
+        return h * (BS * EPB) + r * EPB + ((ch ^ (r & 7)) * EPC) + w;
+    }
+};
+
+template <typename T>
+constexpr size_t chain_smem()
+{
+    using C = SCfg<T>;
+    return (size_t)C::CHB * (1 + C::DN) * tile_bytes<T>() + (size_t)(C::DN + 1) * MAXR * BS * sizeof(T) +
+           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T);
+}
+template <typename T>
+constexpr size_t helper_smem()
+{
+    return (size_t)SCfg<T>::HS * tile_bytes<T>() + (size_t)SCfg<T>::YB * MAXR * BS * sizeof(T) +
+           (size_t)SCfg<T>::MAXOWN * MAXR * BS * sizeof(T);
+}
+template <typename T>
+constexpr size_t sweep_smem() { return (chain_smem<T>() > helper_smem<T>() ? chain_smem<T>() : helper_smem<T>()) + 1024; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// tile (row block I, column block J) -> smem, NBOX swizzled boxes (out of range: zero-filled)
+template <typename T>
+__device__ __forceinline__ void tma_tile(T *dst, const CUtensorMap *map, uint64_t *bar, int J, int I)
+{
+#pragma unroll
+    for (int hb = 0; hb < Sw<T>::NBOX; ++hb)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(dst + hb * BS * Sw<T>::EPB)),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(J * BS + hb * Sw<T>::EPB), "r"(I * BS), "r"(smem_u32(bar))
+            : "memory");
+}
+// named barriers: 1 = compute warps (helpers) / compute + prep + publisher (chain); 2 = solvers -> publisher
+__device__ __forceinline__ void nbar_sync(int id, int count) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int count) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory"); }
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p)
 {
     unsigned v;
@@ -36,207 +147,547 @@ __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-template <typename T> struct V4;
-template <> struct V4<float> { using type = float4; };
-template <> struct V4<double> { using type = double4; };
-
-// LOWER = true : unit-lower forward substitution, block rows in increasing order.
-// LOWER = false: upper backward substitution (non-unit diagonal), decreasing order;
-//                X[rows] = (double) z  (accumulate = 0)  or  X += (double) z  (accumulate = 1).
-template <typename T, bool LOWER>
-__global__ void __launch_bounds__(ST, 1)
-tri_solve_kernel(const T *__restrict__ W, int64_t ldw, int64_t n, int nrhs, T *Y, int64_t ldy, double *X,
-                 int accumulate, unsigned *flags, unsigned *ticket)
+__device__ __forceinline__ void spin_until(const unsigned *flag, unsigned epoch)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *Ld = reinterpret_cast<T *>(smem_raw);             // [BS][LDD]   Ld[j][i] = Tri(i, j) of the diagonal block
-    T *ys = Ld + BS * LDD;                               // [BS][MAXR]  published block J / final block I
-    __shared__ int s_blk;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nblk = (int)ceil_div(n, BS);
-    if (tid == 0) {
-        const unsigned t = atomicAdd(ticket, 1u);
-        s_blk = LOWER ? (int)t : nblk - 1 - (int)t;
-    }
-    __syncthreads();
-    const int I = s_blk;
-    const int64_t i0 = (int64_t)I * BS;
-    const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
+    while (ld_relaxed_u32(flag) != epoch) { }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 
-    // stage the diagonal block transposed (Ld[j][i] = Tri(i0+i, i0+j)) and this block's
-    // right-hand side first: neither depends on other blocks, so this overlaps the waits.
-    // Warp-per-row, lanes along j: coalesced 128 B reads, conflict-free transposed stores.
-    for (int i = warp; i < BS; i += ST / 32) {
-#pragma unroll
-        for (int k = 0; k < BS / 32; ++k) {
-            const int j = lane + 32 * k;
-            Ld[j * LDD + i] = (i < nr && j < nr) ? W[(i0 + i) * ldw + i0 + j] : T(0);
-        }
-    }
-    T rhs[MAXR];
-    {
-        const int rr = tid >> 1;
-#pragma unroll
-        for (int c = 0; c < MAXR; ++c) rhs[c] = (c < nrhs && rr < nr && (tid & 1) == 0) ? Y[c * ldy + i0 + rr] : T(0);
-    }
+#ifdef MP_SOLVE_TRACE
+__device__ unsigned long long g_strace[4096][6];
+// the volatile shared load forces a deferred-blocking bar.sync to complete before the clock read
+#define STRACE(t, k) do { if (tid == 0 && (t) < 4096) { const int d_ = *(volatile int *)&s_nready; \
+    g_strace[(t)][(k)] = (unsigned long long)clock64() + (unsigned long long)(d_ & 0); } } while (0)
+#else
+#define STRACE(t, k) do { } while (0)
+#endif
 
-    // ---- off-diagonal GEMV part: 2 threads per row, each half of every tile
-    const int r = tid >> 1, half = tid & 1;
-    T psum[MAXR];
+template <typename T>
+struct SweepArgs {
+    T *Y;                  // [nrhs][n] right-hand sides in, solutions out
+    double *X;             // [nrhs][n] binary64 solution (upper sweep only)
+    T *F;                  // [nrhs][n] far partial sums
+    unsigned *yflag, *fflag;
+    int64_t n;
+    int nrhs, nblk, accumulate;
+    unsigned epoch;
+};
+
+__device__ __forceinline__ float rcp_rn(float v) { return __frcp_rn(v); }
+__device__ __forceinline__ double rcp_rn(double v) { return __drcp_rn(v); }
+
+// logical block t -> row block index
+template <bool LOWER>
+__device__ __forceinline__ int blk_of(int t, int nblk) { return LOWER ? t : nblk - 1 - t; }
+
+// acc[p][c] += tile row (r0 + p*rstep) . y(c) over this thread's 8 columns tq*4 + 32m (m = 0, 1)
+template <typename T, int R, int NP>
+__device__ __forceinline__ void tile_gemv(const T *__restrict__ tl, const T *__restrict__ yv, int r0, int rstep, int tq,
+                                          int nrhs, T (&acc)[NP][R])
+{
 #pragma unroll
-    for (int c = 0; c < MAXR; ++c) psum[c] = T(0);
-    // visit the off-diagonal blocks in the order they become ready: increasing J for
-    // the forward sweep, DECREASING J for the backward sweep (block nblk-1 is published first)
-    const int ntiles = LOWER ? I : nblk - 1 - I;
-    for (int t = 0; t < ntiles; ++t) {
-        const int J = LOWER ? t : nblk - 1 - t;
-        const int64_t j0 = (int64_t)J * BS;
-        const int nc = (int)((n - j0 < (int64_t)BS) ? (n - j0) : (int64_t)BS);
-        if (tid == 0) {
-            // relaxed polling (an acquire load per poll would invalidate L1 every time),
-            // then one acquire fence once the flag is seen
-            while (ld_relaxed_u32(flags + J) == 0u) { }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        }
-        __syncthreads();
-        for (int idx = tid; idx < nc * nrhs; idx += ST) {
-            const int j = idx % nc, c = idx / nc;
-            ys[j * MAXR + c] = __ldcg(Y + c * ldy + j0 + j);
-        }
-        __syncthreads();
-        if (r < nr) {
-            const T *lrow = W + (i0 + r) * ldw + j0;
-            const int jlo = half * (BS / 2);
-            const int jhi = (nc < jlo + BS / 2) ? nc : jlo + BS / 2;
-            if (nc == BS) {
-                using V = typename V4<T>::type;
-#pragma unroll 4
-                for (int j = jlo; j < jhi; j += 4) {
-                    const V lv = *reinterpret_cast<const V *>(lrow + j);
-                    const T *yj = ys + j * MAXR;
+    for (int m = 0; m < 2; ++m) {
+        const int j = tq * 4 + 32 * m;
 #pragma unroll
-                    for (int c = 0; c < MAXR; ++c) {
-                        if (c < nrhs) {
-                            psum[c] = fma(lv.x, yj[c], psum[c]);
-                            psum[c] = fma(lv.y, yj[MAXR + c], psum[c]);
-                            psum[c] = fma(lv.z, yj[2 * MAXR + c], psum[c]);
-                            psum[c] = fma(lv.w, yj[3 * MAXR + c], psum[c]);
-                        }
-                    }
-                }
+        for (int p = 0; p < NP; ++p) {
+            const int row = r0 + p * rstep;
+            T l[4];
+            if constexpr (sizeof(T) == 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(tl + Sw<T>::off(row, j));
+                l[0] = v.x; l[1] = v.y; l[2] = v.z; l[3] = v.w;
             } else {
-                for (int j = jlo; j < jhi; ++j) {
-                    const T lv = lrow[j];
-#pragma unroll
-                    for (int c = 0; c < MAXR; ++c)
-                        if (c < nrhs) psum[c] = fma(lv, ys[j * MAXR + c], psum[c]);
-                }
+                const double2 v0 = *reinterpret_cast<const double2 *>(tl + Sw<T>::off(row, j));
+                const double2 v1 = *reinterpret_cast<const double2 *>(tl + Sw<T>::off(row, j + 2));
+                l[0] = v0.x; l[1] = v0.y; l[2] = v1.x; l[3] = v1.y;
             }
-        }
-        __syncthreads();
-    }
-    // combine the two halves; rhs block I minus the off-diagonal sums -> ys[r][c]
 #pragma unroll
-    for (int c = 0; c < MAXR; ++c) psum[c] += __shfl_xor_sync(0xffffffffu, psum[c], 1);
-    if (half == 0 && r < nr) {
-#pragma unroll
-        for (int c = 0; c < MAXR; ++c)
-            if (c < nrhs) ys[r * MAXR + c] = rhs[c] - psum[c];
-    }
-    __syncthreads();
-
-    // ---- substitution on the diagonal block, in 32-row sub-blocks (forward: top-down,
-    //      backward: bottom-up).  The 32 x 32 triangle: lane i keeps row i of the triangle in
-    //      registers and its rhs b_i; a fully unrolled chain x_j = shfl(b, j), b_i -= t_ij x_j
-    //      (one warp per right-hand side).  The rows of the block not yet solved then get the
-    //      sub-block's contribution from all 256 threads.
-#pragma unroll 1
-    for (int sbi = 0; sbi < BS / 32; ++sbi) {
-        const int sb = LOWER ? sbi : BS / 32 - 1 - sbi;
-        const int s0 = sb * 32;
-        if (s0 >= nr) continue;
-        const int i = s0 + lane;                           // this lane's row
-        for (int c = warp; c < nrhs; c += ST / 32) {
-            T trow[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) trow[j] = Ld[(s0 + j) * LDD + i];
-            T b = i < nr ? ys[i * MAXR + c] : T(0);
-            if (LOWER) {
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const T xj = __shfl_sync(0xffffffffu, b, j);
-                    if (lane > j && s0 + j < nr) b = fma(-trow[j], xj, b);
+            for (int c = 0; c < R; ++c)
+                if (c < nrhs) {
+                    const T *yp = yv + c * BS + j;
+                    acc[p][c] = fma(l[0], yp[0], fma(l[1], yp[1], fma(l[2], yp[2], fma(l[3], yp[3], acc[p][c]))));
                 }
-            } else {
-#pragma unroll
-                for (int j = 31; j >= 0; --j) {
-                    if (s0 + j < nr) {
-                        if (lane == j) b = b / trow[j];        // U(j, j): non-unit diagonal
-                        const T xj = __shfl_sync(0xffffffffu, b, j);
-                        if (lane < j) b = fma(-trow[j], xj, b);
-                    }
-                }
-            }
-            if (i < nr) ys[i * MAXR + c] = b;
         }
-        __syncthreads();
-        // contribution of the 32 solved rows to the block rows still to be solved
-        const int rlo = LOWER ? s0 + 32 : 0, rhi = LOWER ? nr : s0;
-        const int nrem = rhi > rlo ? rhi - rlo : 0;
-        for (int idx = tid; idx < nrem * nrhs; idx += ST) {
-            const int r = rlo + idx % nrem, c = idx / nrem;
-            T acc = ys[r * MAXR + c];
-#pragma unroll 8
-            for (int j = 0; j < 32; ++j)
-                if (s0 + j < nr) acc = fma(-Ld[(s0 + j) * LDD + r], ys[(s0 + j) * MAXR + c], acc);
-            ys[r * MAXR + c] = acc;
-        }
-        __syncthreads();
-    }
-    // publish the solved block (and, backward, x += z in binary64: step 7)
-    for (int idx = tid; idx < nr * nrhs; idx += ST) {
-        const int r = idx % nr, c = idx / nr;
-        const T v = ys[r * MAXR + c];
-        Y[c * ldy + i0 + r] = v;
-        if (!LOWER) {
-            double *xp = X + c * ldy + i0 + r;
-            *xp = accumulate ? *xp + (double)v : (double)v;
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        st_release_u32(flags + I, 1u);
     }
 }
 
+// reduce over the 8 threads of a row (lanes 8g .. 8g+7) and subtract from dst[c*BS + row]
+template <typename T, int R, int NP>
+__device__ __forceinline__ void reduce_sub(T (&acc)[NP][R], int r0, int rstep, int tq, int nrhs, T *dst)
+{
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+            if (c < nrhs) {
+                T v = acc[p][c];
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                if (tq == 0) dst[c * BS + r0 + p * rstep] -= v;
+            }
+}
+
+// rsb = Y - F for block t (one warp)
+template <typename T, bool LOWER>
+__device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane, T *rsb)
+{
+    constexpr int DN = SCfg<T>::DN;
+    const int I = blk_of<LOWER>(t, a.nblk);
+    const int64_t i0 = (int64_t)I * BS, n = a.n;
+    const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
+    const bool far = t >= DN + 1;
+#ifdef MP_SOLVE_TRACE
+    if (lane == 0 && t < 4096) g_strace[t][4] = (unsigned long long)clock64();
+#endif
+    if (far && lane == 0) spin_until(a.fflag + I, a.epoch);
+    __syncwarp();
+#ifdef MP_SOLVE_TRACE
+    if (lane == 0 && t < 4096) g_strace[t][5] = (unsigned long long)clock64();
+#endif
+    for (int idx = lane; idx < a.nrhs * BS; idx += 32) {
+        const int c = idx / BS, r = idx - c * BS;
+        T v = T(0);
+        if (r < nr) {
+            v = a.Y[(int64_t)c * n + i0 + r];
+            if (far) v -= __ldcg(a.F + (int64_t)c * n + i0 + r);
+        }
+        rsb[idx] = v;
+    }
+}
+
+// 8 consecutive elements (r, c0 .. c0+7) of a swizzled tile, c0 % 8 == 0: 16-byte loads
 template <typename T>
-size_t tri_smem() { return (size_t)BS * LDD * sizeof(T) + (size_t)BS * MAXR * sizeof(T); }
+__device__ __forceinline__ void ld8(const T *__restrict__ tl, int r, int c0, T (&o)[8])
+{
+    constexpr int EPC = Sw<T>::EPC;
+#pragma unroll
+    for (int q = 0; q < 8 / EPC; ++q) {
+        const T *p = tl + Sw<T>::off(r, c0 + q * EPC);
+        if constexpr (sizeof(T) == 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(p);
+            o[4 * q] = v.x; o[4 * q + 1] = v.y; o[4 * q + 2] = v.z; o[4 * q + 3] = v.w;
+        } else {
+            const double2 v = *reinterpret_cast<const double2 *>(p);
+            o[2 * q] = v.x; o[2 * q + 1] = v.y;
+        }
+    }
+}
+
+// diagonal block solve for one right-hand side (one warp): lanes own rows lane and lane+32;
+// rows are finished in 8-row chunks whose 8 x 8 triangle every lane solves redundantly.
+// rinv: per-warp shared scratch of BS reciprocals (upper sweep).
+template <typename T, bool LOWER>
+__device__ __forceinline__ void diag_solve(const T *__restrict__ dg, T *__restrict__ rinv, int lane, int nr, T &v0, T &v1)
+{
+    T ri0 = T(1), ri1 = T(1), u0 = T(1), u1 = T(1);
+    if (!LOWER) {
+        u0 = dg[Sw<T>::off(lane, lane)];
+        u1 = dg[Sw<T>::off(lane + 32, lane + 32)];
+        ri0 = (lane < nr && u0 != T(0)) ? rcp_rn(u0) : T(0);
+        ri1 = (lane + 32 < nr && u1 != T(0)) ? rcp_rn(u1) : T(0);
+        rinv[lane] = ri0;
+        rinv[lane + 32] = ri1;
+        __syncwarp();
+    }
+    constexpr int AHEAD = sizeof(T) == 4 ? 1 : 0;            // operand prefetch distance (chunks)
+    T Lc[AHEAD + 1][8][8], Lr[AHEAD + 1][2][8], Ri[AHEAD + 1][8];
+#pragma unroll
+    for (int kk = 0; kk < BS / 8; ++kk) {
+#pragma unroll
+        for (int kl = (kk == 0 ? 0 : kk + AHEAD); kl <= kk + AHEAD && kl < BS / 8; ++kl) {
+            const int k = LOWER ? kl : BS / 8 - 1 - kl;
+            const int r0 = 8 * k, cb = AHEAD ? (kl & 1) : 0;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) ld8<T>(dg, r0 + m, r0, Lc[cb][m]);
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) ld8<T>(dg, lane + 32 * rr, r0, Lr[cb][rr]);
+            if (!LOWER)
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Ri[cb][i] = rinv[r0 + i];
+        }
+        const int k = LOWER ? kk : BS / 8 - 1 - kk;
+        const int r0 = 8 * k, cb = AHEAD ? (kk & 1) : 0;
+        T bb[8], xx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) bb[i] = __shfl_sync(0xffffffffu, k < 4 ? v0 : v1, (r0 + i) & 31);
+        if (LOWER) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                xx[i] = (r0 + i < nr) ? bb[i] : T(0);
+#pragma unroll
+                for (int m = i + 1; m < 8; ++m) bb[m] = fma(-Lc[cb][m][i], xx[i], bb[m]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 7; i >= 0; --i) {
+                const T u = Lc[cb][i][i], ri = Ri[cb][i];
+                T q = bb[i] * ri;
+                q = fma(fma(-u, q, bb[i]), ri, q);
+                xx[i] = (r0 + i < nr) ? q : T(0);
+#pragma unroll
+                for (int m = 0; m < i; ++m) bb[m] = fma(-Lc[cb][m][i], xx[i], bb[m]);
+            }
+        }
+        // own rows: the same operations in the same order as the redundant chunk solve, so
+        // in-chunk rows reproduce xx bit for bit (no dynamic register indexing)
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int row = lane + 32 * rr;
+            T sv = rr ? v1 : v0;
+            if (LOWER) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (r0 + i < row) sv = fma(-Lr[cb][rr][i], xx[i], sv);
+                if (row >= r0 && row < r0 + 8 && row >= nr) sv = T(0);
+            } else {
+#pragma unroll
+                for (int i = 7; i >= 0; --i)
+                    if (r0 + i > row) sv = fma(-Lr[cb][rr][i], xx[i], sv);
+                if (row >= r0 && row < r0 + 8) {
+                    const T u = rr ? u1 : u0, ri = rr ? ri1 : ri0;
+                    T q = sv * ri;
+                    q = fma(fma(-u, q, sv), ri, q);
+                    sv = row < nr ? q : T(0);
+                }
+            }
+            if (rr) v1 = sv; else v0 = sv;
+        }
+    }
+}
+
+template <typename T, bool LOWER, int R>
+__global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant__ CUtensorMap tmW, SweepArgs<T> a)
+{
+    using C = SCfg<T>;
+    constexpr int DN = C::DN;
+    constexpr int TILE = BS * BS;
+    constexpr uint32_t TB = (uint32_t)tile_bytes<T>();
+    extern __shared__ unsigned char smem_raw[];
+    // 1 KB alignment by pointer arithmetic on the shared array (keeps the shared state space: LDS)
+    T *sm = reinterpret_cast<T *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    __shared__ __align__(8) uint64_t full[16], empty[16];
+    __shared__ int s_nready;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nblk = a.nblk, nrhs = a.nrhs;
+    const int64_t n = a.n;
+
+    if (blockIdx.x == 0) {
+        // =================================================================== chain CTA
+        constexpr int NST = C::CHB * (1 + DN);
+        constexpr int NCH = (NCW + 2) * 32;                   // compute + publisher + prep threads
+        T *tiles = sm;                                        // [NST][TILE] (1 KB aligned)
+        T *ys = tiles + (size_t)NST * TILE;                   // [DN+1][MAXR][BS] last solved blocks
+        T *rs = ys + (size_t)(DN + 1) * MAXR * BS;            // [2][MAXR][BS]  right-hand sides
+        T *nacc = rs + 2 * (size_t)MAXR * BS;                 // [2][MAXR][BS]  near tiles d >= 2, precomputed
+        T *rinvs = nacc + 2 * (size_t)MAXR * BS;              // [NCW][BS] reciprocals of the U diagonal
+        if (tid == 0) {
+            for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        for (int i = tid; i < (DN + 1) * MAXR * BS + 4 * MAXR * BS + NCW * BS; i += NTH) ys[i] = T(0);
+        __syncthreads();
+        if (warp == WPROD) {
+            // ---------------- producer: diagonal + DN near tiles of every block, in order
+            if (lane == 0) {
+                for (int t = 0; t < nblk; ++t) {
+                    const int I = blk_of<LOWER>(t, nblk);
+                    const int b = t % C::CHB;
+                    const uint32_t ph = (uint32_t)((t / C::CHB) & 1);
+                    for (int k = 0; k <= DN; ++k) {
+                        const int s = b * (1 + DN) + k;
+                        mbar_wait(&empty[s], ph ^ 1u);
+                        mbar_expect_tx(&full[s], TB);
+                        // k = 0: diagonal tile; k = d: column block of the logically earlier
+                        // block t - d (t - d < 0: out of range, zero-filled by the TMA unit)
+                        tma_tile<T>(tiles + (size_t)s * TILE, &tmW, &full[s], LOWER ? I - k : I + k, I);
+                    }
+                }
+            }
+            return;
+        }
+        if (warp == WPREP) prep_rhs<T, LOWER>(a, 0, lane, rs);
+        nbar_sync(1, NCH);
+        const int nsolv = nrhs < NCW ? nrhs : NCW;
+        // idle warps precompute the next block's near tiles d >= 2 (needs a second ring slot)
+        const bool split = nsolv <= NCW / 2 && C::CHB > 1;
+        const int tr = tid >> 3, tq = tid & 7;                // rows tr, tr+32; cols tq*4 + 32m
+        for (int t = 0; t < nblk; ++t) {
+            const int I = blk_of<LOWER>(t, nblk);
+            const int64_t i0 = (int64_t)I * BS;
+            const int nr = (int)std::min<int64_t>(BS, n - i0);
+            const int b = t % C::CHB;
+            const uint32_t ph = (uint32_t)((t / C::CHB) & 1);
+            const int slot = t % (DN + 1);
+            T *rsb = rs + (size_t)(t & 1) * MAXR * BS;
+            const T *dg = tiles + (size_t)(b * (1 + DN)) * TILE;
+            STRACE(t, 0);
+            // ---- phase A: near tile d = 1 (all DN when not split): rs -= T(I, J_d) y_{t-d} (+ nacc)
+            if (warp < NCW) {
+                T acc[2][R];
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+                const int dmax = split ? 1 : DN;
+                for (int d = 1; d <= dmax; ++d) {
+                    const int s = b * (1 + DN) + d;
+                    mbar_wait(&full[s], ph);
+                    tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, ys + (size_t)((t - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS,
+                                       tr, 32, tq, nrhs, acc);
+                }
+                if (split && tq == 0) {
+                    const T *nb = nacc + (size_t)(t & 1) * MAXR * BS;
+#pragma unroll
+                    for (int p = 0; p < 2; ++p)
+#pragma unroll
+                        for (int c = 0; c < R; ++c)
+                            if (c < nrhs) acc[p][c] += nb[c * BS + tr + 32 * p];
+                }
+                reduce_sub<T, R, 2>(acc, tr, 32, tq, nrhs, rsb);
+            }
+            nbar_sync(1, NCH);
+            STRACE(t, 1);
+            // ---- phase B
+            if (warp < nsolv) {
+                mbar_wait(&full[b * (1 + DN)], ph);
+                for (int c = warp; c < nrhs; c += NCW) {
+                    double xo0 = 0.0, xo1 = 0.0;              // x of the owned rows, fetched early
+                    if (!LOWER && a.accumulate) {
+                        if (lane < nr) xo0 = a.X[(int64_t)c * n + i0 + lane];
+                        if (lane + 32 < nr) xo1 = a.X[(int64_t)c * n + i0 + lane + 32];
+                    }
+                    T v0 = rsb[c * BS + lane], v1 = rsb[c * BS + lane + 32];
+                    diag_solve<T, LOWER>(dg, rinvs + warp * BS, lane, nr, v0, v1);
+                    // y (or z) to shared (near tiles of later blocks) and global; x (+)= z
+                    ys[(size_t)slot * MAXR * BS + c * BS + lane] = v0;
+                    ys[(size_t)slot * MAXR * BS + c * BS + lane + 32] = v1;
+                    if (lane < nr) {
+                        a.Y[(int64_t)c * n + i0 + lane] = v0;
+                        if (!LOWER) a.X[(int64_t)c * n + i0 + lane] = xo0 + (double)v0;
+                    }
+                    if (lane + 32 < nr) {
+                        a.Y[(int64_t)c * n + i0 + lane + 32] = v1;
+                        if (!LOWER) a.X[(int64_t)c * n + i0 + lane + 32] = xo1 + (double)v1;
+                    }
+                }
+                STRACE(t, 2);
+                nbar_arrive(2, (nsolv + 1) * 32);             // hand the stores to the publisher
+            } else if (warp == WPUB) {
+                // publish y_I for the helpers: the barrier orders the solvers' stores before the
+                // release (cumulativity), so the solvers never wait on the fence
+                nbar_sync(2, (nsolv + 1) * 32);
+                if (lane == 0) {
+                    __threadfence();
+                    st_release_u32(a.yflag + I, a.epoch);
+                }
+            } else if (warp == WPREP) {
+                if (t + 1 < nblk) prep_rhs<T, LOWER>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * MAXR * BS);
+            } else if (split && warp >= NCW / 2 && warp < NCW && t + 1 < nblk) {
+                // next block's near tiles d = 2..DN (their y blocks are all solved)
+                const int lt = tid - (NCW / 2) * 32;          // 0..127: rows (lt>>3) + 16p, cols (lt&7)*4 + 32m
+                const int b1 = (t + 1) % C::CHB;
+                const uint32_t ph1 = (uint32_t)(((t + 1) / C::CHB) & 1);
+                T acc[4][R];
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+                for (int d = 2; d <= DN; ++d) {
+                    const int s = b1 * (1 + DN) + d;
+                    mbar_wait(&full[s], ph1);
+                    tile_gemv<T, R, 4>(tiles + (size_t)s * TILE,
+                                       ys + (size_t)((t + 1 - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS, lt >> 3, 16,
+                                       lt & 7, nrhs, acc);
+                }
+                T *nb = nacc + (size_t)((t + 1) & 1) * MAXR * BS;
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c)
+                        if (c < nrhs) {
+                            T v = acc[p][c];
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            v += __shfl_xor_sync(0xffffffffu, v, 4);
+                            if ((lt & 7) == 0) nb[c * BS + (lt >> 3) + 16 * p] = v;
+                        }
+            }
+            nbar_sync(1, NCH);                                 // ys[slot], rs/nacc[t+1] ready
+            STRACE(t, 3);
+            if (tid == 0)                                      // every tile of block t consumed
+                for (int k = 0; k <= DN; ++k) mbar_arrive(&empty[b * (1 + DN) + k]);
+        }
+        return;
+    }
+
+    // =================================================================== helper CTAs
+    const int h = (int)blockIdx.x - 1, H = (int)gridDim.x - 1;
+    constexpr int HS = C::HS, YB = C::YB, MAXOWN = C::MAXOWN;
+    constexpr int NHC = NCW * 32;
+    T *tiles = sm;                                            // [HS][TILE]
+    T *yb = tiles + (size_t)HS * TILE;                        // [YB][MAXR][BS]
+    T *accs = yb + (size_t)YB * MAXR * BS;                    // [MAXOWN][MAXR][BS]
+    int town[MAXOWN];
+    int nown = 0;
+    for (int t = DN + 1 + h; t < nblk && nown < MAXOWN; t += H) town[nown++] = t;
+    if (nown == 0) return;
+    const int tmax = town[nown - 1] - DN - 1;                 // last y block this CTA consumes
+    if (tid == 0) {
+        for (int s = 0; s < HS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int i = tid; i < MAXOWN * MAXR * BS; i += NTH) accs[i] = T(0);
+    __syncthreads();
+    if (warp == WPROD) {
+        // ---------------- producer: tiles (I_o, J_tp) in consumption order
+        if (lane == 0) {
+            int seq = 0;
+            for (int tp = 0; tp <= tmax; ++tp) {
+                const int J = blk_of<LOWER>(tp, nblk);
+                for (int o = 0; o < nown; ++o) {
+                    if (town[o] < tp + DN + 1) continue;
+                    const int s = seq % HS;
+                    mbar_wait(&empty[s], (uint32_t)(((seq / HS) & 1) ^ 1));
+                    mbar_expect_tx(&full[s], TB);
+                    tma_tile<T>(tiles + (size_t)s * TILE, &tmW, &full[s], J, blk_of<LOWER>(town[o], nblk));
+                    ++seq;
+                }
+            }
+        }
+        return;
+    }
+    if (warp >= NCW) return;
+    const int tr = tid >> 3, tq = tid & 7;
+    int seq = 0;
+    int tp = 0;
+    while (tp <= tmax) {
+        // how many consecutive y blocks are published (at least one: wait for it)
+        if (tid == 0) {
+            spin_until(a.yflag + blk_of<LOWER>(tp, nblk), a.epoch);
+            int k = 1;
+            while (k < YB && tp + k <= tmax && ld_relaxed_u32(a.yflag + blk_of<LOWER>(tp + k, nblk)) == a.epoch) ++k;
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            s_nready = k;
+        }
+        nbar_sync(1, NHC);
+        const int nb = s_nready;
+        for (int idx = tid; idx < nb * nrhs * BS; idx += NHC) {
+            const int k = idx / (nrhs * BS), rem = idx - k * nrhs * BS;
+            const int c = rem / BS, r = rem - c * BS;
+            const int64_t j = (int64_t)blk_of<LOWER>(tp + k, nblk) * BS + r;
+            yb[(size_t)k * MAXR * BS + c * BS + r] = j < n ? __ldcg(a.Y + (int64_t)c * n + j) : T(0);
+        }
+        nbar_sync(1, NHC);
+        for (int k = 0; k < nb; ++k, ++tp) {
+            const T *yv = yb + (size_t)k * MAXR * BS;
+            for (int o = 0; o < nown; ++o) {
+                if (town[o] < tp + DN + 1) continue;
+                const int s = seq % HS;
+                mbar_wait(&full[s], (uint32_t)((seq / HS) & 1));
+                T acc[2][R];
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+                tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, yv, tr, 32, tq, nrhs, acc);
+#pragma unroll
+                for (int p = 0; p < 2; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c)
+                        if (c < nrhs) {
+                            T v = acc[p][c];
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            v += __shfl_xor_sync(0xffffffffu, v, 4);
+                            if (tq == 0) accs[((size_t)o * MAXR + c) * BS + tr + 32 * p] += v;
+                        }
+                nbar_sync(1, NHC);
+                if (tid == 0) mbar_arrive(&empty[s]);
+                ++seq;
+                if (town[o] == tp + DN + 1) {                 // F of block o complete: publish
+                    const int64_t i0 = (int64_t)blk_of<LOWER>(town[o], nblk) * BS;
+                    for (int idx = tid; idx < nrhs * BS; idx += NHC) {
+                        const int c = idx / BS, r = idx - c * BS;
+                        if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * MAXR + c) * BS + r];
+                    }
+                    __threadfence();
+                    nbar_sync(1, NHC);
+                    if (tid == 0) st_release_u32(a.fflag + blk_of<LOWER>(town[o], nblk), a.epoch);
+                }
+            }
+        }
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tm = nullptr;
+
+template <typename T>
+void encode_w_map(CUtensorMap *map, const T *W, int64_t ldw, int64_t n)
+{
+    if (!g_encode_tm) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        MP_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled", __LINE__};
+        g_encode_tm = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)ldw, (cuuint64_t)n};
+    cuuint64_t gstride[1] = {(cuuint64_t)ldw * sizeof(T)};
+    cuuint32_t box[2] = {(cuuint32_t)Sw<T>::EPB, (cuuint32_t)BS};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode_tm(map, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                             const_cast<T *>(W), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled (solve) failed", __LINE__};
+}
+
+template <typename T, bool LOWER>
+void launch_sweep(const CUtensorMap &tm, SweepArgs<T> &a, int grid, cudaStream_t s)
+{
+    auto kern = a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1> : tri_sweep_kernel<T, LOWER, MAXR>;
+    func_smem_once((const void *)kern, sweep_smem<T>());
+    void *args[] = {(void *)&tm, (void *)&a};
+    MP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(NTH), args, sweep_smem<T>(), s));
+}
 
 }  // namespace
 
 int solve_block_rows() { return BS; }
+
+size_t solve_flag_words(int64_t n) { return 4 * (size_t)ceil_div(n, BS); }
 
 template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
                      SolveScratch &ss, cudaStream_t s)
 {
     const int nblk = (int)ceil_div(n, BS);
-    const size_t smem = tri_smem<T>();
-    auto kl = tri_solve_kernel<T, true>;
-    auto ku = tri_solve_kernel<T, false>;
-    func_smem_once((const void *)kl, smem);
-    func_smem_once((const void *)ku, smem);
+    CUtensorMap tm;
+    encode_w_map<T>(&tm, W, ldw, n);
+    int dev = 0, sms = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int helpers = std::max(1, std::min(sms - 1, nblk - SCfg<T>::DN - 1));
+    if (ceil_div(std::max(0, nblk - SCfg<T>::DN - 1), helpers) > SCfg<T>::MAXOWN)
+        throw CudaError{cudaErrorInvalidValue, "matrix too large for the triangular-solve helper grid", __LINE__};
     for (int64_t c0 = 0; c0 < nrhs; c0 += MAXR) {
         const int nc = (int)std::min<int64_t>(MAXR, nrhs - c0);
-        MP_CUDA(cudaMemsetAsync(ss.flags, 0, sizeof(unsigned) * (2 * (size_t)nblk), s));
-        MP_CUDA(cudaMemsetAsync(ss.tickets, 0, sizeof(unsigned) * 2, s));
-        kl<<<nblk, ST, smem, s>>>(W, ldw, n, nc, Y + c0 * n, n, X + c0 * n, accumulate, ss.flags, ss.tickets);
-        MP_LAUNCH_CHECK();
-        ku<<<nblk, ST, smem, s>>>(W, ldw, n, nc, Y + c0 * n, n, X + c0 * n, accumulate, ss.flags + nblk,
-                                  ss.tickets + 1);
-        MP_LAUNCH_CHECK();
+        SweepArgs<T> a;
+        a.Y = Y + c0 * n;
+        a.X = X + c0 * n;
+        a.F = static_cast<T *>(ss.F);
+        a.n = n;
+        a.nrhs = nc;
+        a.nblk = nblk;
+        a.accumulate = accumulate;
+        a.yflag = ss.flags;
+        a.fflag = ss.flags + nblk;
+        a.epoch = ++ss.epoch;
+        launch_sweep<T, true>(tm, a, 1 + helpers, s);
+        a.yflag = ss.flags + 2 * nblk;
+        a.fflag = ss.flags + 3 * nblk;
+        launch_sweep<T, false>(tm, a, 1 + helpers, s);
         g_launches += 2;
     }
 }
