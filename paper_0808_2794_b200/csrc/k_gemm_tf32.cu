@@ -12,13 +12,13 @@
 // the epilogue each thread owns one column and a warp reads / writes 128 contiguous
 // bytes per row: the read-modify-write of C is fully coalesced.
 //
-// Kernel structure (persistent, one CTA per SM, 256 threads):
+// Kernel structure (persistent, one CTA per SM, 384 threads):
 //   warp 0     TMA producer: per 32-deep K chunk, 4 boxes (Uhi, Ulo 128x32; Lhi, Llo 256x32)
 //              SWIZZLE_128B into a 2-stage shared-memory ring, mbarrier expect_tx
 //   warp 1     MMA issuer (one thread): 4 k-steps x 3 tcgen05.mma.cta_group::1.kind::tf32
 //              (M=128, N=256, K=8) per chunk, tcgen05.commit -> ring slot free / accumulator full
 //   warp 2     TMEM allocator (512 columns = two 128x256 fp32 accumulators)
-//   warps 4..7 epilogue: tcgen05.ld 32x32b.x32 -> C -= D (coalesced RMW), accumulator free
+//   warps 4..11 epilogue: tcgen05.ld 32x32b.x32 -> C -= D (coalesced RMW), accumulator free
 // Two accumulators let the epilogue of tile t overlap the MMAs of tile t+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -38,7 +38,7 @@ constexpr int STAGES = 2;
 constexpr int A_BYTES = TM_COLS * KC * 4;     // 16 KB
 constexpr int B_BYTES = TM_ROWS * KC * 4;     // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 96 KB
-constexpr int GT = 256;
+constexpr int GT = 384;            // 4 role warps + 8 epilogue warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -124,6 +124,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
+{
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __global__ void __launch_bounds__(GT, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_constant__ CUtensorMap tmUl,
                    const __grid_constant__ CUtensorMap tmLh, const __grid_constant__ CUtensorMap tmLl,
@@ -142,7 +156,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 4); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&acc_full[a], 1); mbar_init(&acc_empty[a], 8); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 2) {
@@ -209,33 +223,41 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
         }
     } else if (warp >= 4) {
         // ================= epilogue: C[i][j] -= D^T[j][i]
-        const int ew = warp - 4;                                       // TMEM lanes 32*ew .. 32*ew+31
+        // 8 warps: TMEM lane quarter q = warp % 4 (columns j), row half h (TMEM columns).
+        // C rows are loaded one 32-row group ahead (the first group before the accumulator
+        // is ready), so each SM keeps ~64 KB of C loads in flight.
+        const int q = warp & 3, h = (warp - 4) >> 2;
         uint32_t acc_phase[2] = {0, 0};
         int a = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int tn = t % tiles_n, tm = t / tiles_n;
-            const int j = tn * TM_COLS + ew * 32 + lane;
+            const int j = tn * TM_COLS + q * 32 + lane;
+            const int i0 = tm * TM_ROWS + h * (TM_ROWS / 2);
+            const bool jv = j < N;
+            constexpr int GR = 16, NG = TM_ROWS / 2 / GR, PD = 2;   // 16-row groups, 2 groups ahead
+            float cb[PD + 1][GR];
+            const int nrow_ok = jv ? M : 0;                        // rows i < nrow_ok exist
+            auto load_group = [&](float (&dst)[GR], int ib) {
+                const float *cp = C + (int64_t)ib * ldc + j;
+#pragma unroll
+                for (int rr = 0; rr < GR; ++rr) dst[rr] = (ib + rr < nrow_ok) ? __ldcs(cp + (int64_t)rr * ldc) : 0.f;
+            };
+#pragma unroll
+            for (int g = 0; g < PD; ++g) load_group(cb[g], i0 + GR * g);
             mbar_wait(&acc_full[a], acc_phase[a]);
             acc_phase[a] ^= 1;
             tc_fence_after();
-            const uint32_t tacc = tmem_base + ((uint32_t)(ew * 32) << 16) + (uint32_t)(a * TM_ROWS);
-            const int i0 = tm * TM_ROWS;
-            for (int r0 = 0; r0 < TM_ROWS; r0 += 32) {
-                float v[32];
-                tmem_ld32(tacc + (uint32_t)r0, v);
-                if (j < N) {
-                    float c[32];
+            const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * TM_ROWS + h * (TM_ROWS / 2));
 #pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) {
-                        const int i = i0 + r0 + rr;
-                        c[rr] = i < M ? __ldcs(C + (int64_t)i * ldc + j) : 0.f;
-                    }
+            for (int g = 0; g < NG; ++g) {
+                if (g + PD < NG) load_group(cb[(g + PD) % (PD + 1)], i0 + GR * (g + PD));
+                float v[GR];
+                tmem_ld16(tacc + (uint32_t)(GR * g), v);
+                const int ib = i0 + GR * g;
+                float *cp = C + (int64_t)ib * ldc + j;
 #pragma unroll
-                    for (int rr = 0; rr < 32; ++rr) {
-                        const int i = i0 + r0 + rr;
-                        if (i < M) __stcs(C + (int64_t)i * ldc + j, c[rr] - v[rr]);
-                    }
-                }
+                for (int rr = 0; rr < GR; ++rr)
+                    if (ib + rr < nrow_ok) __stcs(cp + (int64_t)rr * ldc, cb[g % (PD + 1)][rr] - v[rr]);
             }
             tc_fence_before();
             __syncwarp();

@@ -26,7 +26,7 @@ constexpr int ROWS = 2 * RT;         // rows per row tile
 constexpr int MAXR = 16;
 constexpr int JU = 8;                // column unroll (loads in flight per thread)
 
-template <bool VEC>
+template <bool VEC, int R>
 __global__ void __launch_bounds__(RT)
 residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int nrhs,
                         const double *__restrict__ X, double *__restrict__ partial, int64_t cols_per_split,
@@ -40,12 +40,12 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
     for (int64_t idx = threadIdx.x; idx < (j1 - j0) * nrhs; idx += RT) {
         const int64_t jj = idx / nrhs;
         const int c = (int)(idx - jj * nrhs);
-        xs[jj * MAXR + c] = X[c * n + j0 + jj];
+        xs[jj * R + c] = X[c * n + j0 + jj];
     }
     __syncthreads();
-    double acc0[MAXR], acc1[MAXR];
+    double acc0[R], acc1[R];
 #pragma unroll
-    for (int c = 0; c < MAXR; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
+    for (int c = 0; c < R; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
     const bool r0 = i < n, r1 = i + 1 < n;
     int64_t j = j0;
     if (VEC && r1) {
@@ -55,9 +55,9 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
             for (int u = 0; u < JU; ++u) a[u] = __ldcs(reinterpret_cast<const double2 *>(A + (j + u) * lda + i));
 #pragma unroll
             for (int u = 0; u < JU; ++u) {
-                const double *xj = xs + (j + u - j0) * MAXR;
+                const double *xj = xs + (j + u - j0) * R;
 #pragma unroll
-                for (int c = 0; c < MAXR; ++c)
+                for (int c = 0; c < R; ++c)
                     if (c < nrhs) {
                         acc0[c] = fma(a[u].x, xj[c], acc0[c]);
                         acc1[c] = fma(a[u].y, xj[c], acc1[c]);
@@ -68,9 +68,9 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
     for (; j < j1; ++j) {
         const double *col = A + j * lda;
         const double a0 = r0 ? __ldcs(col + i) : 0.0, a1 = r1 ? __ldcs(col + i + 1) : 0.0;
-        const double *xj = xs + (j - j0) * MAXR;
+        const double *xj = xs + (j - j0) * R;
 #pragma unroll
-        for (int c = 0; c < MAXR; ++c)
+        for (int c = 0; c < R; ++c)
             if (c < nrhs) {
                 acc0[c] = fma(a0, xj[c], acc0[c]);
                 acc1[c] = fma(a1, xj[c], acc1[c]);
@@ -78,7 +78,7 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
     }
     double *ps = partial + ((int64_t)s * nrhs_total + c_off) * n;
 #pragma unroll
-    for (int c = 0; c < MAXR; ++c)
+    for (int c = 0; c < R; ++c)
         if (c < nrhs) {
             if (r0) ps[c * n + i] = acc0[c];
             if (r1) ps[c * n + i + 1] = acc1[c];
@@ -184,18 +184,14 @@ void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, cons
     const int64_t cps = ceil_div(n, splits);
     const int64_t real_splits = ceil_div(n, cps);
     dim3 g1((unsigned)ceil_div(n, ROWS), (unsigned)real_splits);
-    const size_t smem = (size_t)cps * MAXR * sizeof(double);
     const bool vec = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
-    if (vec) {
-        if (smem > 48 * 1024) func_smem_once((const void *)residual_partial_kernel<true>, smem);
-        for (int c0 = 0; c0 < nr; c0 += MAXR)
-            residual_partial_kernel<true><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
-                                                               rs.partial, cps, c0, nr);
-    } else {
-        if (smem > 48 * 1024) func_smem_once((const void *)residual_partial_kernel<false>, smem);
-        for (int c0 = 0; c0 < nr; c0 += MAXR)
-            residual_partial_kernel<false><<<g1, RT, smem, s>>>(A, lda, n, std::min(MAXR, nr - c0), X + c0 * n,
-                                                                rs.partial, cps, c0, nr);
+    for (int c0 = 0; c0 < nr; c0 += MAXR) {
+        const int nc = std::min(MAXR, nr - c0);
+        const size_t smem = (size_t)cps * (nc == 1 ? 1 : MAXR) * sizeof(double);
+        auto kern = vec ? (nc == 1 ? residual_partial_kernel<true, 1> : residual_partial_kernel<true, MAXR>)
+                        : (nc == 1 ? residual_partial_kernel<false, 1> : residual_partial_kernel<false, MAXR>);
+        if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
+        kern<<<g1, RT, smem, s>>>(A, lda, n, nc, X + c0 * n, rs.partial, cps, c0, nr);
     }
     MP_LAUNCH_CHECK();
     const int g2 = (int)ceil_div(n, RT);

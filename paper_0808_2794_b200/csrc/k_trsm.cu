@@ -5,10 +5,13 @@
 // rows of the columns to its right by forward SUBSTITUTION (no explicit
 // inverse, so exact inputs stay exact — pin P2).
 //
-// Each lane owns one column (32 columns per warp); a row block of 32 rows is
-// held in registers; L11 sub-blocks are staged in shared memory, transposed
-// so that 4 consecutive rows are one broadcast LDS.128.  FMA-bound,
-// w^2/2 FMAs per column.
+// One CTA per 32-column strip; warp b owns row block b (32 rows x 32 columns
+// in registers, lane = column).  Warp b applies X_b -= L(b, k) X_k for every
+// earlier row block k as soon as warp k has published X_k in shared memory
+// (only k = b-1 is on the dependent chain), then solves its 32 x 32 unit-lower
+// diagonal block column-oriented (x_i final -> x_m -= l_mi x_i, m > i), and
+// publishes X_b.  L blocks are staged transposed in shared memory so every
+// inner step is one broadcast LDS.128 + 4 FMAs.  FMA-bound: w^2 N flops.
 #include <algorithm>
 
 #include "internal.h"
@@ -17,62 +20,92 @@ namespace mp {
 
 namespace {
 
-constexpr int TW = 4;             // warps per CTA
-constexpr int TT = TW * 32;
-constexpr int RB = 32;            // rows per register block
-constexpr int LS = RB + 4;        // smem row stride of the transposed L block (16B aligned)
+constexpr int CWS = 32;           // columns per CTA (one per lane)
+constexpr int RB = 32;            // rows per warp block
+constexpr int MAXB = 8;           // w <= MAXB * RB = 256
+constexpr int LP = RB + 4;        // padded stride of a transposed L block (16-byte aligned rows)
 
 template <typename T>
-__global__ void __launch_bounds__(TT)
+__device__ __forceinline__ void load_lt(const T *W, int64_t ldw, int64_t r, int64_t c, int nrows, int ncols,
+                                        T *lt, int lane)
+{
+    // lt[kk * LP + i] = L(r + i, c + kk): lane kk reads column kk of rows i (coalesced row
+    // segments); all 32 loads are issued before the first store (one memory round trip)
+#pragma unroll
+    for (int h = 0; h < RB; h += 16) {
+        T v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            v[i] = (h + i < nrows && lane < ncols) ? __ldg(W + (r + h + i) * ldw + c + lane) : T(0);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) lt[lane * LP + h + i] = v[i];
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(MAXB * 32, 2)
 trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *Ls = reinterpret_cast<T *>(smem_raw);   // [w][LS]: Ls[j][i] = L(rb+i, j)
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t col = c_lo + (int64_t)blockIdx.x * TT + warp * 32 + lane;
-    const bool valid = col < c_hi;
-    T acc[RB];
+    const int nb = (w + RB - 1) / RB;
+    const int lane = threadIdx.x & 31, b = threadIdx.x >> 5;
+    T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb][RB][CWS] published row blocks
+    T *Lt = Xs + (size_t)nb * RB * CWS;                       // [nb warps][RB][LP] transposed L block per warp
+    volatile int *flag = reinterpret_cast<volatile int *>(Lt + (size_t)nb * RB * LP);   // [nb]
+    if (threadIdx.x < MAXB) flag[threadIdx.x] = 0;
+    __syncthreads();
+    if (b >= nb) return;
+    const int64_t col = c_lo + (int64_t)blockIdx.x * CWS + lane;
+    const bool cvalid = col < c_hi;
+    const int rows = (w - b * RB < RB) ? (w - b * RB) : RB;   // rows of this block
+    const int64_t rb0 = r0 + (int64_t)b * RB;
+    T *lt = Lt + (size_t)b * RB * LP;
 
-    for (int rb = 0; rb < w; rb += RB) {
-        const int nr = (w - rb < RB) ? (w - rb) : RB;
-        const int ncols = rb + nr;             // L columns 0 .. rb+nr-1 are needed
-        __syncthreads();
-        for (int idx = threadIdx.x; idx < RB * ncols; idx += TT) {
-            const int i = idx / ncols, j = idx - i * ncols;
-            T v = T(0);
-            if (i < nr && j < rb + i) v = W[(r0 + rb + i) * ldw + r0 + j];   // strictly lower part only
-            Ls[j * LS + i] = v;
-        }
-        __syncthreads();
-        if (valid) {
+    T x[RB];
 #pragma unroll
-            for (int i = 0; i < RB; ++i) acc[i] = i < nr ? W[(r0 + rb + i) * ldw + col] : T(0);
-            // contributions of the already-solved rows 0 .. rb-1
-            // (x_j of the already-solved rows: 8 independent loads in flight per step)
-            for (int j = 0; j < rb; j += 8) {
-                T xv[8];
+    for (int i = 0; i < RB; ++i) x[i] = (cvalid && i < rows) ? W[(rb0 + i) * ldw + col] : T(0);
+
+    // contributions of the earlier row blocks, in the order they are published
+    for (int k = 0; k < b; ++k) {
+        load_lt(W, ldw, rb0, r0 + (int64_t)k * RB, rows, RB, lt, lane);   // L(b, k), independent of X_k
+        __syncwarp();
+        while (flag[k] == 0) { }
+        __threadfence_block();
+        __syncwarp();
+        const T *xk = Xs + (size_t)k * RB * CWS;
+#pragma unroll 4
+        for (int kk = 0; kk < RB; ++kk) {
+            const T xv = xk[kk * CWS + lane];
+            const T *lc = lt + kk * LP;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) xv[u] = W[(r0 + j + u) * ldw + col];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const T *lj = Ls + (j + u) * LS;
-#pragma unroll
-                    for (int i = 0; i < RB; ++i) acc[i] -= lj[i] * xv[u];
-                }
+            for (int i = 0; i < RB; i += 4) {
+                x[i] = fma(-lc[i], xv, x[i]);
+                x[i + 1] = fma(-lc[i + 1], xv, x[i + 1]);
+                x[i + 2] = fma(-lc[i + 2], xv, x[i + 2]);
+                x[i + 3] = fma(-lc[i + 3], xv, x[i + 3]);
             }
-            // the 32 x 32 diagonal block
-#pragma unroll
-            for (int j = 0; j < RB; ++j) {
-                const T xj = acc[j];
-                const T *lj = Ls + (rb + j) * LS;
-#pragma unroll
-                for (int i = j + 1; i < RB; ++i) acc[i] -= lj[i] * xj;
-            }
-#pragma unroll
-            for (int i = 0; i < RB; ++i)
-                if (i < nr) W[(r0 + rb + i) * ldw + col] = acc[i];
         }
+        __syncwarp();
     }
+    // the 32 x 32 unit-lower diagonal block
+    load_lt(W, ldw, rb0, rb0, rows, rows, lt, lane);
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < RB; ++i) {
+        const T *lc = lt + i * LP;
+#pragma unroll
+        for (int m = i + 1; m < RB; ++m) x[m] = fma(-lc[m], x[i], x[m]);
+    }
+    // publish X_b (shared, for later blocks) and store U12 rows
+    T *xb = Xs + (size_t)b * RB * CWS;
+#pragma unroll
+    for (int i = 0; i < RB; ++i) xb[i * CWS + lane] = x[i];
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) flag[b] = 1;
+#pragma unroll
+    for (int i = 0; i < RB; ++i)
+        if (cvalid && i < rows) W[(rb0 + i) * ldw + col] = x[i];
 }
 
 }  // namespace
@@ -81,11 +114,13 @@ template <typename T>
 void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi, cudaStream_t s)
 {
     if (c_hi <= c_lo || w <= 0) return;
-    const int grid = (int)ceil_div(c_hi - c_lo, TT);
-    const size_t smem = (size_t)round_up(w, RB) * LS * sizeof(T);
+    if (w > MAXB * RB) throw CudaError{cudaErrorInvalidValue, "trsm block wider than 256", __LINE__};
+    const int nb = (w + RB - 1) / RB;
+    const int grid = (int)ceil_div(c_hi - c_lo, CWS);
+    const size_t smem = ((size_t)nb * RB * CWS + (size_t)nb * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
     auto kern = trsm_lower_unit_kernel<T>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    kern<<<grid, TT, smem, s>>>(W, ldw, r0, w, c_lo, c_hi);
+    kern<<<grid, nb * 32, smem, s>>>(W, ldw, r0, w, c_lo, c_hi);
     MP_LAUNCH_CHECK();
     ++g_launches;
 }
