@@ -221,23 +221,39 @@ def main():
     pk, pk_src = peaks()
     sm_max = pk.get("sm_max_mhz", 1965.0)
     ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12           # TFLOP/s, FP32 FMA lanes x clock
-    dom = max(kern.items(), key=lambda kv: kv[1]["ms"])[0] if kern else None
+    # TF32 tensor peak: the measured sustained bf16 cuBLAS figure x the nominal tf32/bf16 ratio (1.1 / 2.25)
+    tf32_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)) * (1.1 / 2.25)
     roof = None
-    if dom:
-        d = kern[dom]
-        if dom in ("gemm", "trsm", "panel"):
-            ach = d["work"] / (d["ms"] / 1e3) / 1e12
-            roof = {"kernel": dom, "bound": "alu", "achieved": round(ach, 3), "peak": round(ffma_peak, 1),
-                    "unit": "TFLOP/s", "frac": round(ach / ffma_peak, 4), "traffic": None,
-                    "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",
-                    "launches": d["launches"] // args.steps, "avg_launch_us": round(d["ms"] * 1e3 / d["launches"], 2)}
-        else:
-            ach = d["work"] / (d["ms"] / 1e3) / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                    "frac": round(ach / pk["hbm_gbs"], 4), "traffic": None, "peak_source": pk_src}
+    if "trail" in kern and kern["trail"]["ms"] > 0:
+        # dominant contraction: the trailing Schur update A22 -= L21 U12; 3xTF32 does
+        # 3 tensor-core products per useful product, so achieved = 3 x algorithmic flops / time
+        d = kern["trail"]
+        mult = 3.0 if args.variant == "3xtf32" else 1.0
+        ach = mult * d["work"] / (d["ms"] / 1e3) / 1e12
+        peak = tf32_peak if args.variant == "3xtf32" else ffma_peak
+        roof = {"kernel": "trailing Schur update (K5, %s)" % args.variant,
+                "bound": "tensor" if args.variant == "3xtf32" else "alu",
+                "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                "traffic": None,
+                "peak_source": ("measured bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16), " + pk_src)
+                if args.variant == "3xtf32" else
+                f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",
+                "work_note": "achieved counts 3 x 2MNK tensor flops per launch for 3xTF32" if mult == 3.0 else "2MNK",
+                "launches": d["launches"] // args.steps, "avg_launch_us": round(d["ms"] * 1e3 / d["launches"], 2)}
+    if "residual" in kern and kern["residual"]["ms"] > 0:
+        d = kern["residual"]
+        ach = d["work"] / (d["ms"] / 1e3) / 1e9
+        roof_res = {"kernel": "residual r = b - A x (K8, fp64)", "bound": "hbm", "achieved": round(ach, 1),
+                    "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 4),
+                    "peak_source": pk_src}
+    else:
+        roof_res = None
+    panel_us_col = None
+    if "panel" in kern and kern["panel"]["launches"]:
+        panel_us_col = round(kern["panel"]["ms"] * 1e3 / args.steps / n, 3)     # latency-bound: us per column
     breakdown = {k: {"ms_per_step": round(v["ms"] / args.steps, 3), "launches_per_step": v["launches"] // args.steps,
-                     ("tflops" if k in ("gemm", "trsm", "panel") else "gbs"):
-                         round(v["work"] / (v["ms"] / 1e3) / (1e12 if k in ("gemm", "trsm", "panel") else 1e9), 2)
+                     ("tflops" if k in ("gemm", "trsm", "panel", "trail") else "gbs"):
+                         round(v["work"] / (v["ms"] / 1e3) / (1e12 if k in ("gemm", "trsm", "panel", "trail") else 1e9), 2)
                          if v["ms"] > 0 else None}
                  for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
 
@@ -297,7 +313,8 @@ def main():
                           "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
                "speedup_vs_fp64": round(fp64_ms / ms_step, 3) if fp64_ms else None,
                "fp64_ms_per_step": round(fp64_ms, 3) if fp64_ms else None,
-               "e2e": e2e, "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu,
+               "e2e": e2e, "roofline": roof, "roofline_residual": roof_res,
+               "panel_us_per_column": panel_us_col, "kernels": breakdown, "cpu_baseline": cpu,
                "clocks": clk.summary(), "gpu_launches": launches,
                "phases_ms": {"wall": round(1e3 * sum(walls) / len(walls), 3),
                              "call_device": round(sum(r[2].t_total_ms for r in reps) / len(reps), 3),

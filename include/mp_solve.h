@@ -113,10 +113,10 @@ typedef struct mp_report {
 #define MP_KC_PANEL    1   /* K2 panel factorisation       work = flops of the leaf       */
 #define MP_KC_LASWP    2   /* K3 row interchanges          work = bytes moved             */
 #define MP_KC_TRSM     3   /* K4 U12 <- L11^-1 A12         work = flops (w^2 N)           */
-#define MP_KC_GEMM     4   /* K5 Schur update              work = flops (2 M N K)         */
+#define MP_KC_GEMM     4   /* K5 in-panel Schur updates    work = flops (2 M N K)         */
 #define MP_KC_SOLVE    5   /* K6/K7/K9 triangular solves   work = bytes of the factors    */
 #define MP_KC_RESIDUAL 6   /* K8/K10 residual + test       work = bytes (8 n^2 + vectors)  */
-#define MP_KC_OTHER    7
+#define MP_KC_TRAIL    7   /* K5 on the trailing matrix A22 (3xTF32 tcgen05 or FFMA), work = flops (2 M N K) */
 
 /* Fill *o with the defaults above. */
 void mp_default_opts(mp_opts *o);

@@ -113,7 +113,7 @@ static void prof_collect(mp_report *rep)
     if (!rep || g_prof.recs.empty()) return;
     if (const char *path = std::getenv("MP_TIMELINE")) {        // debug: per-launch device timeline
         if (FILE *f = std::fopen(path, "a")) {
-            static const char *names[] = {"demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "other"};
+            static const char *names[] = {"demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "trail"};
             std::fprintf(f, "# call\n");
             for (const ProfRec &r : g_prof.recs) {
                 float t0 = 0.f, t1 = 0.f;
@@ -255,7 +255,8 @@ struct Factor {
         prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), s);
     }
     void gemm(int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool trailing = false) {
-        prof_begin(KC_GEMM, s);
+        const int cls = trailing ? KC_TRAIL : KC_GEMM;
+        prof_begin(cls, s);
         if constexpr (sizeof(T) == 4) {
             if (trailing && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
                 launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, tf32, sms, s);
@@ -264,7 +265,7 @@ struct Factor {
         } else {
             launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
         }
-        prof_end(KC_GEMM, 2.0 * M * N * K, s);
+        prof_end(cls, 2.0 * M * N * K, s);
     }
     // recursive panel: columns [c0, c0+w) of the panel [klo, khi), rows [c0, n)
     void panel(int64_t c0, int w, int64_t klo, int64_t khi) {

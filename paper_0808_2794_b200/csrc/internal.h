@@ -67,7 +67,7 @@ extern thread_local int64_t g_launches;
 // Optional per-kernel-class timing (mp_opts.flags bit 1): CUDA events recorded
 // on the launching stream around every launch of a class, summed after the
 // call.  Classes follow DESIGN.md's kernel list.
-enum KClass : int { KC_DEMOTE = 0, KC_PANEL, KC_LASWP, KC_TRSM, KC_GEMM, KC_SOLVE, KC_RESIDUAL, KC_OTHER, KC_COUNT };
+enum KClass : int { KC_DEMOTE = 0, KC_PANEL, KC_LASWP, KC_TRSM, KC_GEMM, KC_SOLVE, KC_RESIDUAL, KC_TRAIL, KC_COUNT };
 void prof_begin(int cls, cudaStream_t s);
 void prof_end(int cls, double work, cudaStream_t s);   // work: algorithmic flops (or bytes) of the launch
 

@@ -33,8 +33,15 @@ namespace {
 
 constexpr int TM_COLS = 128;      // C columns per tile (MMA M, TMEM lanes)
 constexpr int TM_ROWS = 256;      // C rows per tile (MMA N)
-constexpr int KC = 32;            // K chunk: 32 tf32 = 128 B rows (one SWIZZLE_128B atom)
-constexpr int STAGES = 2;
+#ifndef MP_TF32_KC
+#define MP_TF32_KC 32
+#endif
+// K chunk per ring stage: KC tf32 = KC*4-byte rows, one swizzle atom (SWIZZLE_64B for KC = 16,
+// SWIZZLE_128B for KC = 32); the ring holds 192 KB either way (4 x 48 KB or 2 x 96 KB).
+constexpr int KC = MP_TF32_KC;
+constexpr int STAGES = KC == 16 ? 4 : 2;
+constexpr uint32_t SW_BYTES = KC * 4;                 // swizzle atom row bytes
+constexpr uint64_t SW_MODE = KC == 16 ? 4u : 2u;      // UMMA descriptor layout: 4 = SWIZZLE_64B, 2 = SWIZZLE_128B
 constexpr int A_BYTES = TM_COLS * KC * 4;     // 16 KB
 constexpr int B_BYTES = TM_ROWS * KC * 4;     // 32 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 96 KB
@@ -74,15 +81,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
-// UMMA shared-memory descriptor: K-major operand, SWIZZLE_128B, 8-row groups 1024 B apart.
+// UMMA shared-memory descriptor: K-major operand, swizzled rows of SW_BYTES, 8-row groups
+// 8 * SW_BYTES apart.
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr)
 {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFFu);          // start address
     d |= (uint64_t)1u << 16;                          // leading byte offset (unused for SW128 K-major)
-    d |= (uint64_t)(1024u >> 4) << 32;                // stride byte offset: 8 rows x 128 B
+    d |= (uint64_t)((8u * SW_BYTES) >> 4) << 32;      // stride byte offset: 8 rows x SW_BYTES
     d |= (uint64_t)1u << 46;                          // descriptor version (sm_100)
-    d |= (uint64_t)2u << 61;                          // layout: SWIZZLE_128B
+    d |= SW_MODE << 61;                               // layout: swizzle mode
     return d;
 }
 
@@ -331,7 +339,7 @@ void encode_kmajor(CUtensorMap *map, const float *base, int rows, int kdim, int 
     cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), gdim, gstride, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, KC == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw CudaError{cudaErrorInvalidValue, "cuTensorMapEncodeTiled failed", __LINE__};
 }
