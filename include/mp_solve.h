@@ -77,11 +77,13 @@ extern "C" {
 typedef struct mp_opts {
     int32_t nb;        /* panel width; 0 = default (64 for n<=1024, 128 for n<=4096, else 256) */
     int32_t itermax;   /* refinement cap; 0 = MP_ITERMAX_DEFAULT */
-    int32_t variant;   /* MP_VARIANT_* (default MP_VARIANT_FFMA) */
+    int32_t variant;   /* MP_VARIANT_* (default MP_VARIANT_3XTF32) */
     int32_t flags;     /* bit 0: force the binary64 fallback path after the binary32 factorisation (testing);
                           bit 1: per-kernel-class CUDA-event timing into mp_report.k_* (measurement);
                           bit 2: with bit 1, keep the events of successive calls and resolve them only in
-                                 mp_profile_collect() (keeps event queries out of timed loops) */
+                                 mp_profile_collect() (keeps event queries out of timed loops);
+                          bit 3: with bit 1, record only the trailing update and the residual classes
+                                 (a handful of events per solve: cheap enough for a timed region) */
 } mp_opts;
 
 #define MP_HIST_MAX 64

@@ -217,7 +217,7 @@ def mp_profile_collect() -> Report:
     return rep
 
 
-def make_opts(nb: int = 0, itermax: int = 30, variant: int = MP_VARIANT_FFMA, flags: int = 0) -> Opts:
+def make_opts(nb: int = 0, itermax: int = 30, variant: int = MP_VARIANT_3XTF32, flags: int = 0) -> Opts:
     o = Opts()
     lib.mp_default_opts(ctypes.byref(o))
     o.nb, o.itermax, o.variant, o.flags = nb, itermax, variant, flags

@@ -70,6 +70,7 @@ namespace {
 struct ProfRec { int cls, a, b; double work; };
 struct ProfState {
     bool on = false;
+    unsigned mask = ~0u;         // classes recorded (flags bit 3: trailing update + residual only)
     std::vector<cudaEvent_t> ev;
     size_t used = 0;
     int open[KC_COUNT] = {0};
@@ -94,7 +95,7 @@ thread_local ProfState g_prof;
 
 void prof_begin(int cls, cudaStream_t s)
 {
-    if (!g_prof.on) return;
+    if (!g_prof.on || !((g_prof.mask >> cls) & 1u)) return;
     const int i = g_prof.take();
     MP_CUDA(cudaEventRecord(g_prof.ev[i], s));
     g_prof.open[cls] = i;
@@ -102,7 +103,7 @@ void prof_begin(int cls, cudaStream_t s)
 
 void prof_end(int cls, double work, cudaStream_t s)
 {
-    if (!g_prof.on) return;
+    if (!g_prof.on || !((g_prof.mask >> cls) & 1u)) return;
     const int i = g_prof.take();
     MP_CUDA(cudaEventRecord(g_prof.ev[i], s));
     g_prof.recs.push_back({cls, g_prof.open[cls], i, work});
@@ -441,6 +442,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     configure_mempool_once();
     g_launches = 0;
     g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
     Timer tm(s);
     const int t0 = tm.mark();
 
@@ -558,6 +560,7 @@ int dgesv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
     configure_mempool_once();
     g_launches = 0;
     g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
     Timer tm(s);
     const int t0 = tm.mark();
     Pool pool(s);
@@ -671,7 +674,7 @@ void mp_default_opts(mp_opts *o)
     if (!o) return;
     o->nb = 0;
     o->itermax = MP_ITERMAX_DEFAULT;
-    o->variant = MP_VARIANT_FFMA;
+    o->variant = MP_VARIANT_3XTF32;
     o->flags = 0;
 }
 

@@ -169,6 +169,93 @@ void launch_tiles(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t
     ++g_launches;
 }
 
+// ---------------------------------------------------------------- tall-skinny variant
+// In-panel Schur updates of the recursive panel (N, K <= 128, M up to n): one CTA per
+// BM-row slab; the whole K x N block B = U12 and the CTA's BM x K slab of L21 are staged
+// in shared memory once (B is shared by every CTA and L2-resident), then a register-
+// blocked FMA loop over K.  Latency-oriented: a single load phase, no k-slice pipeline.
+template <typename T, int BM, int NMAX>
+__global__ void __launch_bounds__(256)
+tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int M, int N, int K)
+{
+    constexpr int TX = 16, TY = 16;                     // threads along N, along rows
+    constexpr int TN = NMAX / TX, TM = BM / TY;
+    constexpr int APAD = BM + 4, BPAD = NMAX + 4;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *As = reinterpret_cast<T *>(smem_raw);            // [K][APAD]  As[k][i] = L21(i, k)
+    T *Bs = As + (size_t)128 * APAD;                    // [K][BPAD]  Bs[k][j] = U12(k, j)
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    const int64_t bm0 = (int64_t)blockIdx.x * BM;
+    // stage B (coalesced along N) and the A slab (coalesced along K, stored transposed)
+    // (8 independent global loads in flight per thread before the shared-memory stores)
+    for (int b0 = tid; b0 < K * NMAX; b0 += 8 * 256) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = b0 + u * 256, k = idx / NMAX, j = idx - k * NMAX;
+            v[u] = (idx < K * NMAX && j < N) ? W[(k0 + k) * ldw + c0 + j] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = b0 + u * 256, k = idx / NMAX, j = idx - k * NMAX;
+            if (idx < K * NMAX) Bs[k * BPAD + j] = v[u];
+        }
+    }
+    for (int b0 = tid; b0 < BM * K; b0 += 8 * 256) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = b0 + u * 256, i = idx / K, k = idx - i * K;
+            v[u] = (idx < BM * K && bm0 + i < M) ? W[(r0 + bm0 + i) * ldw + k0 + k] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int idx = b0 + u * 256, i = idx / K, k = idx - i * K;
+            if (idx < BM * K) As[k * APAD + i] = v[u];
+        }
+    }
+    __syncthreads();
+    T acc[TM][TN];
+#pragma unroll
+    for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        T a[TM], b[TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i) a[i] = As[k * APAD + ty * TM + i];
+#pragma unroll
+        for (int j = 0; j < TN; ++j) b[j] = Bs[k * BPAD + tx * TN + j];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < TM; ++i) {
+        const int64_t row = bm0 + ty * TM + i;
+        if (row >= M) continue;
+        T *crow = W + (r0 + row) * ldw + c0;
+#pragma unroll
+        for (int j = 0; j < TN; ++j) {
+            const int col = tx * TN + j;
+            if (col < N) crow[col] -= acc[i][j];
+        }
+    }
+}
+
+template <typename T, int BM, int NMAX>
+void launch_ts(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, cudaStream_t s)
+{
+    const size_t smem = ((size_t)128 * (BM + 4) + (size_t)128 * (NMAX + 4)) * sizeof(T);
+    auto kern = tsgemm_kernel<T, BM, NMAX>;
+    func_smem_once((const void *)kern, smem);
+    kern<<<(unsigned)ceil_div(M, BM), 256, smem, s>>>(W, ldw, r0, c0, k0, (int)M, (int)N, (int)K);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
 }  // namespace
 
 template <>
@@ -176,6 +263,9 @@ void launch_gemm_update<float>(float *W, int64_t ldw, int64_t r0, int64_t c0, in
                                int64_t K, cudaStream_t s)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
+    if (K <= 128 && N <= 32) return launch_ts<float, 64, 32>(W, ldw, r0, c0, k0, M, N, K, s);
+    if (K <= 128 && N <= 64) return launch_ts<float, 64, 64>(W, ldw, r0, c0, k0, M, N, K, s);
+    if (K <= 128 && N <= 128) return launch_ts<float, 64, 128>(W, ldw, r0, c0, k0, M, N, K, s);
     launch_tiles<float, 128, 128, 8, 8, 8>(W, ldw, r0, c0, k0, M, N, K, s);
 }
 
@@ -184,6 +274,8 @@ void launch_gemm_update<double>(double *W, int64_t ldw, int64_t r0, int64_t c0, 
                                 int64_t K, cudaStream_t s)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
+    if (K <= 128 && N <= 32) return launch_ts<double, 32, 32>(W, ldw, r0, c0, k0, M, N, K, s);
+    if (K <= 128 && N <= 64) return launch_ts<double, 32, 64>(W, ldw, r0, c0, k0, M, N, K, s);
     launch_tiles<double, 128, 64, 8, 8, 4>(W, ldw, r0, c0, k0, M, N, K, s);
 }
 

@@ -51,7 +51,7 @@ def test_version_and_defaults(binding):
     assert "sm_100a" in binding.mp_version()
     o = binding.Opts()
     binding.lib.mp_default_opts(ctypes.byref(o))
-    assert (o.nb, o.itermax, o.variant, o.flags) == (0, 30, 0, 0)
+    assert (o.nb, o.itermax, o.variant, o.flags) == (0, 30, 1, 0)   # default variant: 3xTF32 tcgen05
 
 
 def _call(binding, n, nrhs, A, lda, B, X):

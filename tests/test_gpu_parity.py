@@ -306,3 +306,35 @@ def test_strict_parity_3xtf32(mp, orc):
     Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_3XTF32)
     assert info == 0 and abs(it - ro.iters) <= 1
     assert np.abs(Xg - ro.X).max() / np.abs(ro.X).max() <= 1e-12
+
+
+# --------------------------------------------------------------------------- FFMA variant (B:5), explicitly
+# (the library default is the 3xTF32 variant; the tests above without options exercise it)
+@pytest.mark.parametrize("n", [700, 2100])
+def test_exact_lu_factors_bitwise_ffma(mp, orc, n):
+    A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n + 7)
+    LU, ipiv, info = mp.mp_sgetrf(A, mp.make_opts(variant=mp.MP_VARIANT_FFMA))
+    assert info == 0
+    assert np.array_equal(perm_from_ipiv(ipiv), perm)
+    assert np.array_equal(np.tril(LU, -1).astype(np.float64), np.tril(L, -1))
+    assert np.array_equal(np.triu(LU).astype(np.float64), U)
+    Xg, it, info, _ = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_FFMA)
+    assert (it, info) == (0, 0) and np.array_equal(Xg, X)
+
+
+@pytest.mark.parametrize("n,nrhs,seed", [(1024, 1, 4), (2600, 3, 6)])
+def test_criterion_parity_ffma(mp, orc, n, nrhs, seed):
+    A, B, X = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+    ro = orc.dsgesv(A, B)
+    Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_FFMA)
+    assert info == ro.info == 0
+    assert it >= 0 and abs(it - ro.iters) <= 1, (it, ro.iters, rep.history(), list(ro.hist))
+    assert certificate_ok(A, Xg, B)
+
+
+def test_strict_parity_ffma(mp, orc):
+    A, B, X = inputs.conditioned(1024, 1.0, seed=3)
+    ro = orc.dsgesv(A, B)
+    Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_FFMA)
+    assert info == 0 and abs(it - ro.iters) <= 1
+    assert np.abs(Xg - ro.X).max() / np.abs(ro.X).max() <= 1e-12
