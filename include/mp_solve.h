@@ -83,7 +83,9 @@ typedef struct mp_opts {
                           bit 2: with bit 1, keep the events of successive calls and resolve them only in
                                  mp_profile_collect() (keeps event queries out of timed loops);
                           bit 3: with bit 1, record only the trailing update and the residual classes
-                                 (a handful of events per solve: cheap enough for a timed region) */
+                                 (a handful of events per solve: cheap enough for a timed region);
+                          bit 4: disable the look-ahead (panel k+1 factored on a 16-SM green context
+                                 while the trailing update of step k runs on the other SMs) */
 } mp_opts;
 
 #define MP_HIST_MAX 64

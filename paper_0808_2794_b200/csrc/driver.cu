@@ -26,6 +26,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/mp_solve.h"
 #include "../../include/mp_kernels.h"
 #include "internal.h"
@@ -221,6 +224,96 @@ struct Timer {
     }
 };
 
+// ------------------------------------------------------------------ look-ahead execution resources
+// the factorisation of panel k+1 overlaps the trailing update of step k.
+// The panel work (leaf clusters, in-panel updates, the next panel's columns) runs on a
+// stream of a 16-SM green context (one 16-CTA leaf cluster fits), the trailing update on
+// a stream of a green context holding the remaining SMs, so the two never compete for SMs.
+// Created once per device through driver entry points; if the device or driver refuses,
+// the factorisation runs sequentially on the caller's stream.
+struct ExecRes {
+    bool ok = false;
+    cudaStream_t sP = nullptr, sU = nullptr;
+    int smsP = 0, smsU = 0;
+};
+
+ExecRes make_exec_res(int dev)
+{
+    ExecRes r;
+    if (const char *e = std::getenv("MP_NO_LOOKAHEAD"))
+        if (e[0] == '1') return r;
+    auto entry = [](const char *name) -> void * {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return fn;
+    };
+    auto getRes = reinterpret_cast<PFN_cuDeviceGetDevResource_v12040>(entry("cuDeviceGetDevResource"));
+    auto split = reinterpret_cast<PFN_cuDevSmResourceSplitByCount_v12040>(entry("cuDevSmResourceSplitByCount"));
+    auto genDesc = reinterpret_cast<PFN_cuDevResourceGenerateDesc_v12040>(entry("cuDevResourceGenerateDesc"));
+    auto mkCtx = reinterpret_cast<PFN_cuGreenCtxCreate_v12040>(entry("cuGreenCtxCreate"));
+    auto mkStream = reinterpret_cast<PFN_cuGreenCtxStreamCreate_v12050>(entry("cuGreenCtxStreamCreate"));
+    if (!getRes || !split || !genDesc || !mkCtx || !mkStream) return r;
+    CUdevResource all, grp[1], rest;
+    unsigned ng = 1;
+    if (getRes((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return r;
+    if (split(grp, &ng, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, 16) != CUDA_SUCCESS || ng != 1)
+        return r;
+    if (grp[0].sm.smCount < 16 || rest.sm.smCount < 32) return r;
+    CUdevResourceDesc dP, dU;
+    CUgreenCtx gP, gU;
+    CUstream sP, sU;
+    if (genDesc(&dP, grp, 1) != CUDA_SUCCESS || genDesc(&dU, &rest, 1) != CUDA_SUCCESS) return r;
+    if (mkCtx(&gP, dP, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
+    if (mkCtx(&gU, dU, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
+    if (mkStream(&sU, gU, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return r;
+    // The panel stream is an ordinary (full-device, highest-priority) stream: its kernels run on
+    // the SMs the update partition leaves free (a cluster-capable 16-SM group) while the
+    // trailing update runs, and on the whole GPU otherwise.
+    if (std::getenv("MP_PANEL_GREEN")) {
+        if (mkStream(&sP, gP, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return r;
+    } else {
+        int lo = 0, hi = 0;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) return r;
+        cudaStream_t ps;
+        if (cudaStreamCreateWithPriority(&ps, cudaStreamNonBlocking, hi) != cudaSuccess) return r;
+        sP = (CUstream)ps;
+    }
+    r.ok = true;
+    r.sP = (cudaStream_t)sP;
+    r.sU = (cudaStream_t)sU;
+    r.smsP = (int)grp[0].sm.smCount;
+    r.smsU = (int)rest.sm.smCount;
+    return r;
+}
+
+ExecRes &exec_res()
+{
+    static std::mutex mu;
+    static std::map<int, ExecRes> per_dev;
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it == per_dev.end()) it = per_dev.emplace(dev, make_exec_res(dev)).first;
+    return it->second;
+}
+
+// small reusable event pool (disable-timing events for cross-stream ordering)
+cudaEvent_t la_event(int i)
+{
+    static thread_local std::vector<cudaEvent_t> evs;
+    while ((int)evs.size() <= i) {
+        cudaEvent_t e;
+        MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        evs.push_back(e);
+    }
+    return evs[i];
+}
+
 // ------------------------------------------------------------------ blocked GEPP
 // Right-looking blocked LU (SGETRF's structure): for every panel of nb
 // columns — recursive panel factorisation (cluster leaves K2 + in-panel K3/K4/K5),
@@ -232,88 +325,159 @@ struct Factor {
     int64_t n, ldw;
     int32_t *ipiv, *perm;
     PanelScratch ps;
+    int32_t *ppairs[2], *nppairs[2];   // panel-level pairs, double-buffered for the look-ahead
     DevStatus *st;
     int nb;
     int variant = MP_VARIANT_FFMA;
-    float *tf32 = nullptr;     // 3xTF32 split scratch (variant 1)
+    float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
     cudaStream_t s;
 
-    void leaf(int64_t c0, int w, int64_t klo, int64_t khi) {
+    void leaf(cudaStream_t q, int64_t c0, int w, int64_t klo, int64_t khi) {
         const double m = (double)(n - c0);
-        prof_begin(KC_PANEL, s);
-        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, s);
-        prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, s);
+        prof_begin(KC_PANEL, q);
+        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, q);
+        prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, q);
         if (khi - klo > w) {   // the leaf's interchanges, on the rest of its panel
-            prof_begin(KC_LASWP, s);
-            launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, klo, khi, c0, c0 + w, nullptr, s);
-            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(khi - klo - w) * sizeof(T), s);
+            prof_begin(KC_LASWP, q);
+            launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, klo, khi, c0, c0 + w, nullptr, q);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(khi - klo - w) * sizeof(T), q);
         }
     }
-    void trsm(int64_t r0, int w, int64_t c_lo, int64_t c_hi) {
-        prof_begin(KC_TRSM, s);
-        launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, s);
-        prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), s);
+    void trsm(cudaStream_t q, int64_t r0, int w, int64_t c_lo, int64_t c_hi) {
+        prof_begin(KC_TRSM, q);
+        launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, q);
+        prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), q);
     }
-    void gemm(int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool trailing = false) {
-        const int cls = trailing ? KC_TRAIL : KC_GEMM;
-        prof_begin(cls, s);
+    // Schur update C -= L U.  big: the trailing update or the next panel's columns
+    // (tensor-core variant when selected); scratch / nsm: the launching stream's.
+    void gemm(cudaStream_t q, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool big,
+              int cls, float *scratch, int nsm) {
+        prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
-            if (trailing && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
-                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, tf32, sms, s);
+            if (big && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q);
             else
-                launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+                launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
-            launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, s);
+            launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         }
-        prof_end(cls, 2.0 * M * N * K, s);
+        prof_end(cls, 2.0 * M * N * K, q);
     }
     // recursive panel: columns [c0, c0+w) of the panel [klo, khi), rows [c0, n)
-    void panel(int64_t c0, int w, int64_t klo, int64_t khi) {
+    void panel(cudaStream_t q, int64_t c0, int w, int64_t klo, int64_t khi) {
         const int wl = panel_leaf_width<T>(n - c0);
         if (wl <= 0) throw std::runtime_error("matrix too tall for one panel cluster");
-        if (w <= wl) { leaf(c0, w, klo, khi); return; }
+        if (w <= wl) { leaf(q, c0, w, klo, khi); return; }
         int w1 = (int)round_up(w / 2, 8);
         if (w1 > wl && w1 % wl) w1 = (int)round_up(w1, wl);
-        panel(c0, w1, klo, khi);
-        trsm(c0, w1, c0 + w1, c0 + w);
-        gemm(c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1);
-        panel(c0 + w1, w - w1, klo, khi);
+        panel(q, c0, w1, klo, khi);
+        trsm(q, c0, w1, c0 + w1, c0 + w);
+        gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, false, KC_GEMM, nullptr, 0);
+        panel(q, c0 + w1, w - w1, klo, khi);
     }
-    void run() {
+    // panel [k, k+w) on stream q, its panel-level pairs into buffer b
+    void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
+        launch_orig_init(ps.orig, k, n, q);
+        panel(q, k, w, k, k + w);
+        launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
+    }
+    void run_sequential() {
         launch_init_perm(perm, n, s);
         for (int64_t k = 0; k < n; k += nb) {
             const int w = (int)std::min<int64_t>(nb, n - k);
-            launch_orig_init(ps.orig, k, n, s);
-            panel(k, w, k, k + w);
+            factor_panel(s, k, w, 0);
             // the panel's interchanges on every other column (left factors + trailing matrix)
-            launch_emit_pairs(ps.orig, k, n, ps.ppairs, ps.nppairs, s);
             prof_begin(KC_LASWP, s);
-            launch_laswp_pairs<T>(W, ldw, ps.ppairs, ps.nppairs, 2 * w, 0, n, k, k + w, perm, s);
+            launch_laswp_pairs<T>(W, ldw, ppairs[0], nppairs[0], 2 * w, 0, n, k, k + w, perm, s);
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
             if (k + w < n) {
-                trsm(k, w, k + w, n);                                     // U12 <- L11^-1 A12
-                gemm(k + w, k + w, k, n - k - w, n - k - w, w, true);     // A22 -= L21 U12
+                trsm(s, k, w, k + w, n);                                                   // U12 <- L11^-1 A12
+                gemm(s, k + w, k + w, k, n - k - w, n - k - w, w, true, KC_TRAIL, tf32[0], sms);   // A22 -= L21 U12
             }
         }
+    }
+    // Look-ahead (depth 1).  Step k:
+    //   update stream : [wait: panel k] panel-k interchanges on every other column; U12 and Schur
+    //                   update of the NEXT panel's columns [kn, kn+wn) (all update-stream SMs,
+    //                   tensor cores), event; then U12 and Schur update of the rest [kn+wn, n)
+    //   panel stream  : [wait: next panel's columns updated] factor panel kn
+    // so the factorisation of panel kn overlaps the trailing update of the rest; concurrent
+    // work touches disjoint column sets; pair lists alternate between two buffers.
+    void run_lookahead(const ExecRes &ex) {
+        cudaStream_t sP = ex.sP, sU = ex.sU;
+        cudaEvent_t e0 = la_event(0), eP[2] = {la_event(1), la_event(2)}, eN = la_event(3);
+        cudaEvent_t eEndP = la_event(4), eEndU = la_event(5);
+        MP_CUDA(cudaEventRecord(e0, s));
+        MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
+        MP_CUDA(cudaStreamWaitEvent(sU, e0, 0));
+        launch_init_perm(perm, n, sU);
+        factor_panel(sP, 0, (int)std::min<int64_t>(nb, n), 0);
+        MP_CUDA(cudaEventRecord(eP[0], sP));
+        int idx = 0;
+        for (int64_t k = 0; k < n; k += nb, ++idx) {
+            const int w = (int)std::min<int64_t>(nb, n - k);
+            const int64_t kn = k + w;
+            const int wn = kn < n ? (int)std::min<int64_t>(nb, n - kn) : 0;
+            const int b = idx & 1;
+            MP_CUDA(cudaStreamWaitEvent(sU, eP[b], 0));
+            if (kn < n) {
+                // the next panel's columns first (on the panel's critical path) ...
+                prof_begin(KC_LASWP, sU);
+                launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
+                prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sU);
+                trsm(sU, k, w, kn, kn + wn);
+                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], ex.smsU);
+                MP_CUDA(cudaEventRecord(eN, sU));
+                MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
+                factor_panel(sP, kn, wn, b ^ 1);
+                MP_CUDA(cudaEventRecord(eP[b ^ 1], sP));
+            }
+            // ... then every other column (left factors, rest of the trailing matrix), off it
+            prof_begin(KC_LASWP, sU);
+            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, n, k, kn + wn, perm, sU);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w - wn) * sizeof(T), sU);
+            if (kn < n && kn + wn < n) {
+                trsm(sU, k, w, kn + wn, n);
+                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], ex.smsU);
+            }
+        }
+        MP_CUDA(cudaEventRecord(eEndP, sP));
+        MP_CUDA(cudaEventRecord(eEndU, sU));
+        MP_CUDA(cudaStreamWaitEvent(s, eEndP, 0));
+        MP_CUDA(cudaStreamWaitEvent(s, eEndU, 0));
+    }
+    void run(bool lookahead) {
+        if (lookahead && n > 2 * (int64_t)nb) {
+            const ExecRes &ex = exec_res();
+            if (ex.ok) { run_lookahead(ex); return; }
+        }
+        run_sequential();
     }
 };
 
 template <typename T>
 void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
-                cudaStream_t s, int variant = MP_VARIANT_FFMA)
+                cudaStream_t s, int variant = MP_VARIANT_FFMA, bool lookahead = true)
 {
     Factor<T> f;
     f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
     f.sms = num_sms();
     f.variant = variant;
-    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) f.tf32 = pool.get<float>(tf32_scratch_floats(n, nb));
+    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) {
+        f.tf32[0] = pool.get<float>(tf32_scratch_floats(n, nb));
+        f.tf32[1] = pool.get<float>(tf32_scratch_floats(n, nb));
+    }
     f.ps.orig = pool.get<int32_t>(n);
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
-    f.ps.ppairs = pool.get<int32_t>(4 * (size_t)nb);
-    f.ps.nppairs = pool.get<int32_t>(1);
-    f.run();
+    for (int b = 0; b < 2; ++b) {
+        f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nb);
+        f.nppairs[b] = pool.get<int32_t>(1);
+    }
+    f.ps.ppairs = f.ppairs[0];
+    f.ps.nppairs = f.nppairs[0];
+    f.run(lookahead);
 }
 
 struct Args {
@@ -487,7 +651,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     if (st0.flags & ST_OVERFLOW) code = -2;
     if (!code) {
         // ---- step 1: binary32 blocked GEPP
-        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant);
+        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant, (o.flags & 16) == 0);
         t_fac = tm.mark();
         const DevStatus &st1 = sio.read();
         if (st1.flags & ST_ZERO_PIVOT) code = -3;
