@@ -260,7 +260,9 @@ ExecRes make_exec_res(int dev)
     CUdevResource all, grp[1], rest;
     unsigned ng = 1;
     if (getRes((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return r;
-    if (split(grp, &ng, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, 16) != CUDA_SUCCESS || ng != 1)
+    unsigned psms = 48;                       // SMs kept free of the trailing update (MP_PANEL_SMS)
+    if (const char *e = std::getenv("MP_PANEL_SMS")) psms = (unsigned)std::max(16, std::atoi(e));
+    if (split(grp, &ng, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, psms) != CUDA_SUCCESS || ng != 1)
         return r;
     if (grp[0].sm.smCount < 16 || rest.sm.smCount < 32) return r;
     CUdevResourceDesc dP, dU;
