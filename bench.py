@@ -240,6 +240,7 @@ def main():
         mult = 3.0 if args.variant == "3xtf32" else 1.0
         ach = mult * d["work"] / (d["ms"] / 1e3) / 1e12
         peak = tf32_peak if args.variant == "3xtf32" else ffma_peak
+        la, sms_panel, sms_upd = mp.mp_exec_info()
         roof = {"kernel": "trailing Schur update (K5, %s)" % args.variant,
                 "bound": "tensor" if args.variant == "3xtf32" else "alu",
                 "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
@@ -248,7 +249,11 @@ def main():
                 if args.variant == "3xtf32" else
                 f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",
                 "work_note": "achieved counts 3 x 2MNK tensor flops per launch for 3xTF32" if mult == 3.0 else "2MNK",
-                "launches": d["launches"] // args.steps, "avg_launch_us": round(d["ms"] * 1e3 / d["launches"], 2)}
+                "launches": d["launches"] // args.steps, "avg_launch_us": round(d["ms"] * 1e3 / d["launches"], 2),
+                # with the look-ahead the update runs on a green context of sms_update SMs (the
+                # panel keeps the rest): the same peak scaled to that partition
+                "sms": sms_upd, "sms_total": 148,
+                "frac_of_partition": round(ach / (peak * sms_upd / 148.0), 4)}
     if "residual" in kern and kern["residual"]["ms"] > 0:
         d = kern["residual"]
         ach = d["work"] / (d["ms"] / 1e3) / 1e9
@@ -319,7 +324,9 @@ def main():
                "config": {"workload": WORKLOAD, "n": n, "nrhs": nrhs, "nb": reps[-1][2].nb,
                           "variant": args.variant, "iters": iters,
                           "l2": "inputs larger than L2 (A fp64 = %.2f GB)" % (8 * n * n / 1e9),
-                          "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas"},
+                          "parallelism": "1 GPU" if world == 1 else f"{world} independent replicas",
+                          "lookahead": "panel stream + %d-SM update green context" % mp.mp_exec_info()[2]
+                          if mp.mp_exec_info()[0] else "off"},
                "speedup_vs_fp64": round(fp64_ms / ms_step, 3) if fp64_ms else None,
                "fp64_ms_per_step": round(fp64_ms, 3) if fp64_ms else None,
                "e2e": e2e, "roofline": roof, "roofline_residual": roof_res,

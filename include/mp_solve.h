@@ -173,6 +173,12 @@ const char *mp_last_error(void);
 /* Library version / build string (arch, variant support). */
 const char *mp_version(void);
 
+/* Execution resources of the factorisation on the current device: *lookahead = 1 when the
+ * look-ahead partition is active, *sms_update = SMs of the trailing-update green context,
+ * *sms_panel = SMs kept free for the panel stream (0 / device SM count when inactive).
+ * Returns MP_OK or MP_ERR_CUDA. */
+int mp_exec_info(int *lookahead, int *sms_panel, int *sms_update);
+
 #ifdef __cplusplus
 }
 #endif

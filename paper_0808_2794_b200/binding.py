@@ -71,10 +71,11 @@ lib.mp_set_stream.argtypes = [_p]
 lib.mp_profile_collect.argtypes = [ctypes.POINTER(Report)]
 lib.mp_last_error.restype = ctypes.c_char_p
 lib.mp_version.restype = ctypes.c_char_p
+lib.mp_exec_info.argtypes = [_pi, _pi, _pi]
 
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
-            "mp_profile_collect")
+            "mp_profile_collect", "mp_exec_info")
 
 
 def mp_version() -> str:
@@ -222,3 +223,10 @@ def make_opts(nb: int = 0, itermax: int = 30, variant: int = MP_VARIANT_3XTF32, 
     lib.mp_default_opts(ctypes.byref(o))
     o.nb, o.itermax, o.variant, o.flags = nb, itermax, variant, flags
     return o
+
+
+def mp_exec_info():
+    """(lookahead, sms_panel, sms_update) of the factorisation on the current device."""
+    la, sp, su = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    _check(lib.mp_exec_info(ctypes.byref(la), ctypes.byref(sp), ctypes.byref(su)))
+    return la.value, sp.value, su.value

@@ -922,8 +922,20 @@ const char *mp_last_error(void) { return g_err.c_str(); }
 
 const char *mp_version(void)
 {
-    return "libmpsolve 0.2 (sm_100a; variants: ffma, 3xtf32-tcgen05; blocked right-looking GEPP, cluster panel, "
-           "row-major working copy)";
+    return "libmpsolve 0.3 (sm_100a; variants: ffma, 3xtf32-tcgen05; blocked right-looking GEPP with look-ahead on "
+           "green contexts, cluster panel, row-major working copy)";
+}
+
+int mp_exec_info(int *lookahead, int *sms_panel, int *sms_update)
+{
+    return guarded([&] {
+        const ExecRes &ex = exec_res();
+        const int all = num_sms();
+        if (lookahead) *lookahead = ex.ok ? 1 : 0;
+        if (sms_panel) *sms_panel = ex.ok ? all - ex.smsU : 0;
+        if (sms_update) *sms_update = ex.ok ? ex.smsU : all;
+        return MP_OK;
+    });
 }
 
 }  // extern "C"
