@@ -159,7 +159,7 @@ struct ResidualScratch {
     double *blocksums;    // [nblocks][2*nrhs]
     unsigned *counter;    // last-block ticket
 };
-int64_t residual_splits(int64_t n, int num_sms);
+int64_t residual_splits(int64_t n, int64_t nrhs, int num_sms);
 size_t residual_partial_elems(int64_t n, int64_t nrhs, int num_sms);
 template <typename T>
 void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,

@@ -161,17 +161,20 @@ residual_finalize_kernel(int64_t n, int nrhs, int splits, const double *__restri
 
 }  // namespace
 
-int64_t residual_splits(int64_t n, int num_sms)
+int64_t residual_splits(int64_t n, int64_t nrhs, int num_sms)
 {
     const int64_t tiles = ceil_div(n, ROWS);
     int64_t s = ceil_div((int64_t)num_sms * 8, tiles);
+    // the x slice of a split lives in shared memory: at most 64 KB per CTA
+    const int64_t r = nrhs <= 1 ? 1 : MAXR;
+    s = std::max<int64_t>(s, ceil_div(n * r * (int64_t)sizeof(double), 64 * 1024));
     s = std::max<int64_t>(1, std::min<int64_t>(s, ceil_div(n, 64)));
     return s;
 }
 
 size_t residual_partial_elems(int64_t n, int64_t nrhs, int num_sms)
 {
-    return (size_t)residual_splits(n, num_sms) * (size_t)nrhs * (size_t)n;
+    return (size_t)residual_splits(n, nrhs, num_sms) * (size_t)nrhs * (size_t)n;
 }
 
 template <typename T>
@@ -180,7 +183,7 @@ void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, cons
                      int num_sms, cudaStream_t s)
 {
     const int nr = (int)nrhs;
-    const int64_t splits = residual_splits(n, num_sms);
+    const int64_t splits = residual_splits(n, nrhs, num_sms);
     const int64_t cps = ceil_div(n, splits);
     const int64_t real_splits = ceil_div(n, cps);
     dim3 g1((unsigned)ceil_div(n, ROWS), (unsigned)real_splits);
