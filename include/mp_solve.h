@@ -179,6 +179,39 @@ const char *mp_version(void);
  * Returns MP_OK or MP_ERR_CUDA. */
 int mp_exec_info(int *lookahead, int *sms_panel, int *sms_update);
 
+/* ---------------------------------------------------------------- multi-GPU: 1D block-cyclic
+ * SURVEY 8(e), B:5 ("the matrix is distributed 1D block-cyclic by column blocks; each factored
+ * panel and its pivot vector are broadcast ... the distributed residual GEMV is followed by an
+ * allreduce of r").  One process per GPU.  Global column block j (nb columns) lives on rank
+ * j mod P at local block slot j / P; A_local holds this rank's columns in increasing global
+ * order (column-major, lda_local >= max(1, local columns)); B and X are replicated on every
+ * rank (n x nrhs, ld n).  All matrix / vector pointers are DEVICE pointers.  Calls are
+ * collective: every rank calls with the same n, nrhs, nb and returns the same iters / info
+ * (conventions as mp_dsgesv / mp_dgesv; info -5 / -7 for non-finite A / B).  Argument errors
+ * return info = -i for the i-th argument.  Collective failures return MP_ERR_NCCL. */
+typedef struct mp_comm mp_comm;
+
+/* NCCL unique id for mp_comm_init (create on one rank, share it with the others). */
+int mp_get_unique_id(char id[128]);
+/* NCCL communicator of rank `rank` of `nranks` (one process per GPU, current device). */
+int mp_comm_init(int nranks, int rank, const char id[128], mp_comm **comm);
+/* `nranks` emulated ranks of ONE process on the current GPU (testing the P > 1 algorithm on
+ * a single GPU): comms[r] is used by the host thread playing rank r; collectives meet at a
+ * host barrier and move data with device copies (no kernel ever waits for another rank). */
+int mp_comm_init_loopback(int nranks, mp_comm **comms);
+int mp_comm_destroy(mp_comm *comm);
+/* Number of columns of A owned by `rank` (the width of its A_local). */
+int64_t mp_1dbc_local_cols(int64_t n, int64_t nb, int nranks, int rank);
+
+int mp_dsgesv_1dbc(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local,
+                   int64_t lda_local, const double *B, double *X, int *iters, int *info);
+int mp_dsgesv_1dbc_ex(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local,
+                      int64_t lda_local, const double *B, double *X, int *iters, int *info,
+                      const mp_opts *opts, mp_report *rep);
+/* Distributed binary64 solver built the same way (the speedup denominator at P > 1). */
+int mp_dgesv_1dbc(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local,
+                  int64_t lda_local, const double *B, double *X, int *info);
+
 #ifdef __cplusplus
 }
 #endif

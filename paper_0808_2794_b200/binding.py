@@ -72,10 +72,21 @@ lib.mp_profile_collect.argtypes = [ctypes.POINTER(Report)]
 lib.mp_last_error.restype = ctypes.c_char_p
 lib.mp_version.restype = ctypes.c_char_p
 lib.mp_exec_info.argtypes = [_pi, _pi, _pi]
+lib.mp_get_unique_id.argtypes = [ctypes.c_char_p]
+lib.mp_comm_init.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_p)]
+lib.mp_comm_init_loopback.argtypes = [ctypes.c_int, ctypes.POINTER(_p)]
+lib.mp_comm_destroy.argtypes = [_p]
+lib.mp_1dbc_local_cols.argtypes = [_i64, _i64, ctypes.c_int, ctypes.c_int]
+lib.mp_1dbc_local_cols.restype = _i64
+lib.mp_dsgesv_1dbc_ex.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi, _pi, ctypes.POINTER(Opts),
+                                  ctypes.POINTER(Report)]
+lib.mp_dsgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi, _pi]
+lib.mp_dgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi]
 
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
-            "mp_profile_collect", "mp_exec_info")
+            "mp_profile_collect", "mp_exec_info", "mp_get_unique_id", "mp_comm_init", "mp_comm_init_loopback",
+            "mp_comm_destroy", "mp_1dbc_local_cols", "mp_dsgesv_1dbc", "mp_dsgesv_1dbc_ex", "mp_dgesv_1dbc")
 
 
 def mp_version() -> str:
@@ -230,3 +241,70 @@ def mp_exec_info():
     la, sp, su = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
     _check(lib.mp_exec_info(ctypes.byref(la), ctypes.byref(sp), ctypes.byref(su)))
     return la.value, sp.value, su.value
+
+
+# --------------------------------------------------------------------------- multi-GPU (1D block-cyclic)
+def local_columns(n: int, nb: int, nranks: int, rank: int) -> np.ndarray:
+    """Global column indices owned by `rank` (increasing): block j lives on rank j % nranks."""
+    nb = nb if nb > 0 else 256
+    cols = [np.arange(j * nb, min(n, (j + 1) * nb)) for j in range(rank, -(-n // nb), nranks)]
+    return np.concatenate(cols) if cols else np.zeros(0, dtype=np.int64)
+
+
+def mp_1dbc_local_cols(n: int, nb: int, nranks: int, rank: int) -> int:
+    return int(lib.mp_1dbc_local_cols(n, nb, nranks, rank))
+
+
+def mp_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.mp_get_unique_id(buf))
+    return buf.raw
+
+
+def mp_comm_init(nranks: int, rank: int, uid: bytes):
+    h = _p()
+    _check(lib.mp_comm_init(nranks, rank, uid, ctypes.byref(h)))
+    return h
+
+
+def mp_comm_init_loopback(nranks: int):
+    hs = (_p * nranks)()
+    _check(lib.mp_comm_init_loopback(nranks, hs))
+    return [_p(hs[r]) for r in range(nranks)]
+
+
+def mp_comm_destroy(comm):
+    _check(lib.mp_comm_destroy(comm))
+
+
+def mp_dsgesv_1dbc_ex(comm, n: int, nb: int, A_local, B, X=None, opts: Opts | None = None, report: bool = True):
+    """Distributed mixed-precision solve (collective).  A_local: this rank's columns (column-major CUDA
+    tensor, n x local_cols); B, X replicated CUDA tensors (n x nrhs, column-major).  -> (X, iters, info, rep)."""
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    nloc = A_local.shape[1] if len(A_local.shape) == 2 else 0
+    pa, lda = _ptr_ld(A_local, "A_local", False) if nloc > 0 else (None, 1)
+    pb, _ = _ptr_ld(B, "B", False)
+    px, _ = _ptr_ld(X, "X", False)
+    lib.mp_set_stream(_stream_of(B, X))
+    it, info = ctypes.c_int(0), ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_dsgesv_1dbc_ex(comm, n, nrhs, nb, pa, lda, pb, px, ctypes.byref(it), ctypes.byref(info),
+                                 ctypes.byref(opts) if opts is not None else None,
+                                 ctypes.byref(rep) if rep is not None else None))
+    return X, it.value, info.value, rep
+
+
+def mp_dgesv_1dbc(comm, n: int, nb: int, A_local, B, X=None):
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    nloc = A_local.shape[1] if len(A_local.shape) == 2 else 0
+    pa, lda = _ptr_ld(A_local, "A_local", False) if nloc > 0 else (None, 1)
+    pb, _ = _ptr_ld(B, "B", False)
+    px, _ = _ptr_ld(X, "X", False)
+    lib.mp_set_stream(_stream_of(B, X))
+    info = ctypes.c_int(0)
+    _check(lib.mp_dgesv_1dbc(comm, n, nrhs, nb, pa, lda, pb, px, ctypes.byref(info)))
+    return X, info.value

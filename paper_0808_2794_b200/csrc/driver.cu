@@ -805,6 +805,372 @@ int getrf_impl(int64_t n, const double *A, int64_t lda, T *LU, int32_t *ipiv_out
     return MP_OK;
 }
 
+// ------------------------------------------------------------------ 1D block-cyclic multi-GPU path
+// SURVEY 8(e) / B:5: global column block j (nb columns) lives on rank j mod P at local slot
+// j / P; A (binary64, caller's) and the working copy use the same distribution; B, X, r, z,
+// ipiv and perm are replicated.  Per panel step: the owner factors the panel (the single-GPU
+// recursive panel code, addressed through a column-shifted base pointer), broadcasts it with
+// its pivot list (NCCL), every rank applies the interchanges, U12 and the Schur update to its
+// own columns.  The factors are all-gathered once for the (replicated) triangular solves;
+// each residual is a local GEMV followed by an all-reduce of A_loc x_loc; rank 0's demoted
+// residual and verdict are broadcast so every rank refines identically.
+struct Dist {
+    int64_t n = 0, nb = 0, nblk = 0, nloc = 0;
+    int P = 1, r = 0;
+    int owner(int64_t j) const { return (int)(j % P); }
+    int64_t cols_of(int q) const
+    {
+        int64_t c = 0;
+        for (int64_t j = q; j < nblk; j += P) c += std::min<int64_t>(nb, n - j * nb);
+        return c;
+    }
+    // first local column whose global block is after block j
+    int64_t local_after(int64_t j) const
+    {
+        const int64_t s = (j - r) >= 0 ? (j - r) / P + 1 : 0;
+        return std::min<int64_t>(s * nb, nloc);
+    }
+};
+
+__device__ __forceinline__ int64_t gcol_of(int64_t lc, int64_t nb, int P, int q)
+{
+    return ((lc / nb) * P + q) * nb + lc % nb;
+}
+
+// Xloc[c * nloc + lc] = X[c * n + gcol(lc)]
+__global__ void gather_cols_kernel(const double *__restrict__ X, int64_t n, int64_t nrhs, double *__restrict__ Xloc,
+                                   int64_t nloc, int64_t nb, int P, int q)
+{
+    const int64_t tot = nloc * nrhs;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t / nloc, lc = t - c * nloc;
+        Xloc[t] = X[c * n + gcol_of(lc, nb, P, q)];
+    }
+}
+
+// send[i * nmax + lc] = Wl[i * ldw + lc] (lc < nloc), 0 up to nmax
+template <typename T>
+__global__ void pack_local_kernel(const T *__restrict__ Wl, int64_t ldw, int64_t n, int64_t nloc, int64_t nmax,
+                                  T *__restrict__ send)
+{
+    const int64_t tot = n * nmax;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / nmax, lc = t - i * nmax;
+        send[t] = lc < nloc ? Wl[i * ldw + lc] : T(0);
+    }
+}
+
+// Wf[i * ldf + gcol(q, lc)] = recv[q][i * nmax + lc] for every rank q and lc < its columns
+template <typename T>
+__global__ void unpack_gather_kernel(const T *__restrict__ recv, int64_t n, int64_t nmax, int64_t nb, int P,
+                                     T *__restrict__ Wf, int64_t ldf)
+{
+    const int64_t per = n * nmax, tot = per * P;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
+        const int q = (int)(t / per);
+        const int64_t rem = t - (int64_t)q * per, i = rem / nmax, lc = rem - i * nmax;
+        const int64_t g = gcol_of(lc, nb, P, q);
+        if (g < n) Wf[i * ldf + g] = recv[t];
+    }
+}
+
+// status flags over all ranks: every bit (and the first zero-pivot column) is reduced separately
+__global__ void flags_to_bits_kernel(const DevStatus *st, int32_t *bits)
+{
+    const int i = threadIdx.x;
+    if (i < 8) bits[i] = i < 5 ? ((st->flags >> i) & 1) : (i == 7 ? -st->zero_col : 0);
+}
+__global__ void bits_to_flags_kernel(DevStatus *st, const int32_t *bits)
+{
+    if (threadIdx.x == 0) {
+        int f = 0;
+        for (int i = 0; i < 5; ++i) f |= bits[i] << i;
+        st->flags = f;
+        st->zero_col = -bits[7];
+    }
+}
+void sync_status(Comm &cm, DevStatus *st, int32_t *bits, cudaStream_t s)
+{
+    if (cm.size <= 1) return;
+    flags_to_bits_kernel<<<1, 32, 0, s>>>(st, bits);
+    MP_LAUNCH_CHECK();
+    cm.allreduce_max(bits, 8, s);
+    bits_to_flags_kernel<<<1, 32, 0, s>>>(st, bits);
+    MP_LAUNCH_CHECK();
+}
+
+// binary-T factorisation of the distributed working copy Wl (n rows x ldw, local columns
+// [0, nloc), panel receive area [nloc, nloc + nb)); ipiv/perm replicated
+template <typename T>
+void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int32_t *perm, DevStatus *st,
+                 Pool &pool, cudaStream_t s, int variant)
+{
+    const int64_t n = d.n, nb = d.nb;
+    Factor<T> f;
+    f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = (int)nb; f.s = s;
+    f.sms = num_sms();
+    f.variant = variant;
+    f.ps.orig = pool.get<int32_t>(n);
+    f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
+    f.ps.npairs = pool.get<int32_t>(1);
+    f.ppairs[0] = pool.get<int32_t>(4 * (size_t)nb);
+    f.nppairs[0] = pool.get<int32_t>(1);
+    f.ps.ppairs = f.ppairs[0];
+    f.ps.nppairs = f.nppairs[0];
+    float *tf = nullptr;
+    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) tf = pool.get<float>(tf32_scratch_floats(n, (int)nb));
+    // broadcast buffer: [npairs][pairs 4nb][ipiv nb] then the panel rows (n - k) x nb
+    const size_t hdr = (1 + 4 * (size_t)nb + (size_t)nb) * sizeof(int32_t);
+    const size_t hdr_al = round_up((int64_t)hdr, 256);
+    char *buf = pool.get<char>(hdr_al + (size_t)n * nb * sizeof(T));
+    int32_t *b_np = reinterpret_cast<int32_t *>(buf), *b_pairs = b_np + 1, *b_ipiv = b_pairs + 4 * nb;
+    T *b_panel = reinterpret_cast<T *>(buf + hdr_al);
+    launch_init_perm(perm, n, s);
+    for (int64_t k = 0, j = 0; k < n; k += nb, ++j) {
+        const int w = (int)std::min<int64_t>(nb, n - k);
+        const int o = d.owner(j);
+        const int64_t lc0 = (j / d.P) * nb;                      // owner's local column of the panel
+        if (d.r == o) {
+            f.W = Wl + (lc0 - k);                                // global column c <-> local lc0 + (c - k)
+            f.factor_panel(s, k, w, 0);
+            MP_CUDA(cudaMemcpyAsync(b_np, f.nppairs[0], sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(b_pairs, f.ppairs[0], 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(b_ipiv, ipiv + k, w * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpy2DAsync(b_panel, nb * sizeof(T), Wl + k * ldw + lc0, ldw * sizeof(T), w * sizeof(T),
+                                      n - k, cudaMemcpyDeviceToDevice, s));
+        }
+        if (d.P > 1) cm.bcast(buf, hdr_al + (size_t)(n - k) * nb * sizeof(T), o, s);
+        if (d.r != o) {
+            MP_CUDA(cudaMemcpyAsync(f.nppairs[0], b_np, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(f.ppairs[0], b_pairs, 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(ipiv + k, b_ipiv, w * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpy2DAsync(Wl + k * ldw + d.nloc, ldw * sizeof(T), b_panel, nb * sizeof(T), w * sizeof(T),
+                                      n - k, cudaMemcpyDeviceToDevice, s));
+        }
+        // the panel's interchanges on this rank's other columns (+ the replicated permutation)
+        const int64_t xlo = d.r == o ? lc0 : 0, xhi = d.r == o ? lc0 + w : 0;
+        prof_begin(KC_LASWP, s);
+        launch_laswp_pairs<T>(Wl, ldw, f.ppairs[0], f.nppairs[0], 2 * w, 0, d.nloc, xlo, xhi, perm, s);
+        prof_end(KC_LASWP, 2.0 * 2 * w * (double)d.nloc * sizeof(T), s);
+        const T *Lp = d.r == o ? Wl + lc0 : Wl + d.nloc;        // column 0 of the panel
+        const int64_t lt0 = d.local_after(j), ntr = d.nloc - lt0;
+        if (ntr > 0 && k + w < n) {
+            prof_begin(KC_TRSM, s);
+            launch_trsm_ops<T>(Lp + k * ldw, ldw, Wl + k * ldw + lt0, ldw, w, ntr, s);
+            prof_end(KC_TRSM, (double)w * w * (double)ntr, s);
+            const int64_t M = n - k - w;
+            prof_begin(KC_TRAIL, s);
+            if constexpr (sizeof(T) == 4) {
+                if (tf && M >= 256 && ntr >= 128)
+                    launch_gemm_ops_3xtf32(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0,
+                                           ldw, M, ntr, w, tf, f.sms, s);
+                else
+                    launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0,
+                                       ldw, M, ntr, w, s);
+            } else {
+                launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0, ldw, M,
+                                   ntr, w, s);
+            }
+            prof_end(KC_TRAIL, 2.0 * M * ntr * w, s);
+        }
+    }
+}
+
+// all-gather the distributed factors into the full row-major working copy Wf (n x ldf)
+template <typename T>
+void dist_gather(Comm &cm, const Dist &d, const T *Wl, int64_t ldw, T *Wf, int64_t ldf, Pool &pool, cudaStream_t s)
+{
+    const int64_t nmax = ceil_div(d.nblk, d.P) * d.nb;
+    T *send = pool.get<T>((size_t)d.n * nmax);
+    T *recv = pool.get<T>((size_t)d.n * nmax * d.P);
+    const int64_t tot = d.n * nmax;
+    pack_local_kernel<T><<<(int)std::min<int64_t>(ceil_div(tot, 256), 8192), 256, 0, s>>>(Wl, ldw, d.n, d.nloc, nmax,
+                                                                                          send);
+    MP_LAUNCH_CHECK();
+    cm.allgather(send, recv, (size_t)tot * sizeof(T), s);
+    unpack_gather_kernel<T><<<(int)std::min<int64_t>(ceil_div(tot * d.P, 256), 8192), 256, 0, s>>>(
+        recv, d.n, nmax, d.nb, d.P, Wf, ldf);
+    MP_LAUNCH_CHECK();
+    g_launches += 2;
+}
+
+// binary64 solve on the distribution (fallback and mp_dgesv_1dbc): returns info
+int dist_fp64_solve(Comm &cm, const Dist &d, const double *A, int64_t lda, const double *B, double *X, int64_t nrhs,
+                    Pool &pool, StatusIO &sio, cudaStream_t s)
+{
+    const int64_t n = d.n;
+    const int64_t ldw = round_up(d.nloc + d.nb, 64), ldf = round_up(n, 64);
+    double *Wl = pool.get<double>((size_t)n * ldw);
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
+    sio.reset();
+    launch_demote_rect<double>(A, lda, n, d.nloc, Wl, ldw, nullptr, nullptr, sio.d, s);
+    dist_factor<double>(cm, d, Wl, ldw, ipiv, perm, sio.d, pool, s, MP_VARIANT_FFMA);
+    // status (a zero pivot is seen by the panel's owner only) -> every rank
+    sync_status(cm, sio.d, pool.get<int32_t>(8), s);
+    const DevStatus &st = sio.read();
+    if (st.flags & ST_A_NONFINITE) return -3;
+    if (st.flags & ST_ZERO_PIVOT) return st.zero_col;
+    double *Wf = pool.get<double>((size_t)n * ldf);
+    MP_CUDA(cudaMemsetAsync(Wf, 0, (size_t)n * ldf * sizeof(double), s));
+    dist_gather<double>(cm, d, Wl, ldw, Wf, ldf, pool, s);
+    double *Y = pool.get<double>((size_t)n * nrhs);
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<double>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    launch_invert_perm(perm, pinv, n, s);
+    launch_permute_demote_rhs<double>(B, n, nrhs, pinv, Y, sio.d, s);
+    launch_lu_solve<double>(Wf, ldf, n, nrhs, Y, X, 0, ss, s);
+    return 0;
+}
+
+int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double *A, int64_t lda, const double *B,
+                     double *X, int *iters, int *info, const mp_opts *opts, mp_report *rep, bool fp64_only)
+{
+    *info = 0; *iters = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    Dist d;
+    d.n = n; d.nb = nb > 0 ? nb : 256; d.P = cm.size; d.r = cm.rank;
+    d.nblk = n > 0 ? ceil_div(n, d.nb) : 0;
+    d.nloc = n > 0 ? d.cols_of(d.r) : 0;
+    const int64_t mx = std::max<int64_t>(1, d.nloc);
+    if (n < 0) return *info = -2, MP_OK;
+    if (nrhs < 0) return *info = -3, MP_OK;
+    if (nb < 0) return *info = -4, MP_OK;
+    if (n > 0 && d.nloc > 0 && !A) return *info = -5, MP_OK;
+    if (lda < mx) return *info = -6, MP_OK;
+    if (n > 0 && nrhs > 0 && (!B || !X)) return *info = -7, MP_OK;
+    if ((d.nloc > 0 && !is_device_ptr(A)) || (n > 0 && nrhs > 0 && (!is_device_ptr(B) || !is_device_ptr(X))))
+        throw std::runtime_error("mp_*_1dbc: A_local, B and X must be device pointers");
+    if (n == 0 || nrhs == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    cudaStream_t s = g_stream;
+    configure_mempool_once();
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    StatusIO sio(pool, s);
+    if (fp64_only) {
+        *info = dist_fp64_solve(cm, d, A, lda, B, X, nrhs, pool, sio, s);
+        MP_CUDA(cudaStreamSynchronize(s));
+        if (rep) { rep->info = *info; rep->nb = (int)d.nb; rep->t_total_ms = tm.ms(t0, tm.mark()); }
+        return MP_OK;
+    }
+    const int sms = num_sms();
+    const int64_t ldw = round_up(d.nloc + d.nb, 64), ldf = round_up(n, 64);
+    float *Wl = pool.get<float>((size_t)n * ldw);
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
+    float *Y = pool.get<float>((size_t)n * nrhs);
+    double *R = pool.get<double>((size_t)n * nrhs), *AX = pool.get<double>((size_t)n * nrhs);
+    double *Xloc = pool.get<double>((size_t)std::max<int64_t>(1, d.nloc) * nrhs);
+    ResidualScratch rs;
+    rs.partial = pool.get<double>(residual_partial_elems(n, nrhs, sms));
+    rs.blocksums = pool.get<double>((size_t)ceil_div(n, 256) * 2 * nrhs);
+    rs.counter = pool.get<unsigned>(1);
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<float>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    double *dpart = pool.get<double>((size_t)sms * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+
+    // ---- K1 on the local columns; ||A||_F^2 and the argument / overflow flags over all ranks
+    prof_begin(KC_DEMOTE, s);
+    launch_demote_rect<float>(A, lda, n, d.nloc, Wl, ldw, dpart, dcnt, sio.d, s);
+    prof_end(KC_DEMOTE, 12.0 * n * d.nloc, s);
+    launch_init_perm(perm, n, s);
+    launch_permute_demote_rhs<float>(B, n, nrhs, perm, Y, sio.d, s);
+    int32_t *bits = pool.get<int32_t>(8);
+    if (d.P > 1) {
+        cm.allreduce_sum(&sio.d->anrm2, 1, s);
+        sync_status(cm, sio.d, bits, s);
+    }
+    DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) { *info = -5; if (rep) rep->info = -5; return MP_OK; }
+    if (st0.flags & ST_B_NONFINITE) { *info = -7; if (rep) rep->info = -7; return MP_OK; }
+    const double anrm = std::sqrt(st0.anrm2);
+    const double cte = anrm * std::ldexp(1.0, -53) * std::sqrt((double)n);
+    int code = (st0.flags & ST_OVERFLOW) ? -2 : 0;
+    const int t_dem = tm.mark();
+    int t_fac = t_dem, t_ref = t_dem;
+    int nhist = 0;
+    double hist[MP_HIST_MAX] = {0};
+    float *Wf = nullptr;
+    if (!code) {
+        dist_factor<float>(cm, d, Wl, ldw, ipiv, perm, sio.d, pool, s, o.variant);
+        sync_status(cm, sio.d, bits, s);
+        t_fac = tm.mark();
+        const DevStatus &st1 = sio.read();
+        if (st1.flags & ST_ZERO_PIVOT) code = -3;
+    }
+    if (!code) {
+        Wf = pool.get<float>((size_t)n * ldf);
+        MP_CUDA(cudaMemsetAsync(Wf, 0, (size_t)n * ldf * sizeof(float), s));
+        dist_gather<float>(cm, d, Wl, ldw, Wf, ldf, pool, s);
+        launch_invert_perm(perm, pinv, n, s);
+        launch_permute_demote_rhs<float>(B, n, nrhs, pinv, Y, sio.d, s);
+        prof_begin(KC_SOLVE, s);
+        launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 0, ss, s);
+        prof_end(KC_SOLVE, 4.0 * n * n, s);
+        code = -31;
+        const int gblk = (int)std::min<int64_t>(ceil_div(d.nloc * nrhs, 256), 4096);
+        for (int it = 0; it <= itermax; ++it) {
+            prof_begin(KC_RESIDUAL, s);
+            if (d.nloc > 0) {
+                gather_cols_kernel<<<std::max(1, gblk), 256, 0, s>>>(X, n, nrhs, Xloc, d.nloc, d.nb, d.P, d.r);
+                MP_LAUNCH_CHECK();
+            }
+            launch_residual_products(A, lda, n, d.nloc, nrhs, Xloc, std::max<int64_t>(1, d.nloc), AX, rs, sms, s);
+            if (d.P > 1) cm.allreduce_sum(AX, (size_t)n * nrhs, s);
+            launch_residual_finalize<float>(AX, n, nrhs, B, X, R, pinv, Y, cte, rs, sio.d, s);
+            // rank 0's demoted residual and verdict drive every rank (identical refinement)
+            if (d.P > 1) {
+                cm.bcast(Y, (size_t)n * nrhs * sizeof(float), 0, s);
+                cm.bcast(sio.d, sizeof(DevStatus), 0, s);
+            }
+            prof_end(KC_RESIDUAL, 8.0 * n * d.nloc + 8.0 * 4 * n * nrhs, s);
+            const DevStatus &st = sio.read();
+            if (st.flags & ST_NORM_NONFINITE) break;
+            hist[nhist++] = st.ratio;
+            if (st.converged) { *iters = it; code = 0; break; }
+            if (it == itermax) break;
+            prof_begin(KC_SOLVE, s);
+            launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 1, ss, s);
+            prof_end(KC_SOLVE, 4.0 * n * n, s);
+        }
+        t_ref = tm.mark();
+    }
+    int t_fb = tm.mark();
+    if (code) {
+        *iters = code;
+        *info = dist_fp64_solve(cm, d, A, lda, B, X, nrhs, pool, sio, s);
+        t_fb = tm.mark();
+    }
+    MP_CUDA(cudaStreamSynchronize(s));
+    const int t_end = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = (int)d.nb; rep->variant = o.variant;
+        rep->anrm = anrm;
+        for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
+        rep->t_total_ms = tm.ms(t0, t_end);
+        rep->t_demote_ms = tm.ms(t0, t_dem);
+        rep->t_factor_ms = (t_fac != t_dem) ? tm.ms(t_dem, t_fac) : 0.0;
+        rep->t_refine_ms = (t_ref != t_dem) ? tm.ms(t_fac, t_ref) : 0.0;
+        rep->t_fallback_ms = code ? tm.ms(t_ref, t_fb) : 0.0;
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        if (!g_prof.deferred) prof_collect(rep);
+    }
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
+    return MP_OK;
+}
+
 template <typename F>
 int guarded(F &&f)
 {
@@ -819,6 +1185,9 @@ int guarded(F &&f)
     } catch (const NoMem &) {
         g_err = "device workspace allocation failed";
         return MP_ERR_NOMEM;
+    } catch (const CommError &e) {
+        g_err = e.what;
+        return MP_ERR_NCCL;
     } catch (const std::exception &e) {
         g_err = e.what();
         return MP_ERR_UNSUPPORTED;
@@ -924,6 +1293,79 @@ const char *mp_version(void)
 {
     return "libmpsolve 0.3 (sm_100a; variants: ffma, 3xtf32-tcgen05; blocked right-looking GEPP with look-ahead on "
            "green contexts, cluster panel, row-major working copy)";
+}
+
+struct mp_comm {
+    Comm *c;
+};
+
+int mp_get_unique_id(char id[128])
+{
+    if (!id) { g_err = "id must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { nccl_unique_id(id); return MP_OK; });
+}
+
+int mp_comm_init(int nranks, int rank, const char id[128], mp_comm **comm)
+{
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks) { g_err = "bad mp_comm_init arguments"; return MP_ERR_INTERNAL; }
+    return guarded([&] {
+        *comm = new mp_comm{make_nccl_comm(nranks, rank, id)};
+        return MP_OK;
+    });
+}
+
+int mp_comm_init_loopback(int nranks, mp_comm **comms)
+{
+    if (!comms || nranks < 1) { g_err = "bad mp_comm_init_loopback arguments"; return MP_ERR_INTERNAL; }
+    return guarded([&] {
+        std::vector<Comm *> cs(nranks);
+        make_loopback_comms(nranks, cs.data());
+        for (int r = 0; r < nranks; ++r) comms[r] = new mp_comm{cs[r]};
+        return MP_OK;
+    });
+}
+
+int mp_comm_destroy(mp_comm *comm)
+{
+    if (!comm) return MP_OK;
+    return guarded([&] {
+        delete comm->c;
+        delete comm;
+        return MP_OK;
+    });
+}
+
+int64_t mp_1dbc_local_cols(int64_t n, int64_t nb, int nranks, int rank)
+{
+    if (n <= 0 || nranks < 1 || rank < 0 || rank >= nranks) return 0;
+    Dist d;
+    d.n = n; d.nb = nb > 0 ? nb : 256; d.P = nranks; d.r = rank; d.nblk = ceil_div(n, d.nb);
+    return d.cols_of(rank);
+}
+
+int mp_dsgesv_1dbc_ex(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local, int64_t lda_local,
+                      const double *B, double *X, int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    if (!comm || !iters || !info) { g_err = "comm/iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] {
+        return dsgesv_1dbc_impl(*comm->c, n, nrhs, nb, A_local, lda_local, B, X, iters, info, opts, rep, false);
+    });
+}
+
+int mp_dsgesv_1dbc(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local, int64_t lda_local,
+                   const double *B, double *X, int *iters, int *info)
+{
+    return mp_dsgesv_1dbc_ex(comm, n, nrhs, nb, A_local, lda_local, B, X, iters, info, nullptr, nullptr);
+}
+
+int mp_dgesv_1dbc(mp_comm *comm, int64_t n, int64_t nrhs, int64_t nb, const double *A_local, int64_t lda_local,
+                  const double *B, double *X, int *info)
+{
+    if (!comm || !info) { g_err = "comm/info must not be NULL"; return MP_ERR_INTERNAL; }
+    int iters = 0;
+    return guarded([&] {
+        return dsgesv_1dbc_impl(*comm->c, n, nrhs, nb, A_local, lda_local, B, X, &iters, info, nullptr, nullptr, true);
+    });
 }
 
 int mp_exec_info(int *lookahead, int *sms_panel, int *sms_update)

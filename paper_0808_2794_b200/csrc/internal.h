@@ -79,6 +79,11 @@ template <typename T>
 void launch_demote_transpose(const double *A, int64_t lda, int64_t n, T *W, int64_t ldw,
                              double *partials, unsigned *counter, DevStatus *st, cudaStream_t s);
 
+// Rectangular form: rows n, columns ncols of A (column-major, lda) into W (row-major, ldw).
+template <typename T>
+void launch_demote_rect(const double *A, int64_t lda, int64_t n, int64_t ncols, T *W, int64_t ldw,
+                        double *partials, unsigned *counter, DevStatus *st, cudaStream_t s);
+
 // LU[i + j*n] = W[i*ldw + j]: packed factors back to the column-major ABI layout.
 template <typename T>
 void launch_transpose_out(const T *W, int64_t ldw, int64_t n, T *LU, cudaStream_t s);
@@ -123,6 +128,9 @@ void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStrea
 template <typename T>
 void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi,
                             cudaStream_t s);
+// Same with separate operands: X[w x ncols] <- L^{-1} X, L = unit lower w x w (row-major, ldl).
+template <typename T>
+void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s);
 
 // ---------------------------------------------------------------- K5 Schur update (k_gemm.cu)
 // C[M x N] -= A[M x K] * B[K x N], all row-major views into W with stride ldw:
@@ -131,11 +139,18 @@ template <typename T>
 void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                         int64_t K, cudaStream_t s);
 
+// Same update with separate row-major operands: C[M x N] -= A[M x K] * B[K x N] (lda, ldb, ldc).
+template <typename T>
+void launch_gemm_ops(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
+                     int64_t K, cudaStream_t s);
+
 // 3xTF32 tcgen05 variant (k_gemm_tf32.cu): same operation, binary32 W; scratch holds the
 // hi/lo splits of L21 and U12^T (tf32_scratch_floats(n, nb) floats).
 size_t tf32_scratch_floats(int64_t n, int nbmax);
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                                int64_t K, float *scratch, int num_sms, cudaStream_t s);
+void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s);
 
 // ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
 struct SolveScratch {
@@ -165,5 +180,34 @@ template <typename T>
 void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,
                      double *R, const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
                      int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- multi-GPU (comm.cu)
+struct CommError {
+    const char *what;
+};
+// Collectives of the 1D block-cyclic path, enqueued on (or synchronised with) stream s.
+struct Comm {
+    int rank = 0, size = 1;
+    virtual ~Comm() {}
+    virtual void bcast(void *buf, size_t bytes, int root, cudaStream_t s) = 0;
+    virtual void allreduce_sum(double *buf, size_t count, cudaStream_t s) = 0;
+    virtual void allreduce_max(int32_t *buf, size_t count, cudaStream_t s) = 0;
+    virtual void allgather(const void *send, void *recv, size_t bytes_per_rank, cudaStream_t s) = 0;
+};
+bool nccl_available();
+void nccl_unique_id(char id[128]);
+Comm *make_nccl_comm(int nranks, int rank, const char id[128]);
+void make_loopback_comms(int nranks, Comm **out);
+
+// AX = A X for a rows x cols block of A (column-major, lda) and X (cols x nrhs, ld ldx);
+// AX is rows x nrhs with ld rows (binary64; split-K partials reduced in a fixed order).
+void launch_residual_products(const double *A, int64_t lda, int64_t rows, int64_t cols, int64_t nrhs,
+                              const double *X, int64_t ldx, double *AX, ResidualScratch &rs, int num_sms,
+                              cudaStream_t s);
+// R = B - AX, norms and the B:5 verdict into *st, Y[pinv[i]] = (T) R[i] (as launch_residual).
+template <typename T>
+void launch_residual_finalize(const double *AX, int64_t n, int64_t nrhs, const double *B, const double *X, double *R,
+                              const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
+                              cudaStream_t s);
 
 }  // namespace mp

@@ -23,7 +23,7 @@ __device__ __forceinline__ float to_low(double a) { return __double2float_rn(a);
 
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(THREADS)
-demote_transpose_kernel(const double *__restrict__ A, int64_t lda, int64_t n, T *__restrict__ W,
+demote_transpose_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int64_t ncols, T *__restrict__ W,
                         int64_t ldw, double *__restrict__ partials, unsigned *counter, DevStatus *st)
 {
     constexpr bool LOW = sizeof(T) == 4;
@@ -46,7 +46,7 @@ demote_transpose_kernel(const double *__restrict__ A, int64_t lda, int64_t n, T 
             const int ii = lane * 2;
             const int64_t i = i0 + ii;
             double a0 = 0.0, a1 = 0.0;
-            if (j < n) {
+            if (j < ncols) {
                 const double *col = A + j * lda;
                 if (VEC && i + 1 < n) {
                     double2 v = __ldcs(reinterpret_cast<const double2 *>(col + i));
@@ -176,7 +176,7 @@ template void launch_transpose_out<float>(const float *, int64_t, int64_t, float
 template void launch_transpose_out<double>(const double *, int64_t, int64_t, double *, cudaStream_t);
 
 template <typename T>
-void launch_demote_transpose(const double *A, int64_t lda, int64_t n, T *W, int64_t ldw, double *partials,
+void launch_demote_rect(const double *A, int64_t lda, int64_t n, int64_t ncols, T *W, int64_t ldw, double *partials,
                              unsigned *counter, DevStatus *st, cudaStream_t s)
 {
     const int64_t ntiles = ceil_div(n, TILE) * (ldw / TILE);
@@ -186,11 +186,18 @@ void launch_demote_transpose(const double *A, int64_t lda, int64_t n, T *W, int6
     const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sms * 8);
     const bool vec = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
     if (vec)
-        demote_transpose_kernel<T, true><<<grid, THREADS, 0, s>>>(A, lda, n, W, ldw, partials, counter, st);
+        demote_transpose_kernel<T, true><<<grid, THREADS, 0, s>>>(A, lda, n, ncols, W, ldw, partials, counter, st);
     else
-        demote_transpose_kernel<T, false><<<grid, THREADS, 0, s>>>(A, lda, n, W, ldw, partials, counter, st);
+        demote_transpose_kernel<T, false><<<grid, THREADS, 0, s>>>(A, lda, n, ncols, W, ldw, partials, counter, st);
     MP_LAUNCH_CHECK();
     ++g_launches;
+}
+
+template <typename T>
+void launch_demote_transpose(const double *A, int64_t lda, int64_t n, T *W, int64_t ldw, double *partials,
+                             unsigned *counter, DevStatus *st, cudaStream_t s)
+{
+    launch_demote_rect<T>(A, lda, n, n, W, ldw, partials, counter, st, s);
 }
 
 template <typename T>
@@ -204,6 +211,10 @@ void launch_permute_demote_rhs(const double *B, int64_t n, int64_t nrhs, const i
     ++g_launches;
 }
 
+template void launch_demote_rect<float>(const double *, int64_t, int64_t, int64_t, float *, int64_t, double *,
+                                        unsigned *, DevStatus *, cudaStream_t);
+template void launch_demote_rect<double>(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *,
+                                         unsigned *, DevStatus *, cudaStream_t);
 template void launch_demote_transpose<float>(const double *, int64_t, int64_t, float *, int64_t, double *,
                                              unsigned *, DevStatus *, cudaStream_t);
 template void launch_demote_transpose<double>(const double *, int64_t, int64_t, double *, int64_t, double *,

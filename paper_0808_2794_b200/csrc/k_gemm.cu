@@ -38,55 +38,55 @@ struct Cfg {
 
 template <typename T, int BM, int BN, int BK, int TM, int TN, bool VEC>
 __global__ void __launch_bounds__(Cfg<T, BM, BN, BK, TM, TN>::NT, 2)
-gemm_update_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                   int64_t K)
+gemm_update_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int64_t ldb, T *__restrict__ C,
+                   int64_t ldc, int64_t M, int64_t N, int64_t K)
 {
-    using C = Cfg<T, BM, BN, BK, TM, TN>;
-    constexpr int NT = C::NT;
+    using Cf = Cfg<T, BM, BN, BK, TM, TN>;
+    constexpr int NT = Cf::NT;
     __shared__ __align__(16) T As[2][BK][BM];
     __shared__ __align__(16) T Bs[2][BK][BN];
     const int tid = threadIdx.x;
     const int64_t bm0 = (int64_t)blockIdx.y * BM, bn0 = (int64_t)blockIdx.x * BN;
-    const T *Ag = W + (r0 + bm0) * ldw + k0;          // L21 block rows
-    const T *Bg = W + k0 * ldw + c0 + bn0;            // U12 block columns
-    T *Cg = W + (r0 + bm0) * ldw + c0 + bn0;
+    const T *Ag = A + bm0 * lda;                      // L21 block rows
+    const T *Bg = B + bn0;                            // U12 block columns
+    T *Cg = C + bm0 * ldc + bn0;
 
     // loader coordinates
-    const int a_row = tid / C::A_TPR, a_k = (tid % C::A_TPR) * C::A_PER;
-    const int b_k = tid / C::B_TPR, b_n = (tid % C::B_TPR) * C::B_PER;
-    T ra[C::A_PER], rb[C::B_PER];
+    const int a_row = tid / Cf::A_TPR, a_k = (tid % Cf::A_TPR) * Cf::A_PER;
+    const int b_k = tid / Cf::B_TPR, b_n = (tid % Cf::B_TPR) * Cf::B_PER;
+    T ra[Cf::A_PER], rb[Cf::B_PER];
 
     auto load_slice = [&](int64_t kk) {
         const bool arow_ok = bm0 + a_row < M;
-        if (VEC && arow_ok && kk + a_k + C::A_PER <= K) {
-            using V = typename Vec<T, C::A_PER>::type;
-            V v = *reinterpret_cast<const V *>(Ag + a_row * ldw + kk + a_k);
+        if (VEC && arow_ok && kk + a_k + Cf::A_PER <= K) {
+            using V = typename Vec<T, Cf::A_PER>::type;
+            V v = *reinterpret_cast<const V *>(Ag + a_row * lda + kk + a_k);
             const T *pv = reinterpret_cast<const T *>(&v);
 #pragma unroll
-            for (int e = 0; e < C::A_PER; ++e) ra[e] = pv[e];
+            for (int e = 0; e < Cf::A_PER; ++e) ra[e] = pv[e];
         } else {
 #pragma unroll
-            for (int e = 0; e < C::A_PER; ++e)
-                ra[e] = (arow_ok && kk + a_k + e < K) ? Ag[a_row * ldw + kk + a_k + e] : T(0);
+            for (int e = 0; e < Cf::A_PER; ++e)
+                ra[e] = (arow_ok && kk + a_k + e < K) ? Ag[a_row * lda + kk + a_k + e] : T(0);
         }
         const bool bk_ok = kk + b_k < K;
-        if (VEC && bk_ok && bn0 + b_n + C::B_PER <= N) {
-            using V = typename Vec<T, C::B_PER>::type;
-            V v = *reinterpret_cast<const V *>(Bg + (kk + b_k) * ldw + b_n);
+        if (VEC && bk_ok && bn0 + b_n + Cf::B_PER <= N) {
+            using V = typename Vec<T, Cf::B_PER>::type;
+            V v = *reinterpret_cast<const V *>(Bg + (kk + b_k) * ldb + b_n);
             const T *pv = reinterpret_cast<const T *>(&v);
 #pragma unroll
-            for (int e = 0; e < C::B_PER; ++e) rb[e] = pv[e];
+            for (int e = 0; e < Cf::B_PER; ++e) rb[e] = pv[e];
         } else {
 #pragma unroll
-            for (int e = 0; e < C::B_PER; ++e)
-                rb[e] = (bk_ok && bn0 + b_n + e < N) ? Bg[(kk + b_k) * ldw + b_n + e] : T(0);
+            for (int e = 0; e < Cf::B_PER; ++e)
+                rb[e] = (bk_ok && bn0 + b_n + e < N) ? Bg[(kk + b_k) * ldb + b_n + e] : T(0);
         }
     };
     auto store_slice = [&](int buf) {
 #pragma unroll
-        for (int e = 0; e < C::A_PER; ++e) As[buf][a_k + e][a_row] = ra[e];
+        for (int e = 0; e < Cf::A_PER; ++e) As[buf][a_k + e][a_row] = ra[e];
 #pragma unroll
-        for (int e = 0; e < C::B_PER; ++e) Bs[buf][b_k][b_n + e] = rb[e];
+        for (int e = 0; e < Cf::B_PER; ++e) Bs[buf][b_k][b_n + e] = rb[e];
     };
 
     constexpr int TX = BN / TN;                       // threads along n
@@ -134,7 +134,7 @@ gemm_update_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64
     for (int i = 0; i < TM; ++i) {
         const int row = (i < HM) ? ty * HM + i : BM / 2 + ty * HM + (i - HM);
         if (bm0 + row >= M) continue;
-        T *crow = Cg + (int64_t)row * ldw;
+        T *crow = Cg + (int64_t)row * ldc;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int col = (h == 0) ? tx * HN : BN / 2 + tx * HN;
@@ -155,16 +155,17 @@ gemm_update_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64
 }
 
 template <typename T, int BM, int BN, int BK, int TM, int TN>
-void launch_tiles(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
-                  cudaStream_t s)
+void launch_tiles(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
+                  int64_t K, cudaStream_t s)
 {
-    using C = Cfg<T, BM, BN, BK, TM, TN>;
+    using Cf = Cfg<T, BM, BN, BK, TM, TN>;
     dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM));
-    const bool vec = ((uintptr_t)W % 32 == 0) && (ldw % 8 == 0) && (k0 % 4 == 0) && (c0 % 4 == 0);
+    auto al = [](const void *p, int64_t ld) { return ((uintptr_t)p % 32 == 0) && (ld % 8 == 0); };
+    const bool vec = al(A, lda) && al(B, ldb) && al(C, ldc);
     if (vec)
-        gemm_update_kernel<T, BM, BN, BK, TM, TN, true><<<grid, C::NT, 0, s>>>(W, ldw, r0, c0, k0, M, N, K);
+        gemm_update_kernel<T, BM, BN, BK, TM, TN, true><<<grid, Cf::NT, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
     else
-        gemm_update_kernel<T, BM, BN, BK, TM, TN, false><<<grid, C::NT, 0, s>>>(W, ldw, r0, c0, k0, M, N, K);
+        gemm_update_kernel<T, BM, BN, BK, TM, TN, false><<<grid, Cf::NT, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
     MP_LAUNCH_CHECK();
     ++g_launches;
 }
@@ -176,7 +177,8 @@ void launch_tiles(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t
 // blocked FMA loop over K.  Latency-oriented: a single load phase, no k-slice pipeline.
 template <typename T, int BM, int NMAX>
 __global__ void __launch_bounds__(256)
-tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int M, int N, int K)
+tsgemm_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int64_t ldb, T *__restrict__ C,
+              int64_t ldc, int M, int N, int K)
 {
     constexpr int TX = 16, TY = 16;                     // threads along N, along rows
     constexpr int TN = NMAX / TX, TM = BM / TY;
@@ -193,7 +195,7 @@ tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int idx = b0 + u * 256, k = idx / NMAX, j = idx - k * NMAX;
-            v[u] = (idx < K * NMAX && j < N) ? W[(k0 + k) * ldw + c0 + j] : T(0);
+            v[u] = (idx < K * NMAX && j < N) ? B[(int64_t)k * ldb + j] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -206,7 +208,7 @@ tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int idx = b0 + u * 256, i = idx / K, k = idx - i * K;
-            v[u] = (idx < BM * K && bm0 + i < M) ? W[(r0 + bm0 + i) * ldw + k0 + k] : T(0);
+            v[u] = (idx < BM * K && bm0 + i < M) ? A[(bm0 + i) * lda + k] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -236,7 +238,7 @@ tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0
     for (int i = 0; i < TM; ++i) {
         const int64_t row = bm0 + ty * TM + i;
         if (row >= M) continue;
-        T *crow = W + (r0 + row) * ldw + c0;
+        T *crow = C + row * ldc;
 #pragma unroll
         for (int j = 0; j < TN; ++j) {
             const int col = tx * TN + j;
@@ -246,12 +248,13 @@ tsgemm_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0
 }
 
 template <typename T, int BM, int NMAX>
-void launch_ts(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, cudaStream_t s)
+void launch_ts(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+               cudaStream_t s)
 {
     const size_t smem = ((size_t)128 * (BM + 4) + (size_t)128 * (NMAX + 4)) * sizeof(T);
     auto kern = tsgemm_kernel<T, BM, NMAX>;
     func_smem_once((const void *)kern, smem);
-    kern<<<(unsigned)ceil_div(M, BM), 256, smem, s>>>(W, ldw, r0, c0, k0, (int)M, (int)N, (int)K);
+    kern<<<(unsigned)ceil_div(M, BM), 256, smem, s>>>(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K);
     MP_LAUNCH_CHECK();
     ++g_launches;
 }
@@ -259,24 +262,36 @@ void launch_ts(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M,
 }  // namespace
 
 template <>
-void launch_gemm_update<float>(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, cudaStream_t s)
+void launch_gemm_ops<float>(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,
+                            int64_t M, int64_t N, int64_t K, cudaStream_t s)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
-    if (K <= 128 && N <= 32) return launch_ts<float, 64, 32>(W, ldw, r0, c0, k0, M, N, K, s);
-    if (K <= 128 && N <= 64) return launch_ts<float, 64, 64>(W, ldw, r0, c0, k0, M, N, K, s);
-    if (K <= 128 && N <= 128) return launch_ts<float, 64, 128>(W, ldw, r0, c0, k0, M, N, K, s);
-    launch_tiles<float, 128, 128, 8, 8, 8>(W, ldw, r0, c0, k0, M, N, K, s);
+    if (K <= 128 && N <= 32) return launch_ts<float, 64, 32>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (K <= 128 && N <= 64) return launch_ts<float, 64, 64>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (K <= 128 && N <= 128) return launch_ts<float, 64, 128>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    launch_tiles<float, 128, 128, 8, 8, 8>(A, lda, B, ldb, C, ldc, M, N, K, s);
 }
 
 template <>
-void launch_gemm_update<double>(double *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                                int64_t K, cudaStream_t s)
+void launch_gemm_ops<double>(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+                             int64_t M, int64_t N, int64_t K, cudaStream_t s)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
-    if (K <= 128 && N <= 32) return launch_ts<double, 32, 32>(W, ldw, r0, c0, k0, M, N, K, s);
-    if (K <= 128 && N <= 64) return launch_ts<double, 32, 64>(W, ldw, r0, c0, k0, M, N, K, s);
-    launch_tiles<double, 128, 64, 8, 8, 4>(W, ldw, r0, c0, k0, M, N, K, s);
+    if (K <= 128 && N <= 32) return launch_ts<double, 32, 32>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    if (K <= 128 && N <= 64) return launch_ts<double, 32, 64>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    launch_tiles<double, 128, 64, 8, 8, 4>(A, lda, B, ldb, C, ldc, M, N, K, s);
 }
+
+template <typename T>
+void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
+                        cudaStream_t s)
+{
+    launch_gemm_ops<T>(W + r0 * ldw + k0, ldw, W + k0 * ldw + c0, ldw, W + r0 * ldw + c0, ldw, M, N, K, s);
+}
+
+template void launch_gemm_update<float>(float *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                        cudaStream_t);
+template void launch_gemm_update<double>(double *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                         cudaStream_t);
 
 }  // namespace mp

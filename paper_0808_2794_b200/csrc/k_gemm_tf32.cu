@@ -288,28 +288,28 @@ __device__ __forceinline__ float rna_tf32(float x)
     return __uint_as_float(r);
 }
 
-__global__ void split_rows_kernel(const float *__restrict__ W, int64_t ldw, int64_t r0, int64_t k0, int M, int K,
+__global__ void split_rows_kernel(const float *__restrict__ A, int64_t lda, int M, int K,
                                   float *__restrict__ hi, float *__restrict__ lo, int kp)
 {
     const int64_t tot = (int64_t)M * kp;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / kp;
         const int k = (int)(t - i * kp);
-        const float x = k < K ? W[(r0 + i) * ldw + k0 + k] : 0.f;
+        const float x = k < K ? A[i * lda + k] : 0.f;
         const float h = rna_tf32(x);
         hi[t] = h;
         lo[t] = rna_tf32(x - h);
     }
 }
 
-__global__ void split_cols_T_kernel(const float *__restrict__ W, int64_t ldw, int64_t k0, int64_t c0, int N, int K,
+__global__ void split_cols_T_kernel(const float *__restrict__ B, int64_t ldb, int N, int K,
                                     float *__restrict__ hi, float *__restrict__ lo, int kp)
 {
     __shared__ float tile[32][33];
     const int jb = blockIdx.x * 32, kb = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {               // read U12(kb + r, jb + tx): coalesced
         const int k = kb + r, j = jb + threadIdx.x;
-        tile[r][threadIdx.x] = (k < K && j < N) ? W[(k0 + k) * ldw + c0 + j] : 0.f;
+        tile[r][threadIdx.x] = (k < K && j < N) ? B[(int64_t)k * ldb + j] : 0.f;
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {               // write [j][k]: coalesced along k
@@ -352,8 +352,8 @@ size_t tf32_scratch_floats(int64_t n, int nbmax)
     return (size_t)4 * (size_t)n * (size_t)kp + 4096;
 }
 
-void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, float *scratch, int num_sms, cudaStream_t s)
+void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int kp = (int)round_up(K, 4);
@@ -361,11 +361,11 @@ void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, in
     float *Uh = Ll + (size_t)M * kp, *Ul = Uh + (size_t)N * kp;
     {
         const int64_t tot = M * kp;
-        split_rows_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 4096), 256, 0, s>>>(W, ldw, r0, k0, (int)M, (int)K,
-                                                                                              Lh, Ll, kp);
+        split_rows_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 4096), 256, 0, s>>>(A, lda, (int)M, (int)K, Lh,
+                                                                                              Ll, kp);
         MP_LAUNCH_CHECK();
         dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(kp, 32));
-        split_cols_T_kernel<<<g, dim3(32, 8), 0, s>>>(W, ldw, k0, c0, (int)N, (int)K, Uh, Ul, kp);
+        split_cols_T_kernel<<<g, dim3(32, 8), 0, s>>>(B, ldb, (int)N, (int)K, Uh, Ul, kp);
         MP_LAUNCH_CHECK();
     }
     CUtensorMap mUh, mUl, mLh, mLl;
@@ -377,9 +377,16 @@ void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, in
     const int grid = std::min(ntiles, num_sms);
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
     func_smem_once((const void *)gemm_3xtf32_kernel, smem);
-    gemm_3xtf32_kernel<<<grid, GT, smem, s>>>(mUh, mUl, mLh, mLl, W + r0 * ldw + c0, ldw, (int)M, (int)N, (int)K);
+    gemm_3xtf32_kernel<<<grid, GT, smem, s>>>(mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N, (int)K);
     MP_LAUNCH_CHECK();
     g_launches += 3;
+}
+
+void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s)
+{
+    launch_gemm_ops_3xtf32(W + r0 * ldw + k0, ldw, W + k0 * ldw + c0, ldw, W + r0 * ldw + c0, ldw, M, N, K, scratch,
+                           num_sms, s);
 }
 
 }  // namespace mp

@@ -28,19 +28,19 @@ constexpr int JU = 8;                // column unroll (loads in flight per threa
 
 template <bool VEC, int R>
 __global__ void __launch_bounds__(RT)
-residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int nrhs,
-                        const double *__restrict__ X, double *__restrict__ partial, int64_t cols_per_split,
-                        int c_off, int nrhs_total)
+residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int64_t ncols, int nrhs,
+                        const double *__restrict__ X, int64_t ldx, double *__restrict__ partial,
+                        int64_t cols_per_split, int c_off, int nrhs_total)
 {
     extern __shared__ __align__(16) double xs[];        // [cols_per_split][MAXR]
     const int s = blockIdx.y;
     const int64_t j0 = (int64_t)s * cols_per_split;
-    const int64_t j1 = (n < j0 + cols_per_split) ? n : j0 + cols_per_split;
+    const int64_t j1 = (ncols < j0 + cols_per_split) ? ncols : j0 + cols_per_split;
     const int64_t i = (int64_t)blockIdx.x * ROWS + 2 * threadIdx.x;
     for (int64_t idx = threadIdx.x; idx < (j1 - j0) * nrhs; idx += RT) {
         const int64_t jj = idx / nrhs;
         const int c = (int)(idx - jj * nrhs);
-        xs[jj * R + c] = X[c * n + j0 + jj];
+        xs[jj * R + c] = X[c * ldx + j0 + jj];
     }
     __syncthreads();
     double acc0[R], acc1[R];
@@ -177,16 +177,15 @@ size_t residual_partial_elems(int64_t n, int64_t nrhs, int num_sms)
     return (size_t)residual_splits(n, nrhs, num_sms) * (size_t)nrhs * (size_t)n;
 }
 
-template <typename T>
-void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,
-                     double *R, const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
-                     int num_sms, cudaStream_t s)
+// split-K partial products of a rows x cols block: partial[s][c][i]
+static int64_t launch_partials(const double *A, int64_t lda, int64_t rows, int64_t cols, int64_t nrhs,
+                               const double *X, int64_t ldx, ResidualScratch &rs, int num_sms, cudaStream_t s)
 {
     const int nr = (int)nrhs;
-    const int64_t splits = residual_splits(n, nrhs, num_sms);
-    const int64_t cps = ceil_div(n, splits);
-    const int64_t real_splits = ceil_div(n, cps);
-    dim3 g1((unsigned)ceil_div(n, ROWS), (unsigned)real_splits);
+    const int64_t splits = residual_splits(std::max(rows, cols), nrhs, num_sms);
+    const int64_t cps = ceil_div(cols, splits);
+    const int64_t real_splits = ceil_div(cols, cps);
+    dim3 g1((unsigned)ceil_div(rows, ROWS), (unsigned)real_splits);
     const bool vec = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
     for (int c0 = 0; c0 < nr; c0 += MAXR) {
         const int nc = std::min(MAXR, nr - c0);
@@ -194,16 +193,69 @@ void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, cons
         auto kern = vec ? (nc == 1 ? residual_partial_kernel<true, 1> : residual_partial_kernel<true, MAXR>)
                         : (nc == 1 ? residual_partial_kernel<false, 1> : residual_partial_kernel<false, MAXR>);
         if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-        kern<<<g1, RT, smem, s>>>(A, lda, n, nc, X + c0 * n, rs.partial, cps, c0, nr);
+        kern<<<g1, RT, smem, s>>>(A, lda, rows, cols, nc, X + c0 * ldx, ldx, rs.partial, cps, c0, nr);
     }
     MP_LAUNCH_CHECK();
-    const int g2 = (int)ceil_div(n, RT);
-    residual_finalize_kernel<T><<<g2, RT, 0, s>>>(n, nr, (int)real_splits, B, X, rs.partial, R, pinv, Y, cte,
-                                                  rs.blocksums, rs.counter, st);
-    MP_LAUNCH_CHECK();
-    g_launches += 1 + ceil_div(nr, MAXR);
+    g_launches += ceil_div(nr, MAXR);
+    return real_splits;
 }
 
+__global__ void reduce_splits_kernel(const double *__restrict__ partial, int64_t count, int splits, double *__restrict__ out)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        for (int s = 0; s < splits; ++s) v += partial[(int64_t)s * count + i];
+        out[i] = v;
+    }
+}
+
+void launch_residual_products(const double *A, int64_t lda, int64_t rows, int64_t cols, int64_t nrhs,
+                              const double *X, int64_t ldx, double *AX, ResidualScratch &rs, int num_sms,
+                              cudaStream_t s)
+{
+    if (cols <= 0) {
+        MP_CUDA(cudaMemsetAsync(AX, 0, (size_t)rows * nrhs * sizeof(double), s));
+        return;
+    }
+    const int64_t splits = launch_partials(A, lda, rows, cols, nrhs, X, ldx, rs, num_sms, s);
+    const int64_t count = rows * nrhs;
+    reduce_splits_kernel<<<(int)std::min<int64_t>(ceil_div(count, 256), 1024), 256, 0, s>>>(rs.partial, count,
+                                                                                              (int)splits, AX);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
+template <typename T>
+void launch_residual_finalize(const double *AX, int64_t n, int64_t nrhs, const double *B, const double *X, double *R,
+                              const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
+                              cudaStream_t s)
+{
+    const int g2 = (int)ceil_div(n, RT);
+    residual_finalize_kernel<T><<<g2, RT, 0, s>>>(n, (int)nrhs, 1, B, X, AX, R, pinv, Y, cte, rs.blocksums,
+                                                  rs.counter, st);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
+template <typename T>
+void launch_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *X,
+                     double *R, const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
+                     int num_sms, cudaStream_t s)
+{
+    const int64_t splits = launch_partials(A, lda, n, n, nrhs, X, n, rs, num_sms, s);
+    const int g2 = (int)ceil_div(n, RT);
+    residual_finalize_kernel<T><<<g2, RT, 0, s>>>(n, (int)nrhs, (int)splits, B, X, rs.partial, R, pinv, Y, cte,
+                                                  rs.blocksums, rs.counter, st);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
+template void launch_residual_finalize<float>(const double *, int64_t, int64_t, const double *, const double *,
+                                              double *, const int32_t *, float *, double, ResidualScratch &,
+                                              DevStatus *, cudaStream_t);
+template void launch_residual_finalize<double>(const double *, int64_t, int64_t, const double *, const double *,
+                                               double *, const int32_t *, double *, double, ResidualScratch &,
+                                               DevStatus *, cudaStream_t);
 template void launch_residual<float>(const double *, int64_t, int64_t, int64_t, const double *, const double *,
                                      double *, const int32_t *, float *, double, ResidualScratch &, DevStatus *, int,
                                      cudaStream_t);

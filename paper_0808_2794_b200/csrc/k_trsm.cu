@@ -42,9 +42,10 @@ __device__ __forceinline__ void load_lt(const T *W, int64_t ldw, int64_t r, int6
     }
 }
 
+// L: top-left of the unit-lower w x w block (row-major, ldl); X: top-left of the w x ncols target.
 template <typename T>
 __global__ void __launch_bounds__(MAXB * 32, 2)
-trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi)
+trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int nb = (w + RB - 1) / RB;
@@ -55,19 +56,19 @@ trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_
     if (threadIdx.x < MAXB) flag[threadIdx.x] = 0;
     __syncthreads();
     if (b >= nb) return;
-    const int64_t col = c_lo + (int64_t)blockIdx.x * CWS + lane;
-    const bool cvalid = col < c_hi;
+    const int64_t col = (int64_t)blockIdx.x * CWS + lane;
+    const bool cvalid = col < ncols;
     const int rows = (w - b * RB < RB) ? (w - b * RB) : RB;   // rows of this block
-    const int64_t rb0 = r0 + (int64_t)b * RB;
+    const int64_t rb0 = (int64_t)b * RB;                       // block row offset inside L / X
     T *lt = Lt + (size_t)b * RB * LP;
 
     T x[RB];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) x[i] = (cvalid && i < rows) ? W[(rb0 + i) * ldw + col] : T(0);
+    for (int i = 0; i < RB; ++i) x[i] = (cvalid && i < rows) ? X[(rb0 + i) * ldx + col] : T(0);
 
     // contributions of the earlier row blocks, in the order they are published
     for (int k = 0; k < b; ++k) {
-        load_lt(W, ldw, rb0, r0 + (int64_t)k * RB, rows, RB, lt, lane);   // L(b, k), independent of X_k
+        load_lt(L, ldl, rb0, (int64_t)k * RB, rows, RB, lt, lane);      // L(b, k), independent of X_k
         __syncwarp();
         while (flag[k] == 0) { }
         __threadfence_block();
@@ -88,7 +89,7 @@ trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_
         __syncwarp();
     }
     // the 32 x 32 unit-lower diagonal block
-    load_lt(W, ldw, rb0, rb0, rows, rows, lt, lane);
+    load_lt(L, ldl, rb0, rb0, rows, rows, lt, lane);
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < RB; ++i) {
@@ -105,26 +106,34 @@ trsm_lower_unit_kernel(T *__restrict__ W, int64_t ldw, int64_t r0, int w, int64_
     if (lane == 0) flag[b] = 1;
 #pragma unroll
     for (int i = 0; i < RB; ++i)
-        if (cvalid && i < rows) W[(rb0 + i) * ldw + col] = x[i];
+        if (cvalid && i < rows) X[(rb0 + i) * ldx + col] = x[i];
 }
 
 }  // namespace
 
 template <typename T>
-void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi, cudaStream_t s)
+void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s)
 {
-    if (c_hi <= c_lo || w <= 0) return;
+    if (ncols <= 0 || w <= 0) return;
     if (w > MAXB * RB) throw CudaError{cudaErrorInvalidValue, "trsm block wider than 256", __LINE__};
     const int nb = (w + RB - 1) / RB;
-    const int grid = (int)ceil_div(c_hi - c_lo, CWS);
+    const int grid = (int)ceil_div(ncols, CWS);
     const size_t smem = ((size_t)nb * RB * CWS + (size_t)nb * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
     auto kern = trsm_lower_unit_kernel<T>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    kern<<<grid, nb * 32, smem, s>>>(W, ldw, r0, w, c_lo, c_hi);
+    kern<<<grid, nb * 32, smem, s>>>(L, ldl, X, ldx, w, ncols);
     MP_LAUNCH_CHECK();
     ++g_launches;
 }
 
+template <typename T>
+void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi, cudaStream_t s)
+{
+    launch_trsm_ops<T>(W + r0 * ldw + r0, ldw, W + r0 * ldw + c_lo, ldw, w, c_hi - c_lo, s);
+}
+
+template void launch_trsm_ops<float>(const float *, int64_t, float *, int64_t, int, int64_t, cudaStream_t);
+template void launch_trsm_ops<double>(const double *, int64_t, double *, int64_t, int, int64_t, cudaStream_t);
 template void launch_trsm_lower_unit<float>(float *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t);
 template void launch_trsm_lower_unit<double>(double *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t);
 
