@@ -36,6 +36,14 @@
 namespace mp {
 
 thread_local int64_t g_launches = 0;
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char *e = std::getenv("MP_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
 
 namespace {
 std::mutex g_attr_mu;
@@ -70,7 +78,7 @@ struct NoMem {};
 
 // ------------------------------------------------------------------ per-class timing
 namespace {
-struct ProfRec { int cls, a, b; double work; };
+struct ProfRec { int cls, a, b; double work; cudaStream_t s; };
 struct ProfState {
     bool on = false;
     unsigned mask = ~0u;         // classes recorded (flags bit 3: trailing update + residual only)
@@ -109,7 +117,7 @@ void prof_end(int cls, double work, cudaStream_t s)
     if (!g_prof.on || !((g_prof.mask >> cls) & 1u)) return;
     const int i = g_prof.take();
     MP_CUDA(cudaEventRecord(g_prof.ev[i], s));
-    g_prof.recs.push_back({cls, g_prof.open[cls], i, work});
+    g_prof.recs.push_back({cls, g_prof.open[cls], i, work, s});
 }
 
 static void prof_collect(mp_report *rep)
@@ -119,11 +127,15 @@ static void prof_collect(mp_report *rep)
         if (FILE *f = std::fopen(path, "a")) {
             static const char *names[] = {"demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "trail"};
             std::fprintf(f, "# call\n");
+            std::vector<cudaStream_t> sids;
             for (const ProfRec &r : g_prof.recs) {
+                int sid = 0;
+                while (sid < (int)sids.size() && sids[sid] != r.s) ++sid;
+                if (sid == (int)sids.size()) sids.push_back(r.s);
                 float t0 = 0.f, t1 = 0.f;
                 cudaEventElapsedTime(&t0, g_prof.ev[g_prof.recs[0].a], g_prof.ev[r.a]);
                 cudaEventElapsedTime(&t1, g_prof.ev[g_prof.recs[0].a], g_prof.ev[r.b]);
-                std::fprintf(f, "%s %.4f %.4f\n", names[r.cls], t0, t1);
+                std::fprintf(f, "%s %.4f %.4f %d\n", names[r.cls], t0, t1, sid);
             }
             std::fclose(f);
         }
@@ -380,7 +392,7 @@ struct Factor {
     }
     // panel [k, k+w) on stream q, its panel-level pairs into buffer b
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
-        launch_orig_init(ps.orig, k, n, q);
+        launch_orig_init(ps.orig, k, n, nppairs[b], q);
         panel(q, k, w, k, k + w);
         launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
     }

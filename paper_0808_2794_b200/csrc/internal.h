@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 namespace mp {
 
 constexpr int kMaxSMs = 256;
@@ -64,6 +66,44 @@ void func_cluster16_once(const void *fn);
 // Per-launch counters (how many library kernels ran), read by the report.
 extern thread_local int64_t g_launches;
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// The factorisation's panel path is a chain of short dependent kernels (leaf -> laswp -> TRSM
+// -> GEMM -> leaf ...).  Kernels on it are launched with programmatic stream serialisation:
+// the next kernel's CTAs are scheduled while the current one runs and block in pdl_wait()
+// (griddepcontrol.wait: returns once every prerequisite grid has COMPLETED and its memory
+// is visible), so the launch latency of each link is hidden.  Every kernel launched this
+// way calls pdl_wait() before its first global-memory access (read or write) and then
+// pdl_trigger() (its own dependents may be scheduled).  Both are no-ops for a kernel
+// launched without the attribute.  MP_NO_PDL=1 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();
+
+// Launch kern<<<grid, block, smem, s>>>(args...) with the PDL attribute (when enabled) and
+// up to one extra attribute (cluster dimension / cooperative), through cudaLaunchKernelEx.
+template <typename... KArgs, typename... Args>
+void launch_ex(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+               const cudaLaunchAttribute *extra, Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    unsigned na = 0;
+    if (extra) at[na++] = *extra;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    MP_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+    ++g_launches;
+}
+
 // Optional per-kernel-class timing (mp_opts.flags bit 1): CUDA events recorded
 // on the launching stream around every launch of a class, summed after the
 // call.  Classes follow DESIGN.md's kernel list.
@@ -110,7 +150,7 @@ int panel_leaf_width(int64_t m);
 template <typename T>
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
                        DevStatus *st, cudaStream_t s);
-void launch_orig_init(int32_t *orig, int64_t k, int64_t n, cudaStream_t s);
+void launch_orig_init(int32_t *orig, int64_t k, int64_t n, int32_t *npairs, cudaStream_t s);   // also zeroes *npairs
 void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 laswp (k_laswp.cu)

@@ -45,6 +45,8 @@ gemm_update_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B
     constexpr int NT = Cf::NT;
     __shared__ __align__(16) T As[2][BK][BM];
     __shared__ __align__(16) T Bs[2][BK][BN];
+    pdl_wait();
+    pdl_trigger();
     const int tid = threadIdx.x;
     const int64_t bm0 = (int64_t)blockIdx.y * BM, bn0 = (int64_t)blockIdx.x * BN;
     const T *Ag = A + bm0 * lda;                      // L21 block rows
@@ -163,11 +165,11 @@ void launch_tiles(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_
     auto al = [](const void *p, int64_t ld) { return ((uintptr_t)p % 32 == 0) && (ld % 8 == 0); };
     const bool vec = al(A, lda) && al(B, ldb) && al(C, ldc);
     if (vec)
-        gemm_update_kernel<T, BM, BN, BK, TM, TN, true><<<grid, Cf::NT, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
+        launch_ex(gemm_update_kernel<T, BM, BN, BK, TM, TN, true>, grid, dim3(Cf::NT), 0, s, nullptr, A, lda, B, ldb, C,
+                  ldc, M, N, K);
     else
-        gemm_update_kernel<T, BM, BN, BK, TM, TN, false><<<grid, Cf::NT, 0, s>>>(A, lda, B, ldb, C, ldc, M, N, K);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+        launch_ex(gemm_update_kernel<T, BM, BN, BK, TM, TN, false>, grid, dim3(Cf::NT), 0, s, nullptr, A, lda, B, ldb,
+                  C, ldc, M, N, K);
 }
 
 // ---------------------------------------------------------------- tall-skinny variant
@@ -184,6 +186,8 @@ tsgemm_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int
     constexpr int TN = NMAX / TX, TM = BM / TY;
     constexpr int APAD = BM + 4, BPAD = NMAX + 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
     T *As = reinterpret_cast<T *>(smem_raw);            // [K][APAD]  As[k][i] = L21(i, k)
     T *Bs = As + (size_t)128 * APAD;                    // [K][BPAD]  Bs[k][j] = U12(k, j)
     const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
@@ -254,9 +258,8 @@ void launch_ts(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t l
     const size_t smem = ((size_t)128 * (BM + 4) + (size_t)128 * (NMAX + 4)) * sizeof(T);
     auto kern = tsgemm_kernel<T, BM, NMAX>;
     func_smem_once((const void *)kern, smem);
-    kern<<<(unsigned)ceil_div(M, BM), 256, smem, s>>>(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(kern, dim3((unsigned)ceil_div(M, BM)), dim3(256), smem, s, nullptr, A, lda, B, ldb, C, ldc, (int)M,
+              (int)N, (int)K);
 }
 
 }  // namespace

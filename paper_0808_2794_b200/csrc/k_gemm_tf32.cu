@@ -176,6 +176,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = tmem_base_sh;
+    // PDL: barrier init and the TMEM allocation above overlap the previous kernel; no early
+    // trigger (a dependent parked on the update partition for the whole GEMM would only
+    // hold resources)
+    pdl_wait();
 
     if (warp == 0) {
         // ================= TMA producer
@@ -291,6 +295,8 @@ __device__ __forceinline__ float rna_tf32(float x)
 __global__ void split_rows_kernel(const float *__restrict__ A, int64_t lda, int M, int K,
                                   float *__restrict__ hi, float *__restrict__ lo, int kp)
 {
+    pdl_wait();
+    pdl_trigger();
     const int64_t tot = (int64_t)M * kp;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = t / kp;
@@ -306,6 +312,8 @@ __global__ void split_cols_T_kernel(const float *__restrict__ B, int64_t ldb, in
                                     float *__restrict__ hi, float *__restrict__ lo, int kp)
 {
     __shared__ float tile[32][33];
+    pdl_wait();
+    pdl_trigger();
     const int jb = blockIdx.x * 32, kb = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {               // read U12(kb + r, jb + tx): coalesced
         const int k = kb + r, j = jb + threadIdx.x;
@@ -361,12 +369,10 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
     float *Uh = Ll + (size_t)M * kp, *Ul = Uh + (size_t)N * kp;
     {
         const int64_t tot = M * kp;
-        split_rows_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 4096), 256, 0, s>>>(A, lda, (int)M, (int)K, Lh,
-                                                                                              Ll, kp);
-        MP_LAUNCH_CHECK();
+        launch_ex(split_rows_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(tot, 256), 4096)), dim3(256), 0, s,
+                  nullptr, A, lda, (int)M, (int)K, Lh, Ll, kp);
         dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(kp, 32));
-        split_cols_T_kernel<<<g, dim3(32, 8), 0, s>>>(B, ldb, (int)N, (int)K, Uh, Ul, kp);
-        MP_LAUNCH_CHECK();
+        launch_ex(split_cols_T_kernel, g, dim3(32, 8), 0, s, nullptr, B, ldb, (int)N, (int)K, Uh, Ul, kp);
     }
     CUtensorMap mUh, mUl, mLh, mLl;
     encode_kmajor(&mUh, Uh, (int)N, (int)K, kp, TM_COLS);
@@ -377,9 +383,8 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
     const int grid = std::min(ntiles, num_sms);
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
     func_smem_once((const void *)gemm_3xtf32_kernel, smem);
-    gemm_3xtf32_kernel<<<grid, GT, smem, s>>>(mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N, (int)K);
-    MP_LAUNCH_CHECK();
-    g_launches += 3;
+    launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N,
+              (int)K);
 }
 
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,

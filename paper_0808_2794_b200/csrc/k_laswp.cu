@@ -26,6 +26,8 @@ laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ p
                    int64_t x_hi, int32_t *__restrict__ perm, int nstrips)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
     const int np = *npairs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if ((int)blockIdx.x == nstrips) {          // extra CTA: compose the running permutation
@@ -40,25 +42,55 @@ laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ p
     if (s0 >= x_lo && s0 + STRIP <= x_hi) return;   // strip entirely inside the excluded panel
     const int64_t col = s0 + lane;
     const bool valid = col < c_hi && !(col >= x_lo && col < x_hi);
-    for (int i = warp; i < np; i += LT / 32) {
-        const int64_t src = pairs[2 * i + 1];
-        buf[i * STRIP + lane] = valid ? W[src * ldw + col] : T(0);
+    // U rows per warp per round: all pair indices, then all row loads, in flight together
+    constexpr int U = 8, NW = LT / 32;
+    int32_t dst[U];
+    for (int i0 = warp; i0 < np; i0 += NW * U) {
+        int32_t src[U];
+        T v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + NW * u;
+            src[u] = i < np ? pairs[2 * i + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + NW * u;
+            v[u] = (i < np && valid) ? W[(int64_t)src[u] * ldw + col] : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + NW * u;
+            if (i < np) buf[i * STRIP + lane] = v[u];
+        }
     }
     __syncthreads();
-    for (int i = warp; i < np; i += LT / 32) {
-        const int64_t dst = pairs[2 * i];
-        if (valid) W[dst * ldw + col] = buf[i * STRIP + lane];
+    for (int i0 = warp; i0 < np; i0 += NW * U) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + NW * u;
+            dst[u] = i < np ? pairs[2 * i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + NW * u;
+            if (i < np && valid) W[(int64_t)dst[u] * ldw + col] = buf[i * STRIP + lane];
+        }
     }
 }
 
 __global__ void init_perm_kernel(int32_t *perm, int64_t n)
 {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         perm[i] = (int32_t)i;
 }
 
 __global__ void invert_perm_kernel(const int32_t *perm, int32_t *pinv, int64_t n)
 {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
         pinv[perm[t]] = (int32_t)t;
 }
@@ -75,23 +107,20 @@ void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *
     const size_t smem = std::max<size_t>((size_t)max_pairs * STRIP * sizeof(T), (size_t)max_pairs * 4);
     auto kern = laswp_pairs_kernel<T>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    kern<<<grid, LT, smem, s>>>(W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm, nstrips);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(kern, dim3(grid), dim3(LT), smem, s, nullptr, W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm,
+              nstrips);
 }
 
 void launch_init_perm(int32_t *perm, int64_t n, cudaStream_t s)
 {
-    init_perm_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, s>>>(perm, n);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(init_perm_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 1024)), dim3(256), 0, s, nullptr,
+              perm, n);
 }
 
 void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStream_t s)
 {
-    invert_perm_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, s>>>(perm, pinv, n);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(invert_perm_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 1024)), dim3(256), 0, s, nullptr,
+              perm, pinv, n);
 }
 
 template void launch_laswp_pairs<float>(float *, int64_t, const int32_t *, const int32_t *, int, int64_t, int64_t,

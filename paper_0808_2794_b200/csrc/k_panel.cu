@@ -209,6 +209,8 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     static_assert(sizeof(SlotT) % 16 == 0, "slot must be 16-byte chunks");
     constexpr int CH = (int)(sizeof(SlotT) / 16);
     constexpr int EPC = 16 / (int)sizeof(T);     // elements per 16-byte chunk
+    pdl_wait();
+    pdl_trigger();
     cg::cluster_group cluster = cg::this_cluster();
     const int g = (int)cluster.block_rank();
     const int CL = (int)cluster.num_blocks();
@@ -444,14 +446,19 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     }
 }
 
-__global__ void orig_init_kernel(int32_t *orig, int64_t k, int64_t n)
+__global__ void orig_init_kernel(int32_t *orig, int64_t k, int64_t n, int32_t *npairs)
 {
+    pdl_wait();
+    pdl_trigger();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *npairs = 0;     // emit_pairs_kernel's counter
     for (int64_t i = k + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         orig[i] = (int32_t)i;
 }
 
 __global__ void emit_pairs_kernel(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs)
 {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = k + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t o = orig[i];
         if (o != (int32_t)i) {
@@ -483,19 +490,12 @@ void launch_cfg(const LeafArgs<T> &a, int cl, cudaStream_t s)
     constexpr int UG = W > MP_PANEL_UG ? MP_PANEL_UG : W;
     auto kern = cl > 1 ? panel_leaf_kernel<T, NT, RPT, W, UG, true> : panel_leaf_kernel<T, NT, RPT, W, UG, false>;
     if (cl > 8) func_cluster16_once((const void *)kern);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(cl, 1, 1);
-    cfg.blockDim = dim3(NT, 1, 1);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = cl;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    MP_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = cl;
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    launch_ex(kern, dim3(cl), dim3(NT), 0, s, &at, a);
 }
 
 int cluster_size()
@@ -570,22 +570,18 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
         default: launch_cfg<T, 512, 8, 4>(a, cl, s); break;
         }
     }
-    ++g_launches;
 }
 
-void launch_orig_init(int32_t *orig, int64_t k, int64_t n, cudaStream_t s)
+void launch_orig_init(int32_t *orig, int64_t k, int64_t n, int32_t *npairs, cudaStream_t s)
 {
-    orig_init_kernel<<<(int)std::min<int64_t>(ceil_div(n - k, 256), 512), 256, 0, s>>>(orig, k, n);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(orig_init_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n - k, 256), 512)), dim3(256), 0, s,
+              nullptr, orig, k, n, npairs);
 }
 
 void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s)
 {
-    MP_CUDA(cudaMemsetAsync(npairs, 0, sizeof(int32_t), s));
-    emit_pairs_kernel<<<(int)std::min<int64_t>(ceil_div(n - k, 256), 512), 256, 0, s>>>(orig, k, n, pairs, npairs);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(emit_pairs_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n - k, 256), 512)), dim3(256), 0, s,
+              nullptr, orig, k, n, pairs, npairs);
 }
 
 template int panel_leaf_width<float>(int64_t);

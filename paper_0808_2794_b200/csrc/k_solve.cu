@@ -154,7 +154,7 @@ __device__ __forceinline__ void spin_until(const unsigned *flag, unsigned epoch)
 }
 
 #ifdef MP_SOLVE_TRACE
-__device__ unsigned long long g_strace[4096][6];
+__device__ unsigned long long g_strace[4096][8];
 // the volatile shared load forces a deferred-blocking bar.sync to complete before the clock read
 #define STRACE(t, k) do { if (tid == 0 && (t) < 4096) { const int d_ = *(volatile int *)&s_nready; \
     g_strace[(t)][(k)] = (unsigned long long)clock64() + (unsigned long long)(d_ & 0); } } while (0)
@@ -451,6 +451,9 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             // ---- phase B
             if (warp < nsolv) {
                 mbar_wait(&full[b * (1 + DN)], ph);
+#ifdef MP_SOLVE_TRACE
+                if (tid == 0 && t < 4096) g_strace[t][6] = (unsigned long long)clock64();
+#endif
                 for (int c = warp; c < nrhs; c += NCW) {
                     double xo0 = 0.0, xo1 = 0.0;              // x of the owned rows, fetched early
                     if (!LOWER && a.accumulate) {
@@ -459,6 +462,9 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     }
                     T v0 = rsb[c * BS + lane], v1 = rsb[c * BS + lane + 32];
                     diag_solve<T, LOWER>(dg, rinvs + warp * BS, lane, nr, v0, v1);
+#ifdef MP_SOLVE_TRACE
+                    if (tid == 0 && t < 4096) g_strace[t][7] = (unsigned long long)clock64() + (unsigned long long)(__float_as_int((float)v0) & 0);
+#endif
                     // y (or z) to shared (near tiles of later blocks) and global; x (+)= z
                     ys[(size_t)slot * MAXR * BS + c * BS + lane] = v0;
                     ys[(size_t)slot * MAXR * BS + c * BS + lane + 32] = v1;

@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(MAXB * 32, 2)
 trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
     const int nb = (w + RB - 1) / RB;
     const int lane = threadIdx.x & 31, b = threadIdx.x >> 5;
     T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb][RB][CWS] published row blocks
@@ -121,9 +123,7 @@ void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t 
     const size_t smem = ((size_t)nb * RB * CWS + (size_t)nb * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
     auto kern = trsm_lower_unit_kernel<T>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    kern<<<grid, nb * 32, smem, s>>>(L, ldl, X, ldx, w, ncols);
-    MP_LAUNCH_CHECK();
-    ++g_launches;
+    launch_ex(kern, dim3(grid), dim3(nb * 32), smem, s, nullptr, L, ldl, X, ldx, w, ncols);
 }
 
 template <typename T>

@@ -34,7 +34,7 @@ int main(int argc, char **argv) {
     }
     printf("n=%d: forward+backward %.1f us (%s)\n", n, best * 1e3, cudaGetErrorString(cudaGetLastError()));
 #ifdef MP_SOLVE_TRACE
-    static unsigned long long tr[4096][6];
+    static unsigned long long tr[4096][8];
     cudaMemcpyFromSymbol(tr, g_strace, sizeof(tr));
     const int nblk = (n + 63) / 64;
     double acc[5] = {0};
@@ -44,6 +44,9 @@ int main(int argc, char **argv) {
            (double)(tr[nblk - 1][0] - tr[1][0]) / (nblk - 2));
     double sp = 0, prep_start_rel = 0; int cnt = 0;
     for (int t = 6; t < nblk; ++t) { sp += (double)(tr[t][5] - tr[t][4]); prep_start_rel += (double)((long long)tr[t][4] - (long long)tr[t - 1][1]); ++cnt; }
+    double w6 = 0, w7 = 0, w8 = 0; int c6 = 0;
+    for (int t = 6; t < nblk; ++t) { w6 += (double)(tr[t][6] - tr[t][1]); w7 += (double)(tr[t][7] - tr[t][6]); w8 += (double)(tr[t][2] - tr[t][7]); ++c6; }
+    printf("  solve phase: diag-tile wait %.0f, diag_solve %.0f, stores %.0f\n", w6 / c6, w7 / c6, w8 / c6);
     printf("  prep: fflag spin %.0f cycles/block; prep start - previous block phase-A end %.0f\n", sp / cnt, prep_start_rel / cnt);
 #endif
     cudaFree(W); cudaFree(Y); cudaFree(F); cudaFree(X); cudaFree(fl);
