@@ -85,7 +85,10 @@ typedef struct mp_opts {
                           bit 3: with bit 1, record only the trailing update and the residual classes
                                  (a handful of events per solve: cheap enough for a timed region);
                           bit 4: disable the look-ahead (panel k+1 factored on a 16-SM green context
-                                 while the trailing update of step k runs on the other SMs) */
+                                 while the trailing update of step k runs on the other SMs);
+                          bit 5: binary32 triangular solves by plain substitution inside the 64-row
+                                 diagonal blocks instead of the default inverted diagonal blocks
+                                 (reading A-19); exact inputs then stay exact (pin P2) */
 } mp_opts;
 
 #define MP_HIST_MAX 64
@@ -93,7 +96,9 @@ typedef struct mp_opts {
 typedef struct mp_report {
     int32_t iters, info;        /* same values as the *iters / *info outputs */
     int32_t nhist;              /* number of residual checks recorded in hist[] */
-    int32_t nb, variant, pad;   /* panel width / variant actually used */
+    int32_t nb, variant;        /* panel width / variant actually used */
+    int32_t solve_inv;          /* 1: binary32 solves used inverted 64x64 diagonal blocks (reading A-19),
+                                   0: substitution (flags bit 5, or a block with kappa_inf > 1e5) */
     double  anrm;               /* ||A||_F (binary64, computed once on device) */
     double  hist[MP_HIST_MAX];  /* per residual check: max_c ||r_c|| / (||x_c|| * ||A||_F * 2^-53 * sqrt(n)) */
     double  t_total_ms;         /* device time of the whole call (CUDA events) */

@@ -32,7 +32,7 @@ class Opts(ctypes.Structure):
 
 class Report(ctypes.Structure):
     _fields_ = [("iters", ctypes.c_int32), ("info", ctypes.c_int32), ("nhist", ctypes.c_int32),
-                ("nb", ctypes.c_int32), ("variant", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("nb", ctypes.c_int32), ("variant", ctypes.c_int32), ("solve_inv", ctypes.c_int32),
                 ("anrm", ctypes.c_double), ("hist", ctypes.c_double * MP_HIST_MAX),
                 ("t_total_ms", ctypes.c_double), ("t_demote_ms", ctypes.c_double),
                 ("t_factor_ms", ctypes.c_double), ("t_refine_ms", ctypes.c_double),

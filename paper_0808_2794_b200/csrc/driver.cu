@@ -661,6 +661,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     int t_fac = t_dem, t_ref = t_dem;
     int nhist = 0;
     double hist[MP_HIST_MAX] = {0};
+    bool used_inv = false;
 
     if (st0.flags & ST_OVERFLOW) code = -2;
     if (!code) {
@@ -675,8 +676,18 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         // ---- steps 2-3: x0 = LUsolve(fl32(P b))
         launch_invert_perm(perm, pinv, n, s);
         launch_permute_demote_rhs<float>(v.B, n, nrhs, pinv, Y, sio.d, s);
+        // inverted diagonal blocks for the solves (reading A-19; flags bit 5: substitution)
+        float *inv = nullptr;
+        if (!(o.flags & 32)) {
+            inv = pool.get<float>(solve_inv_floats(n));
+            prof_begin(KC_SOLVE, s);
+            launch_solve_inverses(W, ldw, n, inv, s);
+            prof_end(KC_SOLVE, 0.0, s);
+            if (!(solve_inverses_cond(inv, n, s) <= kInvCondMax)) inv = nullptr;   // ill-conditioned block
+        }
+        used_inv = inv != nullptr;
         prof_begin(KC_SOLVE, s);
-        launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 0, ss, s);
+        launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 0, ss, s, inv);
         prof_end(KC_SOLVE, 4.0 * n * n, s);
         code = -31;
         for (int it = 0; it <= itermax; ++it) {
@@ -691,7 +702,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
             if (it == itermax) break;
             // ---- steps 5-7: z = LUsolve(y) (binary32), x += z (binary64)
             prof_begin(KC_SOLVE, s);
-            launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 1, ss, s);
+            launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 1, ss, s, inv);
             prof_end(KC_SOLVE, 4.0 * n * n, s);
         }
         t_ref = tm.mark();
@@ -707,6 +718,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     MP_CUDA(cudaStreamSynchronize(s));
     if (rep) {
         rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = nb; rep->variant = o.variant;
+        rep->solve_inv = used_inv ? 1 : 0;
         rep->anrm = anrm;
         for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
         rep->t_total_ms = tm.ms(t0, t_end);
@@ -1111,6 +1123,7 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
     int t_fac = t_dem, t_ref = t_dem;
     int nhist = 0;
     double hist[MP_HIST_MAX] = {0};
+    bool used_inv = false;
     float *Wf = nullptr;
     if (!code) {
         dist_factor<float>(cm, d, Wl, ldw, ipiv, perm, sio.d, pool, s, o.variant);
@@ -1125,8 +1138,15 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
         dist_gather<float>(cm, d, Wl, ldw, Wf, ldf, pool, s);
         launch_invert_perm(perm, pinv, n, s);
         launch_permute_demote_rhs<float>(B, n, nrhs, pinv, Y, sio.d, s);
+        float *inv = nullptr;
+        if (!(o.flags & 32)) {
+            inv = pool.get<float>(solve_inv_floats(n));
+            launch_solve_inverses(Wf, ldf, n, inv, s);
+            if (!(solve_inverses_cond(inv, n, s) <= kInvCondMax)) inv = nullptr;
+        }
+        used_inv = inv != nullptr;
         prof_begin(KC_SOLVE, s);
-        launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 0, ss, s);
+        launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 0, ss, s, inv);
         prof_end(KC_SOLVE, 4.0 * n * n, s);
         code = -31;
         const int gblk = (int)std::min<int64_t>(ceil_div(d.nloc * nrhs, 256), 4096);
@@ -1151,7 +1171,7 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
             if (st.converged) { *iters = it; code = 0; break; }
             if (it == itermax) break;
             prof_begin(KC_SOLVE, s);
-            launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 1, ss, s);
+            launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 1, ss, s, inv);
             prof_end(KC_SOLVE, 4.0 * n * n, s);
         }
         t_ref = tm.mark();
@@ -1167,6 +1187,7 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
     MP_CUDA(cudaStreamSynchronize(s));
     if (rep) {
         rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = (int)d.nb; rep->variant = o.variant;
+        rep->solve_inv = used_inv ? 1 : 0;
         rep->anrm = anrm;
         for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
         rep->t_total_ms = tm.ms(t0, t_end);

@@ -200,10 +200,18 @@ struct SolveScratch {
 };
 // Forward (unit L) then backward (U) substitution on Y (n x nrhs, T, column-major
 // with ld n) with the packed LU in W; then X (double, ld n) = (mode 0) or += (mode 1) Y.
+// inv (binary32 solves only; nullptr = substitution): the inverted diagonal blocks and the
+// M blocks of launch_solve_inverses (reading A-19); the dependent chain is then one GEMV per block.
 template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
-                     SolveScratch &ss, cudaStream_t s);
+                     SolveScratch &ss, cudaStream_t s, const float *inv = nullptr);
 size_t solve_flag_words(int64_t n);
+size_t solve_inv_floats(int64_t n);      // [D_L | M_L | D_U | M_U], each ceil(n/64) 64x64 blocks
+void launch_solve_inverses(const float *W, int64_t ldw, int64_t n, float *inv, cudaStream_t s);
+// max over the diagonal blocks of kappa_inf (L and U) computed by launch_solve_inverses (synchronises s)
+double solve_inverses_cond(const float *inv, int64_t n, cudaStream_t s);
+// inverted diagonal blocks are used only when every block has kappa_inf below this (reading A-19)
+constexpr double kInvCondMax = 1e5;
 int solve_block_rows();
 
 // ---------------------------------------------------------------- K8/K10 residual (k_residual.cu)

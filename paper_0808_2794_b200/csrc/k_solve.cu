@@ -34,6 +34,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "internal.h"
 
@@ -88,7 +89,7 @@ constexpr size_t chain_smem()
 {
     using C = SCfg<T>;
     return (size_t)C::CHB * (1 + C::DN) * tile_bytes<T>() + (size_t)(C::DN + 1) * MAXR * BS * sizeof(T) +
-           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T);
+           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T) + (size_t)MAXR * BS * sizeof(T);
 }
 template <typename T>
 constexpr size_t helper_smem()
@@ -112,15 +113,32 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// the same wait for warps OFF the critical chain: polling backs off with nanosleep (callable
+// from a single lane; full-warp callers reconverge with __syncwarp() themselves)
+__device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity)
+{
+    while (!mbar_try(bar, parity)) __nanosleep(100);
+}
+// Spin-wait on an mbarrier phase.  The loop is C++ (not a branch inside inline asm), so the
+// compiler places the reconvergence point after it: lanes that leave the loop in different
+// iterations would otherwise run the following code diverged (every instruction issued
+// once per lane group, shuffles on the divergent slow path) until the next warp barrier.
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
+    while (!mbar_try(bar, parity)) { }
+    __syncwarp();
 }
 // tile (row block I, column block J) -> smem, NBOX swizzled boxes (out of range: zero-filled)
 template <typename T>
@@ -154,12 +172,16 @@ __device__ __forceinline__ void spin_until(const unsigned *flag, unsigned epoch)
 }
 
 #ifdef MP_SOLVE_TRACE
-__device__ unsigned long long g_strace[4096][8];
+__device__ unsigned long long g_strace[4096][12];
 // the volatile shared load forces a deferred-blocking bar.sync to complete before the clock read
 #define STRACE(t, k) do { if (tid == 0 && (t) < 4096) { const int d_ = *(volatile int *)&s_nready; \
     g_strace[(t)][(k)] = (unsigned long long)clock64() + (unsigned long long)(d_ & 0); } } while (0)
+// the clock read waits (branch dependency) for value v to exist
+#define STRACEV(t, k, v) do { if (tid == 0 && (t) < 4096) { s_tv = (v); const float d_ = *(volatile float *)&s_tv; \
+    if (d_ != 1.2345e-30f) g_strace[(t)][(k)] = (unsigned long long)clock64(); } } while (0)
 #else
 #define STRACE(t, k) do { } while (0)
+#define STRACEV(t, k, v) do { } while (0)
 #endif
 
 template <typename T>
@@ -244,14 +266,21 @@ __device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane,
 #ifdef MP_SOLVE_TRACE
     if (lane == 0 && t < 4096) g_strace[t][5] = (unsigned long long)clock64();
 #endif
-    for (int idx = lane; idx < a.nrhs * BS; idx += 32) {
-        const int c = idx / BS, r = idx - c * BS;
-        T v = T(0);
-        if (r < nr) {
-            v = a.Y[(int64_t)c * n + i0 + r];
-            if (far) v -= __ldcg(a.F + (int64_t)c * n + i0 + r);
+    // 4 rows per lane per round, all 8 loads in flight together
+    for (int i0b = 0; i0b < a.nrhs * BS; i0b += 128) {
+        T yv[4], fv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = i0b + lane + 32 * u, c = idx / BS, r = idx - c * BS;
+            const bool ok = idx < a.nrhs * BS && r < nr;
+            yv[u] = ok ? a.Y[(int64_t)c * n + i0 + r] : T(0);
+            fv[u] = (ok && far) ? __ldcg(a.F + (int64_t)c * n + i0 + r) : T(0);
         }
-        rsb[idx] = v;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int idx = i0b + lane + 32 * u;
+            if (idx < a.nrhs * BS) rsb[idx] = yv[u] - fv[u];
+        }
     }
 }
 
@@ -355,8 +384,10 @@ __device__ __forceinline__ void diag_solve(const T *__restrict__ dg, T *__restri
     }
 }
 
-template <typename T, bool LOWER, int R>
-__global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant__ CUtensorMap tmW, SweepArgs<T> a)
+template <typename T, bool LOWER, int R, bool INV>
+__global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant__ CUtensorMap tmW,
+                                                           const __grid_constant__ CUtensorMap tmD,
+                                                           const __grid_constant__ CUtensorMap tmM, SweepArgs<T> a)
 {
     using C = SCfg<T>;
     constexpr int DN = C::DN;
@@ -367,6 +398,9 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
     T *sm = reinterpret_cast<T *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     __shared__ __align__(8) uint64_t full[16], empty[16];
     __shared__ int s_nready;
+#ifdef MP_SOLVE_TRACE
+    __shared__ float s_tv;
+#endif
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nblk = a.nblk, nrhs = a.nrhs;
@@ -381,11 +415,13 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         T *rs = ys + (size_t)(DN + 1) * MAXR * BS;            // [2][MAXR][BS]  right-hand sides
         T *nacc = rs + 2 * (size_t)MAXR * BS;                 // [2][MAXR][BS]  near tiles d >= 2, precomputed
         T *rinvs = nacc + 2 * (size_t)MAXR * BS;              // [NCW][BS] reciprocals of the U diagonal
+        T *sbuf = rinvs + (size_t)NCW * BS;                   // [MAXR][BS] (INV) s of the next block
         if (tid == 0) {
-            for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+            // INV: a stage is released by the 4 chain warps right after their GEMV (count 4)
+            for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], INV ? 4 : 1); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int i = tid; i < (DN + 1) * MAXR * BS + 4 * MAXR * BS + NCW * BS; i += NTH) ys[i] = T(0);
+        for (int i = tid; i < (DN + 1) * MAXR * BS + 5 * MAXR * BS + NCW * BS; i += NTH) ys[i] = T(0);
         __syncthreads();
         if (warp == WPROD) {
             // ---------------- producer: diagonal + DN near tiles of every block, in order
@@ -396,11 +432,15 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     const uint32_t ph = (uint32_t)((t / C::CHB) & 1);
                     for (int k = 0; k <= DN; ++k) {
                         const int s = b * (1 + DN) + k;
-                        mbar_wait(&empty[s], ph ^ 1u);
+                        mbar_wait_idle(&empty[s], ph ^ 1u);
                         mbar_expect_tx(&full[s], TB);
                         // k = 0: diagonal tile; k = d: column block of the logically earlier
                         // block t - d (t - d < 0: out of range, zero-filled by the TMA unit)
-                        tma_tile<T>(tiles + (size_t)s * TILE, &tmW, &full[s], LOWER ? I - k : I + k, I);
+                        // (INV: k = 0 the inverse of the diagonal block, k = 1 M = Dinv T(I, J_1))
+                        const CUtensorMap *map = &tmW;
+                        int J = LOWER ? I - k : I + k;
+                        if (INV && k <= 1) { map = k == 0 ? &tmD : &tmM; J = 0; }
+                        tma_tile<T>(tiles + (size_t)s * TILE, map, &full[s], J, I);
                     }
                 }
             }
@@ -408,6 +448,160 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         }
         if (warp == WPREP) prep_rhs<T, LOWER>(a, 0, lane, rs);
         nbar_sync(1, NCH);
+        if constexpr (INV) {
+            // ---------------- inverted-diagonal-block chain (reading A-19):
+            //   y_t = w_t - M_t y_{t-1},   M_t = D_t^-1 T(t, t-1)                  (group P, warps 0-3)
+            //   w_{t+1} = D_{t+1}^-1 (rs_{t+1} - sum_{d=2..DN} T(t+1, t+1-d) y_{t+1-d}) (group L, warps 4-7)
+            // so the dependent chain per block is ONE 64 x 64 GEMV; w_{t+1} only needs y up to
+            // y_{t-1} and is formed while block t runs.
+            T *wbuf = nacc;                                   // [2][MAXR][BS]
+            const int lt = tid & 127, gr = lt >> 3, gq = lt & 7;   // rows gr + 16p, cols gq*4 + 32m
+            auto make_w = [&](int tt, bool prep_sync) {
+                const int b1 = tt % C::CHB;
+                const uint32_t ph1 = (uint32_t)((tt / C::CHB) & 1);
+                T acc[4][R];
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+                for (int d = 2; d <= DN; ++d) {
+                    const int s = b1 * (1 + DN) + d;
+                    mbar_wait_idle(&full[s], ph1);
+                    __syncwarp();
+                    tile_gemv<T, R, 4>(tiles + (size_t)s * TILE, ys + (size_t)((tt - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS,
+                                       gr, 16, gq, nrhs, acc);
+                }
+                if (prep_sync) nbar_sync(3, 160);             // rs_tt prepared by the prep warp
+                const T *r1 = rs + (size_t)(tt & 1) * MAXR * BS;
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c)
+                        if (c < nrhs) {
+                            T v = acc[p][c];
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            v += __shfl_xor_sync(0xffffffffu, v, 4);
+                            if (gq == 0) sbuf[c * BS + gr + 16 * p] = r1[c * BS + gr + 16 * p] - v;
+                            acc[p][c] = T(0);
+                        }
+                nbar_sync(4, 128);
+                const int s0 = b1 * (1 + DN);
+                mbar_wait_idle(&full[s0], ph1);
+                __syncwarp();
+                tile_gemv<T, R, 4>(tiles + (size_t)s0 * TILE, sbuf, gr, 16, gq, nrhs, acc);
+                T *wb = wbuf + (size_t)(tt & 1) * MAXR * BS;
+#pragma unroll
+                for (int p = 0; p < 4; ++p)
+#pragma unroll
+                    for (int c = 0; c < R; ++c)
+                        if (c < nrhs) {
+                            T v = acc[p][c];
+                            v += __shfl_xor_sync(0xffffffffu, v, 1);
+                            v += __shfl_xor_sync(0xffffffffu, v, 2);
+                            v += __shfl_xor_sync(0xffffffffu, v, 4);
+                            if (gq == 0) wb[c * BS + gr + 16 * p] = v;
+                        }
+            };
+            if (warp >= 4 && warp < NCW) make_w(0, false);
+            nbar_sync(1, NCH);
+            for (int t = 0; t < nblk; ++t) {
+                const int I = blk_of<LOWER>(t, nblk);
+                const int64_t i0 = (int64_t)I * BS;
+                const int nr = (int)std::min<int64_t>(BS, n - i0);
+                const int b = t % C::CHB;
+                const uint32_t ph = (uint32_t)((t / C::CHB) & 1);
+                const int slot = t % (DN + 1);
+                STRACE(t, 0);
+                if (warp < 4) {
+                    double xo[4] = {0.0, 0.0, 0.0, 0.0};      // x of the owned rows, fetched early (R = 1)
+                    if (!LOWER && R == 1 && a.accumulate && gq == 0)
+#pragma unroll
+                        for (int p = 0; p < 4; ++p)
+                            if (gr + 16 * p < nr) xo[p] = a.X[i0 + gr + 16 * p];
+                    T acc[4][R];
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+                    const int s1 = b * (1 + DN) + 1;
+                    mbar_wait(&full[s1], ph);
+#ifdef MP_SOLVE_TRACE
+                    if (tid == 0 && t < 4096) g_strace[t][1] = (unsigned long long)clock64();
+#endif
+                    tile_gemv<T, R, 4>(tiles + (size_t)s1 * TILE, ys + (size_t)((t + DN) % (DN + 1)) * MAXR * BS, gr, 16,
+                                       gq, nrhs, acc);
+                    STRACEV(t, 8, (float)acc[0][0]);
+                    // every tile of stage b is consumed (L read D_t, T(t, t-d) during block t-1)
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int k = 0; k <= DN; ++k) mbar_arrive(&empty[b * (1 + DN) + k]);
+                    // the 8-lane reductions of all rows first (independent shuffles in flight)
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int c = 0; c < R; ++c)
+                            if (c < nrhs) acc[p][c] += __shfl_xor_sync(0xffffffffu, acc[p][c], 1);
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int c = 0; c < R; ++c)
+                            if (c < nrhs) acc[p][c] += __shfl_xor_sync(0xffffffffu, acc[p][c], 2);
+#pragma unroll
+                    for (int p = 0; p < 4; ++p)
+#pragma unroll
+                        for (int c = 0; c < R; ++c)
+                            if (c < nrhs) acc[p][c] += __shfl_xor_sync(0xffffffffu, acc[p][c], 4);
+                    STRACEV(t, 9, (float)acc[3][0]);
+                    const T *wb = wbuf + (size_t)(t & 1) * MAXR * BS;
+                    T *yo = ys + (size_t)slot * MAXR * BS;
+                    if (gq == 0) {
+#pragma unroll
+                        for (int p = 0; p < 4; ++p)
+#pragma unroll
+                            for (int c = 0; c < R; ++c)
+                                if (c < nrhs) {
+                                    const int row = gr + 16 * p;
+                                    const T y = wb[c * BS + row] - acc[p][c];
+                                    yo[c * BS + row] = y;
+                                    if (row < nr) {
+                                        const int64_t gi = (int64_t)c * n + i0 + row;
+                                        a.Y[gi] = y;
+                                        if (!LOWER) {
+                                            const double xv = !a.accumulate ? 0.0 : (R == 1 ? xo[p] : a.X[gi]);
+                                            a.X[gi] = xv + (double)y;
+                                        }
+                                    }
+                                }
+                    }
+                    STRACE(t, 2);
+                    nbar_arrive(2, 160);                      // hand the stores to the publisher
+                } else if (warp < NCW) {
+                    if (t + 1 < nblk) make_w(t + 1, true);
+#ifdef MP_SOLVE_TRACE
+                    if (tid == 128 && t < 4096) g_strace[t][6] = (unsigned long long)clock64();
+#endif
+                } else if (warp == WPUB) {
+                    nbar_sync(2, 160);
+                    if (lane == 0) {
+                        __threadfence();
+                        st_release_u32(a.yflag + I, a.epoch);
+                    }
+                } else if (warp == WPREP) {
+                    if (t + 1 < nblk) {
+                        prep_rhs<T, LOWER>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * MAXR * BS);
+                        __syncwarp();
+#ifdef MP_SOLVE_TRACE
+                        if (lane == 0 && t < 4096) g_strace[t][7] = (unsigned long long)clock64();
+#endif
+                        nbar_arrive(3, 160);
+                    }
+                }
+                nbar_sync(1, NCH);                             // y_t, w_{t+1} ready
+                STRACE(t, 3);
+            }
+            return;
+        }
         const int nsolv = nrhs < NCW ? nrhs : NCW;
         // idle warps precompute the next block's near tiles d >= 2 (needs a second ring slot)
         const bool split = nsolv <= NCW / 2 && C::CHB > 1;
@@ -501,7 +695,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     for (int c = 0; c < R; ++c) acc[p][c] = T(0);
                 for (int d = 2; d <= DN; ++d) {
                     const int s = b1 * (1 + DN) + d;
-                    mbar_wait(&full[s], ph1);
+                    mbar_wait_idle(&full[s], ph1);
+                    __syncwarp();
                     tile_gemv<T, R, 4>(tiles + (size_t)s * TILE,
                                        ys + (size_t)((t + 1 - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS, lt >> 3, 16,
                                        lt & 7, nrhs, acc);
@@ -554,7 +749,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 for (int o = 0; o < nown; ++o) {
                     if (town[o] < tp + DN + 1) continue;
                     const int s = seq % HS;
-                    mbar_wait(&empty[s], (uint32_t)(((seq / HS) & 1) ^ 1));
+                    mbar_wait_idle(&empty[s], (uint32_t)(((seq / HS) & 1) ^ 1));
                     mbar_expect_tx(&full[s], TB);
                     tma_tile<T>(tiles + (size_t)s * TILE, &tmW, &full[s], J, blk_of<LOWER>(town[o], nblk));
                     ++seq;
@@ -617,9 +812,13 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                         const int c = idx / BS, r = idx - c * BS;
                         if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * MAXR + c) * BS + r];
                     }
-                    __threadfence();
+                    // the barrier orders every thread's F stores before thread 0's fence + release
+                    // (cumulativity): one fence per publish instead of one per thread
                     nbar_sync(1, NHC);
-                    if (tid == 0) st_release_u32(a.fflag + blk_of<LOWER>(town[o], nblk), a.epoch);
+                    if (tid == 0) {
+                        __threadfence();
+                        st_release_u32(a.fflag + blk_of<LOWER>(town[o], nblk), a.epoch);
+                    }
                 }
             }
         }
@@ -628,8 +827,9 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
 
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tm = nullptr;
 
+// 2D map over a row-major array of `rows` rows x `cols` columns (row stride ld elements)
 template <typename T>
-void encode_w_map(CUtensorMap *map, const T *W, int64_t ldw, int64_t n)
+void encode_map(CUtensorMap *map, const T *W, int64_t ld, int64_t cols, int64_t rows)
 {
     if (!g_encode_tm) {
         cudaDriverEntryPointQueryResult q;
@@ -638,8 +838,8 @@ void encode_w_map(CUtensorMap *map, const T *W, int64_t ldw, int64_t n)
         if (!fn || q != cudaDriverEntryPointSuccess) throw CudaError{cudaErrorNotSupported, "cuTensorMapEncodeTiled", __LINE__};
         g_encode_tm = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    cuuint64_t gdim[2] = {(cuuint64_t)ldw, (cuuint64_t)n};
-    cuuint64_t gstride[1] = {(cuuint64_t)ldw * sizeof(T)};
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)ld * sizeof(T)};
     cuuint32_t box[2] = {(cuuint32_t)Sw<T>::EPB, (cuuint32_t)BS};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode_tm(map, sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
@@ -650,12 +850,95 @@ void encode_w_map(CUtensorMap *map, const T *W, int64_t ldw, int64_t n)
 }
 
 template <typename T, bool LOWER>
-void launch_sweep(const CUtensorMap &tm, SweepArgs<T> &a, int grid, cudaStream_t s)
+void launch_sweep(const CUtensorMap &tm, const CUtensorMap &tD, const CUtensorMap &tM, bool inv, SweepArgs<T> &a,
+                  int grid, cudaStream_t s)
 {
-    auto kern = a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1> : tri_sweep_kernel<T, LOWER, MAXR>;
+    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, SweepArgs<T>) =
+        a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1, false> : tri_sweep_kernel<T, LOWER, MAXR, false>;
+    if constexpr (sizeof(T) == 4)
+        if (inv) kern = a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1, true> : tri_sweep_kernel<T, LOWER, MAXR, true>;
     func_smem_once((const void *)kern, sweep_smem<T>());
-    void *args[] = {(void *)&tm, (void *)&a};
+    void *args[] = {(void *)&tm, (void *)&tD, (void *)&tM, (void *)&a};
     MP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(NTH), args, sweep_smem<T>(), s));
+}
+
+// Inverted diagonal blocks for the INV sweeps (reading A-19), once per factorisation.
+// Block I (rows i0 .. i0+nr-1): D_I = inverse of the diagonal block of L (unit lower) or U
+// (upper), formed in binary64 from the binary32 factors by column substitution, and
+// M_I = D_I T(I, J) with J = I - 1 (L) / I + 1 (U) the block the sweep visits just before I;
+// both rounded once to binary32.  Rows / columns >= nr and a missing J give zeros, so the
+// sweep's padded rows stay zero.  A zero u_ii (only with a recorded zero pivot, which
+// sends the driver to the fallback before any solve) gives a zero row.
+template <bool LOWER>
+__global__ void __launch_bounds__(256) diag_inv_kernel(const float *__restrict__ W, int64_t ldw, int64_t n,
+                                                       float *__restrict__ Dinv, float *__restrict__ Mo,
+                                                       unsigned long long *__restrict__ cond_max)
+{
+    constexpr int LD = BS + 1;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double *Ls = reinterpret_cast<double *>(smem_raw);       // [BS][LD] diagonal block (unit / identity padded)
+    double *Xs = Ls + BS * LD;                               // [BS][LD] its inverse
+    double *Os = Xs + BS * LD;                               // [BS][LD] T(I, J)
+    const int I = blockIdx.x, nblk = gridDim.x, tid = threadIdx.x;
+    const int64_t i0 = (int64_t)I * BS;
+    const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
+    const int J = LOWER ? I - 1 : I + 1;
+    for (int idx = tid; idx < BS * BS; idx += blockDim.x) {
+        const int r = idx / BS, c = idx - r * BS;
+        double d = (r == c) ? 1.0 : 0.0;
+        if (r < nr && c < nr && (LOWER ? r > c : r <= c)) d = (double)W[(i0 + r) * ldw + i0 + c];
+        Ls[r * LD + c] = d;
+        double o = 0.0;
+        if (J >= 0 && J < nblk && r < nr) {
+            const int64_t jc = (int64_t)J * BS + c;
+            if (jc < n) o = (double)W[(i0 + r) * ldw + jc];
+        }
+        Os[r * LD + c] = o;
+    }
+    __syncthreads();
+    if (tid < BS) {                                          // column j of the inverse
+        const int j = tid;
+        if (LOWER) {
+            for (int i = 0; i < BS; ++i) {
+                double acc = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) acc = fma(-Ls[i * LD + k], Xs[k * LD + j], acc);
+                Xs[i * LD + j] = acc;
+            }
+        } else {
+            for (int i = BS - 1; i >= 0; --i) {
+                double acc = (i == j) ? 1.0 : 0.0;
+                for (int k = i + 1; k <= j; ++k) acc = fma(-Ls[i * LD + k], Xs[k * LD + j], acc);
+                const double u = Ls[i * LD + i];
+                Xs[i * LD + j] = (i > j || u == 0.0) ? 0.0 : acc / u;
+            }
+        }
+    }
+    __syncthreads();
+    // kappa_inf(T_II) = ||T_II||_inf ||T_II^-1||_inf, max over blocks (the driver keeps
+    // substitution when it is large: the inverse's rounding error grows with it)
+    __shared__ double rs_t[BS], rs_x[BS];
+    if (tid < BS) {
+        double a = 0.0, x = 0.0;
+        if (tid < nr)
+            for (int c = 0; c < nr; ++c) { a += fabs(Ls[tid * LD + c]); x += fabs(Xs[tid * LD + c]); }
+        rs_t[tid] = a;
+        rs_x[tid] = x;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a = 0.0, x = 0.0;
+        for (int r = 0; r < BS; ++r) { a = fmax(a, rs_t[r]); x = fmax(x, rs_x[r]); }
+        double kap = a * x;
+        if (!(kap <= 1e300)) kap = 1e300;                    // non-finite -> huge
+        atomicMax(cond_max, (unsigned long long)__double_as_longlong(kap));   // non-negative: bit order = value order
+    }
+    for (int idx = tid; idx < BS * BS; idx += blockDim.x) {
+        const int r = idx / BS, c = idx - r * BS;
+        double m = 0.0;
+        for (int k = 0; k < BS; ++k) m = fma(Xs[r * LD + k], Os[k * LD + c], m);
+        Dinv[(i0 + r) * BS + c] = (r < nr && c < nr) ? (float)Xs[r * LD + c] : 0.f;
+        Mo[(i0 + r) * BS + c] = r < nr ? (float)m : 0.f;
+    }
 }
 
 }  // namespace
@@ -664,13 +947,54 @@ int solve_block_rows() { return BS; }
 
 size_t solve_flag_words(int64_t n) { return 4 * (size_t)ceil_div(n, BS); }
 
+size_t solve_inv_floats(int64_t n) { return (size_t)4 * (size_t)ceil_div(n, BS) * BS * BS + 2; }
+
+void launch_solve_inverses(const float *W, int64_t ldw, int64_t n, float *inv, cudaStream_t s)
+{
+    if (n <= 0) return;
+    unsigned long long *cond = reinterpret_cast<unsigned long long *>(inv + (size_t)4 * ceil_div(n, BS) * BS * BS);
+    MP_CUDA(cudaMemsetAsync(cond, 0, sizeof(unsigned long long), s));
+    const int nblk = (int)ceil_div(n, BS);
+    const size_t blk = (size_t)nblk * BS * BS;
+    const size_t smem = (size_t)3 * BS * (BS + 1) * sizeof(double);
+    func_smem_once((const void *)diag_inv_kernel<true>, smem);
+    func_smem_once((const void *)diag_inv_kernel<false>, smem);
+    launch_ex(diag_inv_kernel<true>, dim3(nblk), dim3(256), smem, s, nullptr, W, ldw, n, inv, inv + blk, cond);
+    launch_ex(diag_inv_kernel<false>, dim3(nblk), dim3(256), smem, s, nullptr, W, ldw, n, inv + 2 * blk, inv + 3 * blk,
+              cond);
+}
+
+double solve_inverses_cond(const float *inv, int64_t n, cudaStream_t s)
+{
+    if (n <= 0) return 0.0;
+    const unsigned long long *cond =
+        reinterpret_cast<const unsigned long long *>(inv + (size_t)4 * ceil_div(n, BS) * BS * BS);
+    unsigned long long v = 0;
+    MP_CUDA(cudaMemcpyAsync(&v, cond, sizeof(v), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    double d;
+    std::memcpy(&d, &v, sizeof(d));
+    return d;
+}
+
 template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
-                     SolveScratch &ss, cudaStream_t s)
+                     SolveScratch &ss, cudaStream_t s, const float *inv)
 {
     const int nblk = (int)ceil_div(n, BS);
-    CUtensorMap tm;
-    encode_w_map<T>(&tm, W, ldw, n);
+    CUtensorMap tm, tDL, tML, tDU, tMU;
+    encode_map<T>(&tm, W, ldw, ldw, n);
+    const bool use_inv = sizeof(T) == 4 && inv != nullptr;
+    if (use_inv) {
+        const size_t blk = (size_t)nblk * BS * BS;
+        const T *b = reinterpret_cast<const T *>(inv);
+        encode_map<T>(&tDL, b, BS, BS, (int64_t)nblk * BS);
+        encode_map<T>(&tML, b + blk, BS, BS, (int64_t)nblk * BS);
+        encode_map<T>(&tDU, b + 2 * blk, BS, BS, (int64_t)nblk * BS);
+        encode_map<T>(&tMU, b + 3 * blk, BS, BS, (int64_t)nblk * BS);
+    } else {
+        tDL = tML = tDU = tMU = tm;
+    }
     int dev = 0, sms = 0;
     MP_CUDA(cudaGetDevice(&dev));
     MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -690,17 +1014,17 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
         a.yflag = ss.flags;
         a.fflag = ss.flags + nblk;
         a.epoch = ++ss.epoch;
-        launch_sweep<T, true>(tm, a, 1 + helpers, s);
+        launch_sweep<T, true>(tm, tDL, tML, use_inv, a, 1 + helpers, s);
         a.yflag = ss.flags + 2 * nblk;
         a.fflag = ss.flags + 3 * nblk;
-        launch_sweep<T, false>(tm, a, 1 + helpers, s);
+        launch_sweep<T, false>(tm, tDU, tMU, use_inv, a, 1 + helpers, s);
         g_launches += 2;
     }
 }
 
 template void launch_lu_solve<float>(const float *, int64_t, int64_t, int64_t, float *, double *, int,
-                                     SolveScratch &, cudaStream_t);
+                                     SolveScratch &, cudaStream_t, const float *);
 template void launch_lu_solve<double>(const double *, int64_t, int64_t, int64_t, double *, double *, int,
-                                      SolveScratch &, cudaStream_t);
+                                      SolveScratch &, cudaStream_t, const float *);
 
 }  // namespace mp

@@ -146,6 +146,46 @@ def test_criterion_parity_gaussian(mp, orc, n, nrhs, seed):
     assert len(h) == it + 1 and h[-1] < 1.0 and all(v >= 1.0 for v in h[:-1])
 
 
+# --------------------------------------------------------------------------- A-19 inverted diagonal blocks
+@pytest.mark.parametrize("n,nrhs,seed", [(700, 1, 31), (1500, 3, 32), (2100, 16, 33)])
+def test_solve_inv_vs_substitution(mp, orc, n, nrhs, seed):
+    """Default solves (inverted 64x64 diagonal blocks) and plain substitution (flags bit 5)
+    both reach the B:5 criterion within one iteration of the oracle."""
+    A, B, X = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+    ro = orc.dsgesv(A, B)
+    Xi, iti, infoi, repi = gpu_solve(mp, A, B)
+    Xs, its, infos, reps = gpu_solve(mp, A, B, flags=32)
+    assert repi.solve_inv == 1 and reps.solve_inv == 0
+    assert infoi == infos == ro.info == 0
+    assert abs(iti - ro.iters) <= 1 and abs(its - ro.iters) <= 1, (iti, its, ro.iters)
+    assert certificate_ok(A, Xi, B) and certificate_ok(A, Xs, B)
+
+
+def block_kappa_max(L, U, bs=64):
+    """max over the 64-row diagonal blocks of L and U of kappa_inf = ||T||_inf ||T^-1||_inf."""
+    n = L.shape[0]
+    k = 0.0
+    for i0 in range(0, n, bs):
+        for T in (L[i0:i0 + bs, i0:i0 + bs], U[i0:i0 + bs, i0:i0 + bs]):
+            Ti = np.linalg.inv(T)
+            k = max(k, np.abs(T).sum(1).max() * np.abs(Ti).sum(1).max())
+    return k
+
+
+@pytest.mark.parametrize("n,seed", [(300, 41), (513, 42)])
+def test_solve_inv_gating(mp, n, seed):
+    """The inverted blocks are used only when every diagonal block has kappa_inf <= 1e5
+    (reading A-19); the exact-LU family (random dyadic triangles) stays on substitution
+    and therefore exact."""
+    A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=seed)
+    Xg, it, info, rep = gpu_solve(mp, A, B)
+    expect = 1 if block_kappa_max(L, U) <= 1e5 else 0
+    assert rep.solve_inv == expect
+    assert info == 0 and certificate_ok(A, Xg, B)
+    if expect == 0:
+        assert it == 0 and np.array_equal(Xg, X)
+
+
 def test_factor_parity_gaussian(mp, orc):
     n = 640
     A, _, _ = inputs.gaussian(n, seed=11)
