@@ -343,6 +343,7 @@ struct Factor {
     DevStatus *st;
     int nb;
     int variant = MP_VARIANT_FFMA;
+    bool fuse_trsm = true;                 // MP_NO_FUSED_TRSM=1: separate K4 + K5 in the panel
     float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
     cudaStream_t s;
@@ -386,8 +387,14 @@ struct Factor {
         int w1 = (int)round_up(w / 2, 8);
         if (w1 > wl && w1 % wl) w1 = (int)round_up(w1, wl);
         panel(q, c0, w1, klo, khi);
-        trsm(q, c0, w1, c0 + w1, c0 + w);
-        gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, false, KC_GEMM, nullptr, 0);
+        prof_begin(KC_GEMM, q);
+        const bool fused = fuse_trsm &&
+                           launch_trsm_gemm_fused<T>(W, ldw, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, ps.ticket, q);
+        prof_end(KC_GEMM, fused ? 2.0 * (n - c0 - w1) * (w - w1) * w1 + (double)w1 * w1 * (w - w1) : 0.0, q);
+        if (!fused) {
+            trsm(q, c0, w1, c0 + w1, c0 + w);
+            gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, false, KC_GEMM, nullptr, 0);
+        }
         panel(q, c0 + w1, w - w1, klo, khi);
     }
     // panel [k, k+w) on stream q, its panel-level pairs into buffer b
@@ -485,6 +492,9 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
     f.ps.orig = pool.get<int32_t>(n);
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
+    f.ps.ticket = pool.get<int32_t>(1);
+    MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
+    if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
     for (int b = 0; b < 2; ++b) {
         f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nb);
         f.nppairs[b] = pool.get<int32_t>(1);
@@ -937,6 +947,9 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     f.ps.orig = pool.get<int32_t>(n);
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
+    f.ps.ticket = pool.get<int32_t>(1);
+    MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
+    if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
     f.ppairs[0] = pool.get<int32_t>(4 * (size_t)nb);
     f.nppairs[0] = pool.get<int32_t>(1);
     f.ps.ppairs = f.ppairs[0];

@@ -140,6 +140,7 @@ struct PanelScratch {
     int32_t *npairs;      // 1
     int32_t *ppairs;      // panel-level pairs [2*nbmax][2]
     int32_t *nppairs;     // 1
+    int32_t *ticket;      // 1, zero: fused TRSM+GEMM write-back ticket (launch_trsm_gemm_fused)
 };
 // Widest leaf one thread-block cluster can hold for m = n - c0 rows (0: too tall).
 template <typename T>
@@ -187,6 +188,12 @@ void launch_gemm_ops(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int
 // 3xTF32 tcgen05 variant (k_gemm_tf32.cu): same operation, binary32 W; scratch holds the
 // hi/lo splits of L21 and U12^T (tf32_scratch_floats(n, nb) floats).
 size_t tf32_scratch_floats(int64_t n, int nbmax);
+// K4 fused into K5 for the small in-panel levels (K in {32, 64}, N <= 64): A12 -> U12 in place
+// and C -= L21 U12; false = no fused variant for this shape (launch K4 + K5).  ticket: one
+// zero-initialised int per stream (re-armed by the kernel).
+template <typename T>
+bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
+                            int32_t *ticket, cudaStream_t s);
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                                int64_t K, float *scratch, int num_sms, cudaStream_t s);
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,

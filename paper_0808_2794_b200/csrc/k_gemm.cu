@@ -177,10 +177,16 @@ void launch_tiles(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_
 // BM-row slab; the whole K x N block B = U12 and the CTA's BM x K slab of L21 are staged
 // in shared memory once (B is shared by every CTA and L2-resident), then a register-
 // blocked FMA loop over K.  Latency-oriented: a single load phase, no k-slice pipeline.
-template <typename T, int BM, int NMAX>
+//
+// KT > 0 (K == KT): B is A12 before the TRSM and the kernel applies L11^-1 itself (K4 fused
+// into K5 for the small in-panel levels): every CTA solves the KT x N unit-lower system in
+// shared memory (one column per thread, the column in registers, substitution in the same
+// order as K4 -> identical U12 bits), uses it, and the LAST CTA to have read A12 (ticket
+// counter, so no CTA ever waits) writes U12 back over it and re-arms the counter.
+template <typename T, int BM, int NMAX, int KT>
 __global__ void __launch_bounds__(256)
-tsgemm_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int64_t ldb, T *__restrict__ C,
-              int64_t ldc, int M, int N, int K)
+tsgemm_kernel(const T *__restrict__ A, int64_t lda, T *__restrict__ B, int64_t ldb, T *__restrict__ C,
+              int64_t ldc, int M, int N, int K, const T *__restrict__ L11, int32_t *__restrict__ ticket)
 {
     constexpr int TX = 16, TY = 16;                     // threads along N, along rows
     constexpr int TN = NMAX / TX, TM = BM / TY;
@@ -221,6 +227,36 @@ tsgemm_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int
         }
     }
     __syncthreads();
+    if constexpr (KT > 0) {
+        // ---- U12 = L11^-1 A12 (unit lower, forward substitution per column)
+        T *Ls = Bs + (size_t)128 * BPAD;                    // [KT][KT] L11
+        for (int idx = tid; idx < KT * KT; idx += 256) {
+            const int i = idx / KT, k = idx - i * KT;
+            Ls[idx] = i > k ? L11[(int64_t)i * lda + k] : T(0);
+        }
+        __syncthreads();
+        if (tid < N) {
+            T x[KT];
+#pragma unroll
+            for (int i = 0; i < KT; ++i) x[i] = Bs[i * BPAD + tid];
+#pragma unroll
+            for (int k = 0; k < KT; ++k)
+#pragma unroll
+                for (int i = k + 1; i < KT; ++i) x[i] = fma(-Ls[i * KT + k], x[k], x[i]);
+#pragma unroll
+            for (int i = 0; i < KT; ++i) Bs[i * BPAD + tid] = x[i];
+        }
+        __shared__ int s_last;
+        if (tid == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;   // this CTA's A12 reads are done
+        __syncthreads();
+        if (s_last) {
+            for (int idx = tid; idx < KT * N; idx += 256) {
+                const int k = idx / N, j = idx - k * N;
+                B[(int64_t)k * ldb + j] = Bs[k * BPAD + j];
+            }
+            if (tid == 0) *ticket = 0;
+        }
+    }
     T acc[TM][TN];
 #pragma unroll
     for (int i = 0; i < TM; ++i)
@@ -251,18 +287,43 @@ tsgemm_kernel(const T *__restrict__ A, int64_t lda, const T *__restrict__ B, int
     }
 }
 
-template <typename T, int BM, int NMAX>
+template <typename T, int BM, int NMAX, int KT = 0>
 void launch_ts(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N, int64_t K,
-               cudaStream_t s)
+               cudaStream_t s, const T *L11 = nullptr, int32_t *ticket = nullptr)
 {
-    const size_t smem = ((size_t)128 * (BM + 4) + (size_t)128 * (NMAX + 4)) * sizeof(T);
-    auto kern = tsgemm_kernel<T, BM, NMAX>;
+    const size_t smem = ((size_t)128 * (BM + 4) + (size_t)128 * (NMAX + 4) + (size_t)KT * KT) * sizeof(T);
+    auto kern = tsgemm_kernel<T, BM, NMAX, KT>;
     func_smem_once((const void *)kern, smem);
-    launch_ex(kern, dim3((unsigned)ceil_div(M, BM)), dim3(256), smem, s, nullptr, A, lda, B, ldb, C, ldc, (int)M,
-              (int)N, (int)K);
+    launch_ex(kern, dim3((unsigned)ceil_div(M, BM)), dim3(256), smem, s, nullptr, A, lda, const_cast<T *>(B), ldb, C,
+              ldc, (int)M, (int)N, (int)K, L11, ticket);
 }
 
 }  // namespace
+
+// In-panel Schur update with the TRSM fused (K = w1 in {32, 64}, N <= 64): W rows [k0, k0+K)
+// of columns [c0, c0+N) hold A12 on entry and U12 on exit; rows [r0, r0+M) are updated.
+// Returns false (nothing launched) when the shape has no fused variant.
+template <typename T>
+bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
+                            int32_t *ticket, cudaStream_t s)
+{
+    if (M <= 0 || N <= 0 || N > 64 || !(K == 32 || K == 64)) return false;
+    const T *A = W + r0 * ldw + k0, *L11 = W + k0 * ldw + k0;
+    T *B = W + k0 * ldw + c0, *C = W + r0 * ldw + c0;
+    constexpr int BMF = sizeof(T) == 4 ? 64 : 32;
+    if (K == 32) {
+        if (N <= 32) launch_ts<T, BMF, 32, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+        else launch_ts<T, BMF, 64, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+    } else {
+        if (N <= 32) launch_ts<T, BMF, 32, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+        else launch_ts<T, BMF, 64, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+    }
+    return true;
+}
+template bool launch_trsm_gemm_fused<float>(float *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                            int32_t *, cudaStream_t);
+template bool launch_trsm_gemm_fused<double>(double *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                             int32_t *, cudaStream_t);
 
 template <>
 void launch_gemm_ops<float>(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc,

@@ -257,6 +257,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
 #pragma unroll
             for (int g = 0; g < PD; ++g) load_group(cb[g], i0 + GR * g);
             mbar_wait(&acc_full[a], acc_phase[a]);
+            __syncwarp();                                          // lanes leave the wait loop together
             acc_phase[a] ^= 1;
             tc_fence_after();
             const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(a * TM_ROWS + h * (TM_ROWS / 2));

@@ -349,6 +349,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                     }
                     // ---- every warp: wait for the CL candidates, identical cluster arg-max
                     mbar_wait_cluster(&mbar[par], (unsigned)((c >> 1) & 1));
+                    __syncwarp();                        // reconverge after the wait loop (asm branch)
                     TRACE(c, 3);
                     K gk = lane < CL ? K::load(slots[par][lane].rec) : K::none();
                     const K mine = gk;
