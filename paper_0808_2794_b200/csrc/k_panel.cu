@@ -38,6 +38,8 @@
 //    (store the leaf, orig[] and the leaf's row pairs), plus ipiv.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace cg = cooperative_groups;
@@ -476,7 +478,17 @@ __global__ void emit_pairs_kernel(const int32_t *orig, int64_t k, int64_t n, int
 // RPT * W * sizeof(T) / 4 <= 128.  Capacity per cluster = CLMAX * NT * RPT rows; the
 // cluster uses ceil(m / (NT * RPT)) CTAs.
 struct LeafCfg { int nt, rpt, w; };
-constexpr LeafCfg kCfgF[] = {{128, 4, 32}, {256, 4, 32}, {512, 4, 16}, {512, 8, 8}};
+#ifndef MP_LEAF_C1_NT
+#define MP_LEAF_C1_NT 256
+#define MP_LEAF_C1_RPT 4
+#endif
+#ifndef MP_LEAF_C0_NT
+#define MP_LEAF_C0_NT 256          // 256 x 2 beats 128 x 4 by ~10 % for m <= 8192 (more warps per
+#define MP_LEAF_C0_RPT 2           // SMSP hide the per-column chain; tools/bench_panel.cu)
+#endif
+#define MP_LEAF_C1 MP_LEAF_C1_NT, MP_LEAF_C1_RPT, 32
+#define MP_LEAF_C0 MP_LEAF_C0_NT, MP_LEAF_C0_RPT, 32
+constexpr LeafCfg kCfgF[] = {{MP_LEAF_C0}, {MP_LEAF_C1}, {512, 4, 16}, {512, 8, 8}};
 constexpr LeafCfg kCfgD[] = {{128, 4, 16}, {256, 4, 16}, {512, 4, 8}, {512, 8, 4}};
 constexpr int kNumCfg = 4;
 
@@ -527,7 +539,8 @@ int cluster_size()
 int select_cfg(size_t elem, int64_t m, int cl)
 {
     const LeafCfg *c = elem == 4 ? kCfgF : kCfgD;
-    for (int i = 0; i < kNumCfg; ++i)
+    static const int first = [] { const char *e = std::getenv("MP_LEAF_MIN_CFG"); return e ? std::atoi(e) : 0; }();
+    for (int i = first; i < kNumCfg; ++i)
         if ((int64_t)cl * c[i].nt * c[i].rpt >= m) return i;
     return -1;
 }
@@ -558,8 +571,8 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
     a.orig = ps.orig; a.pairs = ps.pairs; a.npairs = ps.npairs; a.st = st;
     if constexpr (sizeof(T) == 4) {
         switch (sel) {
-        case 0: launch_cfg<T, 128, 4, 32>(a, cl, s); break;
-        case 1: launch_cfg<T, 256, 4, 32>(a, cl, s); break;
+        case 0: launch_cfg<T, MP_LEAF_C0>(a, cl, s); break;
+        case 1: launch_cfg<T, MP_LEAF_C1>(a, cl, s); break;
         case 2: launch_cfg<T, 512, 4, 16>(a, cl, s); break;
         default: launch_cfg<T, 512, 8, 8>(a, cl, s); break;
         }

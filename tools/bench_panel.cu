@@ -8,11 +8,12 @@ namespace mp {
 thread_local int64_t g_launches = 0;
 void func_smem_once(const void *fn, size_t bytes) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); }
 void func_cluster16_once(const void *fn) { cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); }
+bool pdl_enabled() { return false; }
 }
 #include "../paper_0808_2794_b200/csrc/k_panel.cu"
 using namespace mp;
 int main(int argc, char **argv) {
-  for (int m : {512, 1024, 4096, 16384}) {
+  for (int m : {512, 1024, 2048, 4096, 6144, 8192, 12288, 16384}) {
     const int n = m, ldw = ((n + 63) / 64) * 64, w = 32;
     std::vector<float> h((size_t)n * ldw);
     std::mt19937 rng(1); std::normal_distribution<float> nd;
@@ -21,7 +22,7 @@ int main(int argc, char **argv) {
     cudaMalloc(&W, h.size() * 4); cudaMalloc(&ipiv, n * 4); cudaMalloc(&orig, n * 4); cudaMalloc(&pairs, 4 * 64 * 4);
     cudaMalloc(&np, 4); cudaMalloc(&st, sizeof(DevStatus)); cudaMemset(st, 0, sizeof(DevStatus));
     std::vector<int> o(n); for (int i = 0; i < n; ++i) o[i] = i; cudaMemcpy(orig, o.data(), n * 4, cudaMemcpyHostToDevice);
-    PanelScratch ps{orig, pairs, np, nullptr, nullptr};
+    PanelScratch ps{orig, pairs, np, nullptr, nullptr, nullptr};
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     float best = 1e9;
     for (int r = 0; r < 5; ++r) {
