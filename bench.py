@@ -259,6 +259,19 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
 
 
 # --------------------------------------------------------------------------- our arm
+def _gemm_traffic():
+    """dram bytes (read + write) of one trailing-update launch from the committed ncu --set full
+    capture (profiles/r01_gemm_full_v4.json), with its algorithmic bytes; None if absent."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_full_v4.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    return {"bytes": d["dram_read_bytes"] + d["dram_write_bytes"], "algorithmic_bytes": d["algorithmic_bytes"],
+            "ratio": d["traffic_over_algorithmic"], "launch": "M=N=%d K=%d (%s)" % (d["M"], d["K"], os.path.basename(p))}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -375,7 +388,7 @@ def main():
         roof = {"kernel": "trailing Schur update (K5, %s)" % args.variant,
                 "bound": "tensor" if args.variant == "3xtf32" else "alu",
                 "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                "traffic": None,
+                "traffic": _gemm_traffic(),
                 "peak_source": ("measured bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16), " + pk_src)
                 if args.variant == "3xtf32" else
                 f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",
