@@ -344,6 +344,8 @@ struct Factor {
     int nb;
     int variant = MP_VARIANT_FFMA;
     bool fuse_trsm = true;                 // MP_NO_FUSED_TRSM=1: separate K4 + K5 in the panel
+    bool tc_inpanel = true;                // MP_NO_TC_INPANEL=1: FFMA tall-skinny GEMM for every in-panel level
+    int psms = 148;                        // SMs the panel stream can count on
     float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
     cudaStream_t s;
@@ -393,7 +395,9 @@ struct Factor {
         prof_end(KC_GEMM, fused ? 2.0 * (n - c0 - w1) * (w - w1) * w1 + (double)w1 * w1 * (w - w1) : 0.0, q);
         if (!fused) {
             trsm(q, c0, w1, c0 + w1, c0 + w);
-            gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, false, KC_GEMM, nullptr, 0);
+            // the widest in-panel level (K >= 128) on the tensor cores too, on the SMs the update leaves
+            const bool tc = tc_inpanel && w1 >= 128;
+            gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, tc, KC_GEMM, tc ? tf32[1] : nullptr, psms);
         }
         panel(q, c0 + w1, w - w1, klo, khi);
     }
@@ -404,6 +408,7 @@ struct Factor {
         launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
     }
     void run_sequential() {
+        psms = sms;
         launch_init_perm(perm, n, s);
         for (int64_t k = 0; k < n; k += nb) {
             const int w = (int)std::min<int64_t>(nb, n - k);
@@ -427,6 +432,7 @@ struct Factor {
     // work touches disjoint column sets; pair lists alternate between two buffers.
     void run_lookahead(const ExecRes &ex) {
         cudaStream_t sP = ex.sP, sU = ex.sU;
+        psms = std::max(8, sms - ex.smsU);
         cudaEvent_t e0 = la_event(0), eP[2] = {la_event(1), la_event(2)}, eN = la_event(3);
         cudaEvent_t eEndP = la_event(4), eEndU = la_event(5);
         MP_CUDA(cudaEventRecord(e0, s));
@@ -495,6 +501,7 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
     f.ps.ticket = pool.get<int32_t>(1);
     MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
     if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
+    if (const char *e = std::getenv("MP_NO_TC_INPANEL")) f.tc_inpanel = e[0] != '1';
     for (int b = 0; b < 2; ++b) {
         f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nb);
         f.nppairs[b] = pool.get<int32_t>(1);
@@ -950,12 +957,14 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     f.ps.ticket = pool.get<int32_t>(1);
     MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
     if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
+    if (const char *e = std::getenv("MP_NO_TC_INPANEL")) f.tc_inpanel = e[0] != '1';
     f.ppairs[0] = pool.get<int32_t>(4 * (size_t)nb);
     f.nppairs[0] = pool.get<int32_t>(1);
     f.ps.ppairs = f.ppairs[0];
     f.ps.nppairs = f.nppairs[0];
     float *tf = nullptr;
     if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) tf = pool.get<float>(tf32_scratch_floats(n, (int)nb));
+    f.tf32[0] = f.tf32[1] = tf;                                  // one stream: panel and update share it
     // broadcast buffer: [npairs][pairs 4nb][ipiv nb] then the panel rows (n - k) x nb
     const size_t hdr = (1 + 4 * (size_t)nb + (size_t)nb) * sizeof(int32_t);
     const size_t hdr_al = round_up((int64_t)hdr, 256);
