@@ -14,6 +14,8 @@
 // Algorithmic work 2*M*N*K flops; C is read and written once (8 M N bytes).
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace mp {
@@ -310,6 +312,19 @@ bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k
     if (M <= 0 || N <= 0 || N > 64 || !(K == 32 || K == 64)) return false;
     const T *A = W + r0 * ldw + k0, *L11 = W + k0 * ldw + k0;
     T *B = W + k0 * ldw + c0, *C = W + r0 * ldw + c0;
+    static const bool big_bm = [] { const char *e = std::getenv("MP_FUSED_BM128"); return e && e[0] == '1'; }();
+    if constexpr (sizeof(T) == 4) {
+        if (big_bm) {
+            if (K == 32) {
+                if (N <= 32) launch_ts<T, 128, 32, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+                else launch_ts<T, 128, 64, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+            } else {
+                if (N <= 32) launch_ts<T, 128, 32, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+                else launch_ts<T, 128, 64, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+            }
+            return true;
+        }
+    }
     constexpr int BMF = sizeof(T) == 4 ? 64 : 32;
     if (K == 32) {
         if (N <= 32) launch_ts<T, BMF, 32, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);

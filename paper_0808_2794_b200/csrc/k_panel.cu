@@ -264,6 +264,25 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
         act[q] = valid;
     }
 
+    // push plan of the leader warp (loop invariant): lane handles chunks idx = lane + 32 j of the
+    // CL x CH (destination CTA, 16-byte chunk) grid; remote slot / mbarrier addresses per parity
+    constexpr int PJ = (CLMAX * CH + 31) / 32;
+    uint32_t pdst[2][PJ], pbar[2][PJ];
+    int pch[PJ];
+    if (MULTI && warp == 0) {
+#pragma unroll
+        for (int j = 0; j < PJ; ++j) {
+            const int idx = lane + 32 * j, r = idx / CH, ch = idx - r * CH;
+            const bool ok = idx < CL * CH;
+            pch[j] = ok ? ch : -1;
+#pragma unroll
+            for (int pp = 0; pp < 2; ++pp) {
+                pdst[pp][j] = ok ? mapa(smem_u32(&slots[pp][g]) + 16u * ch, r) : 0u;
+                pbar[pp][j] = ok ? mapa(smem_u32(&mbar[pp]), r) : 0u;
+            }
+        }
+    }
+
     // this thread's candidate for column 0
     K ck = K::none();
 #pragma unroll
@@ -339,12 +358,14 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                         const int ww = __ffs(__ballot_sync(0xffffffffu, mine == bk && lane < NWP)) - 1;
                         if (lane == 0) mbar_arm(&mbar[par], bytes_per_col);
                         const uint4 *s4 = reinterpret_cast<const uint4 *>(&wstage[par][ww]);
-                        const uint32_t dst = smem_u32(&slots[par][g]), b = smem_u32(&mbar[par]);
-                        for (int idx = lane; idx < CL * CH; idx += 32) {
-                            const int r = idx / CH, ch = idx - r * CH;
-                            const uint4 v = s4[ch];
-                            st_async16(mapa(dst + 16u * ch, r), v, mapa(b, r));
-                        }
+                        // every chunk load first, then every one-sided store (no per-chunk round trip)
+                        uint4 pv[PJ];
+#pragma unroll
+                        for (int j = 0; j < PJ; ++j)
+                            if (pch[j] >= 0) pv[j] = s4[pch[j]];
+#pragma unroll
+                        for (int j = 0; j < PJ; ++j)
+                            if (pch[j] >= 0) st_async16(pdst[par][j], pv[j], pbar[par][j]);
                         TRACE(c, 2);
                     } else {
                         named_bar_arrive(1, NT);
