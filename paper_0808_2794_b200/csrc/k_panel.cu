@@ -39,6 +39,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "internal.h"
 
@@ -201,7 +202,7 @@ struct LeafArgs {
 // the frame is rotated by UG after every group (W/UG rotations = identity at the end).
 // Slots s >= W - o*UG hold multipliers of earlier columns ("dead"); the staged pivot
 // row has them zeroed so the rank-1 update leaves them unchanged.
-template <typename T, int NT, int RPT, int W, int UG, bool MULTI>
+template <typename T, int NT, int RPT, int W, int UG, bool MULTI, bool HW = true>
 __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 {
     constexpr int NWP = NT / 32;
@@ -289,8 +290,10 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     for (int q = 0; q < RPT; ++q)
         if (act[q]) ck.take(K::make(x[q][0], cur[q]));
 
-#pragma unroll 1
-    for (int o = 0; o < W / UG; ++o) {
+    // One group of UG columns.  LM: slots >= LM are dead in every column of the group (live <= LM),
+    // so the rank-1 update stops there (the second half of the leaf runs half-width FMAs).
+    auto group = [&](const int o, auto lmax) {
+        constexpr int LM = decltype(lmax)::value;
         const int live = W - o * UG;             // slots >= live are dead (multipliers)
 #pragma unroll
         for (int u = 0; u < UG; ++u) {
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                     l = upd ? l : T(0);
                     x[q][u] = upd ? l : xv;
 #pragma unroll
-                    for (int s2 = u + 1; s2 < W; ++s2) x[q][s2] = fma(-l, win->row[s2], x[q][s2]);
+                    for (int s2 = u + 1; s2 < LM; ++s2) x[q][s2] = fma(-l, win->row[s2], x[q][s2]);
                     if (u + 1 < W) {
                         const K kq = K::make(x[q][(u + 1) % W], cur[q]);
                         ck.take(upd ? kq : K::none());
@@ -435,7 +438,13 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                 for (int s = 0; s < UG; ++s) x[q][W - UG + s] = t[s];
             }
         }
-    }
+    };
+    constexpr int NG = W / UG;
+    constexpr int HALF = NG >= 2 ? NG / 2 : NG;  // groups o < HALF have live > W / 2
+#pragma unroll 1
+    for (int o = 0; o < HALF; ++o) group(o, std::integral_constant<int, W>{});
+#pragma unroll 1
+    for (int o = HALF; o < NG; ++o) group(o, std::integral_constant<int, (HW && HALF < NG ? W / 2 : W)>{});
 
     // ---- store every row at its final position, orig[] and the leaf pairs
     cluster.sync();   // orders the npairs reset before the pair emission below
@@ -522,7 +531,9 @@ template <typename T, int NT, int RPT, int W>
 void launch_cfg(const LeafArgs<T> &a, int cl, cudaStream_t s)
 {
     constexpr int UG = W > MP_PANEL_UG ? MP_PANEL_UG : W;
-    auto kern = cl > 1 ? panel_leaf_kernel<T, NT, RPT, W, UG, true> : panel_leaf_kernel<T, NT, RPT, W, UG, false>;
+    static const bool fullw = [] { const char *e = std::getenv("MP_LEAF_FULLW"); return e && e[0] == '1'; }();
+    auto kern = cl > 1 ? (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, true, false> : panel_leaf_kernel<T, NT, RPT, W, UG, true>)
+                       : (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, false, false> : panel_leaf_kernel<T, NT, RPT, W, UG, false>);
     if (cl > 8) func_cluster16_once((const void *)kern);
     cudaLaunchAttribute at;
     at.id = cudaLaunchAttributeClusterDimension;
