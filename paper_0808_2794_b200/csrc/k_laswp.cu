@@ -17,9 +17,10 @@ namespace mp {
 namespace {
 
 constexpr int LT = 256;
-constexpr int STRIP = 32;
 
-template <typename T>
+// SW columns per CTA (32: one lane per column; 8: a warp instruction covers 4 rows x 8 columns
+// = 32-byte row segments, 4x the CTAs for narrow column ranges such as one panel's columns)
+template <typename T, int SW>
 __global__ void __launch_bounds__(LT)
 laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ pairs,
                    const int32_t *__restrict__ npairs, int64_t c_lo, int64_t c_hi, int64_t x_lo,
@@ -37,44 +38,46 @@ laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ p
         for (int i = threadIdx.x; i < np; i += LT) perm[pairs[2 * i]] = tmp[i];
         return;
     }
-    T *buf = reinterpret_cast<T *>(smem_raw);  // [np][STRIP]
-    const int64_t s0 = c_lo + (int64_t)blockIdx.x * STRIP;
-    if (s0 >= x_lo && s0 + STRIP <= x_hi) return;   // strip entirely inside the excluded panel
-    const int64_t col = s0 + lane;
+    T *buf = reinterpret_cast<T *>(smem_raw);  // [np][SW]
+    const int64_t s0 = c_lo + (int64_t)blockIdx.x * SW;
+    if (s0 >= x_lo && s0 + SW <= x_hi) return;   // strip entirely inside the excluded panel
+    constexpr int RPW = 32 / SW;                 // rows per warp instruction
+    const int cl = lane % SW, rs = lane / SW;
+    const int64_t col = s0 + cl;
     const bool valid = col < c_hi && !(col >= x_lo && col < x_hi);
-    // U rows per warp per round: all pair indices, then all row loads, in flight together
-    constexpr int U = 8, NW = LT / 32;
-    int32_t dst[U];
-    for (int i0 = warp; i0 < np; i0 += NW * U) {
+    // U row groups per warp per round: all pair indices, then all row loads, in flight together
+    constexpr int U = 8, NW = LT / 32, STEP = NW * RPW;
+    for (int i0 = warp * RPW + rs; i0 < np; i0 += STEP * U) {
         int32_t src[U];
         T v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = i0 + NW * u;
+            const int i = i0 + STEP * u;
             src[u] = i < np ? pairs[2 * i + 1] : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = i0 + NW * u;
+            const int i = i0 + STEP * u;
             v[u] = (i < np && valid) ? W[(int64_t)src[u] * ldw + col] : T(0);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = i0 + NW * u;
-            if (i < np) buf[i * STRIP + lane] = v[u];
+            const int i = i0 + STEP * u;
+            if (i < np) buf[i * SW + cl] = v[u];
         }
     }
     __syncthreads();
-    for (int i0 = warp; i0 < np; i0 += NW * U) {
+    for (int i0 = warp * RPW + rs; i0 < np; i0 += STEP * U) {
+        int32_t dst[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = i0 + NW * u;
+            const int i = i0 + STEP * u;
             dst[u] = i < np ? pairs[2 * i] : 0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int i = i0 + NW * u;
-            if (i < np && valid) W[(int64_t)dst[u] * ldw + col] = buf[i * STRIP + lane];
+            const int i = i0 + STEP * u;
+            if (i < np && valid) W[(int64_t)dst[u] * ldw + col] = buf[i * SW + cl];
         }
     }
 }
@@ -101,11 +104,14 @@ template <typename T>
 void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *npairs, int max_pairs,
                         int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm, cudaStream_t s)
 {
-    const int nstrips = c_hi > c_lo ? (int)ceil_div(c_hi - c_lo, STRIP) : 0;
+    // narrow column ranges (one panel's columns): 8-column strips, 4x the CTAs
+    const bool narrow = c_hi - c_lo <= 1024;
+    const int sw = narrow ? 8 : 32;
+    const int nstrips = c_hi > c_lo ? (int)ceil_div(c_hi - c_lo, sw) : 0;
     const int grid = nstrips + (perm ? 1 : 0);
     if (grid == 0) return;
-    const size_t smem = std::max<size_t>((size_t)max_pairs * STRIP * sizeof(T), (size_t)max_pairs * 4);
-    auto kern = laswp_pairs_kernel<T>;
+    const size_t smem = std::max<size_t>((size_t)max_pairs * sw * sizeof(T), (size_t)max_pairs * 4);
+    auto kern = narrow ? laswp_pairs_kernel<T, 8> : laswp_pairs_kernel<T, 32>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
     launch_ex(kern, dim3(grid), dim3(LT), smem, s, nullptr, W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm,
               nstrips);

@@ -42,9 +42,19 @@ __device__ __forceinline__ void load_lt(const T *W, int64_t ldw, int64_t r, int6
     }
 }
 
+template <int BYTES>
+__device__ __forceinline__ void cp_async(uint32_t dst, const void *src, bool ok)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(dst), "l"(src), "n"(BYTES), "r"(ok ? BYTES : 0)
+                 : "memory");
+}
+
 // L: top-left of the unit-lower w x w block (row-major, ldl); X: top-left of the w x ncols target.
+// The lower-triangular blocks of L are staged ONCE per CTA, transposed, with cp.async (every
+// element in flight at once, no register staging), so the warp chain below never waits on
+// global memory: Lt[tri(b, k)][kk][i] = L(32b + i, 32k + kk), tri(b, k) = b(b+1)/2 + k.
 template <typename T>
-__global__ void __launch_bounds__(MAXB * 32, 2)
+__global__ void __launch_bounds__(MAXB * 32, 1)
 trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -53,16 +63,30 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
     const int nb = (w + RB - 1) / RB;
     const int lane = threadIdx.x & 31, b = threadIdx.x >> 5;
     T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb][RB][CWS] published row blocks
-    T *Lt = Xs + (size_t)nb * RB * CWS;                       // [nb warps][RB][LP] transposed L block per warp
-    volatile int *flag = reinterpret_cast<volatile int *>(Lt + (size_t)nb * RB * LP);   // [nb]
+    T *Lt = Xs + (size_t)nb * RB * CWS;                       // [nb(nb+1)/2][RB][LP] transposed L blocks
+    const int ntri = nb * (nb + 1) / 2;
+    volatile int *flag = reinterpret_cast<volatile int *>(Lt + (size_t)ntri * RB * LP);   // [nb]
     if (threadIdx.x < MAXB) flag[threadIdx.x] = 0;
+    // ---- stage: thread -> (row i, column kk) of a block, consecutive threads along kk (coalesced)
+    for (int bb = 0; bb < nb; ++bb)
+        for (int kb = 0; kb <= bb; ++kb) {
+            const int t = bb * (bb + 1) / 2 + kb;
+            const uint32_t base = (uint32_t)__cvta_generic_to_shared(Lt + (size_t)t * RB * LP);
+            for (int e = threadIdx.x; e < RB * RB; e += blockDim.x) {
+                const int i = e >> 5, kk = e & 31;
+                const int gr = bb * RB + i, gc = kb * RB + kk;
+                const bool ok = gr < w && gc < w && (kb < bb || kk < i);
+                cp_async<(int)sizeof(T)>(base + (uint32_t)(kk * LP + i) * sizeof(T),
+                                         L + (int64_t)(ok ? gr : 0) * ldl + (ok ? gc : 0), ok);
+            }
+        }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     if (b >= nb) return;
     const int64_t col = (int64_t)blockIdx.x * CWS + lane;
     const bool cvalid = col < ncols;
     const int rows = (w - b * RB < RB) ? (w - b * RB) : RB;   // rows of this block
     const int64_t rb0 = (int64_t)b * RB;                       // block row offset inside L / X
-    T *lt = Lt + (size_t)b * RB * LP;
 
     T x[RB];
 #pragma unroll
@@ -70,8 +94,7 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
 
     // contributions of the earlier row blocks, in the order they are published
     for (int k = 0; k < b; ++k) {
-        load_lt(L, ldl, rb0, (int64_t)k * RB, rows, RB, lt, lane);      // L(b, k), independent of X_k
-        __syncwarp();
+        const T *lt = Lt + (size_t)(b * (b + 1) / 2 + k) * RB * LP;   // L(b, k)
         while (flag[k] == 0) { }
         __threadfence_block();
         __syncwarp();
@@ -90,14 +113,15 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
         }
         __syncwarp();
     }
-    // the 32 x 32 unit-lower diagonal block
-    load_lt(L, ldl, rb0, rb0, rows, rows, lt, lane);
-    __syncwarp();
+    // the 32 x 32 unit-lower diagonal block (strictly lower part staged; zeros elsewhere)
+    {
+        const T *lt = Lt + (size_t)(b * (b + 1) / 2 + b) * RB * LP;
 #pragma unroll
-    for (int i = 0; i < RB; ++i) {
-        const T *lc = lt + i * LP;
+        for (int i = 0; i < RB; ++i) {
+            const T *lc = lt + i * LP;
 #pragma unroll
-        for (int m = i + 1; m < RB; ++m) x[m] = fma(-lc[m], x[i], x[m]);
+            for (int m = i + 1; m < RB; ++m) x[m] = fma(-lc[m], x[i], x[m]);
+        }
     }
     // publish X_b (shared, for later blocks) and store U12 rows
     T *xb = Xs + (size_t)b * RB * CWS;
@@ -114,16 +138,30 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
 }  // namespace
 
 template <typename T>
+size_t trsm_smem(int w)
+{
+    const int nb = (w + RB - 1) / RB;
+    return ((size_t)nb * RB * CWS + (size_t)(nb * (nb + 1) / 2) * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
+}
+
+template <typename T>
 void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s)
 {
     if (ncols <= 0 || w <= 0) return;
     if (w > MAXB * RB) throw CudaError{cudaErrorInvalidValue, "trsm block wider than 256", __LINE__};
+    constexpr int WMAX = sizeof(T) == 4 ? 256 : 128;          // staged triangle must fit shared memory
+    if (w > WMAX) {                                            // [L11 0; L21 L22]: X1, X2 -= L21 X1, X2
+        const int w1 = WMAX;
+        launch_trsm_ops<T>(L, ldl, X, ldx, w1, ncols, s);
+        launch_gemm_ops<T>(L + (int64_t)w1 * ldl, ldl, X, ldx, X + (int64_t)w1 * ldx, ldx, w - w1, ncols, w1, s);
+        launch_trsm_ops<T>(L + (int64_t)w1 * ldl + w1, ldl, X + (int64_t)w1 * ldx, ldx, w - w1, ncols, s);
+        return;
+    }
     const int nb = (w + RB - 1) / RB;
     const int grid = (int)ceil_div(ncols, CWS);
-    const size_t smem = ((size_t)nb * RB * CWS + (size_t)nb * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
     auto kern = trsm_lower_unit_kernel<T>;
-    if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    launch_ex(kern, dim3(grid), dim3(nb * 32), smem, s, nullptr, L, ldl, X, ldx, w, ncols);
+    func_smem_once((const void *)kern, trsm_smem<T>(WMAX));   // the largest request, set once
+    launch_ex(kern, dim3(grid), dim3(nb * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols);
 }
 
 template <typename T>

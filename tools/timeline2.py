@@ -43,3 +43,14 @@ if ps:
     seg = r[starts[len(starts) // 2]:starts[len(starts) // 2 + 1]]
     t0 = seg[0][1]
     print("  mid panel:", [(n, round(1e3 * (a - t0), 1), round(1e3 * (b - a), 1)) for n, a, b, _ in seg])
+# update-stream launches between the end of a mid panel and the start of the next one
+if ps and len(streams) > 1:
+    su = [sid for sid in streams if sid != ps[0] and any(x[0] == "trail" and x[3] == sid for x in c)]
+    if su:
+        u = [x for x in c if x[3] == su[0]]
+        k = len(starts) // 2
+        seg = r[starts[k]:starts[k + 1]]
+        t_end = seg[-1][2]
+        t_next = r[starts[k + 1]][1]
+        between = [(n, round(1e3 * (a - t_end), 1), round(1e3 * (b - a), 1)) for n, a, b, _ in u if b > t_end - 0.05 and a < t_next]
+        print(f"  update stream between panel {k} end and panel {k + 1} start ({1e3 * (t_next - t_end):.1f} us):", between)
