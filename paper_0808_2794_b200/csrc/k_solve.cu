@@ -89,7 +89,8 @@ constexpr size_t chain_smem()
 {
     using C = SCfg<T>;
     return (size_t)C::CHB * (1 + C::DN) * tile_bytes<T>() + (size_t)(C::DN + 1) * MAXR * BS * sizeof(T) +
-           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T) + (size_t)MAXR * BS * sizeof(T);
+           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T) + (size_t)MAXR * BS * sizeof(T) +
+           2 * (size_t)MAXR * BS * sizeof(double);
 }
 template <typename T>
 constexpr size_t helper_smem()
@@ -416,6 +417,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         T *nacc = rs + 2 * (size_t)MAXR * BS;                 // [2][MAXR][BS]  near tiles d >= 2, precomputed
         T *rinvs = nacc + 2 * (size_t)MAXR * BS;              // [NCW][BS] reciprocals of the U diagonal
         T *sbuf = rinvs + (size_t)NCW * BS;                   // [MAXR][BS] (INV) s of the next block
+        double *xs = reinterpret_cast<double *>(sbuf + (size_t)MAXR * BS);   // [2][MAXR][BS] (INV) x of the next block
         if (tid == 0) {
             // INV: a stage is released by the 4 chain warps right after their GEMV (count 4)
             for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], INV ? 4 : 1); }
@@ -503,6 +505,28 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                             if (gq == 0) wb[c * BS + gr + 16 * p] = v;
                         }
             };
+            // backward sweep with accumulation: the prep warp also fetches x of the block it prepares,
+            // so the chain's x += z never waits on global memory
+            // (loads issued before the F wait, stored after it: their latency hides under the spin)
+            constexpr int XR = 2 * R;                          // R * BS / 32 values per lane
+            auto prep_x_load = [&](int tt, double (&v)[XR]) {
+                const int64_t j0 = (int64_t)blk_of<LOWER>(tt, nblk) * BS;
+#pragma unroll
+                for (int u = 0; u < XR; ++u) {
+                    const int idx = lane + 32 * u, c = idx / BS, r = idx - c * BS;
+                    v[u] = (!LOWER && a.accumulate && c < nrhs && j0 + r < n) ? a.X[(int64_t)c * n + j0 + r] : 0.0;
+                }
+            };
+            auto prep_x_store = [&](int tt, const double (&v)[XR]) {
+                double *xb = xs + (size_t)(tt & 1) * MAXR * BS;
+#pragma unroll
+                for (int u = 0; u < XR; ++u) xb[lane + 32 * u] = v[u];
+            };
+            if (warp == WPREP) {
+                double v[XR];
+                prep_x_load(0, v);
+                prep_x_store(0, v);
+            }
             if (warp >= 4 && warp < NCW) make_w(0, false);
             nbar_sync(1, NCH);
             for (int t = 0; t < nblk; ++t) {
@@ -514,11 +538,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 const int slot = t % (DN + 1);
                 STRACE(t, 0);
                 if (warp < 4) {
-                    double xo[4] = {0.0, 0.0, 0.0, 0.0};      // x of the owned rows, fetched early (R = 1)
-                    if (!LOWER && R == 1 && a.accumulate && gq == 0)
-#pragma unroll
-                        for (int p = 0; p < 4; ++p)
-                            if (gr + 16 * p < nr) xo[p] = a.X[i0 + gr + 16 * p];
+                    const double *xb = xs + (size_t)(t & 1) * MAXR * BS;   // x of this block (prep warp)
                     T acc[4][R];
 #pragma unroll
                     for (int p = 0; p < 4; ++p)
@@ -568,7 +588,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                                         const int64_t gi = (int64_t)c * n + i0 + row;
                                         a.Y[gi] = y;
                                         if (!LOWER) {
-                                            const double xv = !a.accumulate ? 0.0 : (R == 1 ? xo[p] : a.X[gi]);
+                                            const double xv = a.accumulate ? xb[c * BS + row] : 0.0;
                                             a.X[gi] = xv + (double)y;
                                         }
                                     }
@@ -589,7 +609,10 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     }
                 } else if (warp == WPREP) {
                     if (t + 1 < nblk) {
+                        double xv[XR];
+                        prep_x_load(t + 1, xv);
                         prep_rhs<T, LOWER>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * MAXR * BS);
+                        prep_x_store(t + 1, xv);
                         __syncwarp();
 #ifdef MP_SOLVE_TRACE
                         if (lane == 0 && t < 4096) g_strace[t][7] = (unsigned long long)clock64();

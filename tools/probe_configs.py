@@ -13,7 +13,7 @@ if "c5" in which:
         torch.cuda.synchronize()
         err = float(np.abs(Xg.cpu().numpy() - X).max() / np.abs(X).max())
         print(json.dumps({"cfg": "C5", "n": n, "kappa": kappa, "iters": it, "info": info, "ms": round(rep.t_total_ms, 2),
-                          "fallback_ms": round(rep.t_fallback_ms, 2), "fwd_err": err}), flush=True)
+                          "fallback_ms": round(rep.t_fallback_ms, 2), "fwd_err": err, "solve_inv": rep.solve_inv}), flush=True)
 if "c4" in which:
     n, nrhs = 49152, 16
     g = torch.Generator(device="cuda").manual_seed(2794)
@@ -27,7 +27,7 @@ if "c4" in which:
         torch.cuda.synchronize()
         print(json.dumps({"cfg": "C4", "n": n, "nrhs": nrhs, "iters": it, "info": info, "ms": round(rep.t_total_ms, 1),
                           "factor_ms": round(rep.t_factor_ms, 1), "refine_ms": round(rep.t_refine_ms, 1),
-                          "gflops": round(2 * n**3 / 3 / rep.t_total_ms / 1e6, 1)}), flush=True)
+                          "gflops": round(2 * n**3 / 3 / rep.t_total_ms / 1e6, 1), "solve_inv": rep.solve_inv}), flush=True)
     R = dB - dA @ Xg
     print("C4 max ||r_c|| / (||x_c|| ||A||_F eps sqrt(n)):",
           float((R.norm(dim=0) / (Xg.norm(dim=0) * dA.norm() * 2**-53 * n**0.5)).max()))
