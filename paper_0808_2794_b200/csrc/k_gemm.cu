@@ -300,6 +300,144 @@ void launch_ts(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t l
               ldc, (int)M, (int)N, (int)K, L11, ticket);
 }
 
+// Persistent, software-pipelined form of the fused in-panel update (K = KT in {32, 64},
+// N <= NMAX <= 64): the U12 solve happens ONCE per CTA, then each CTA walks its BM-row blocks
+// with the next block's L21 slab and C tile loaded (into registers) while the current one is
+// multiplied — the slab is latency-bound, so overlapping the round trips is the whole gain.
+template <typename T, int BM, int NMAX, int KT>
+__global__ void __launch_bounds__(256)
+tsgemm_fused_persist_kernel(const T *__restrict__ A, int64_t lda, T *__restrict__ B, int64_t ldb,
+                            T *__restrict__ C, int64_t ldc, int M, int N, const T *__restrict__ L11,
+                            int32_t *__restrict__ ticket)
+{
+    constexpr int TX = 16, TY = 16, TN = NMAX / TX, TM = BM / TY;
+    constexpr int APAD = BM + 4, BPAD = NMAX + 4;
+    constexpr int AV = BM * KT / 256;                     // slab elements per thread
+    static_assert(BM * KT % 256 == 0, "slab split");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
+    T *Bs = reinterpret_cast<T *>(smem_raw);              // [KT][BPAD]  U12 (after the solve)
+    T *As = Bs + (size_t)KT * BPAD;                       // [2][KT][APAD] L21 slab, transposed
+    T *Ls = As + (size_t)2 * KT * APAD;                   // [KT][KT] L11
+    const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+    const int nblk = (M + BM - 1) / BM;
+    auto load_slab = [&](int rb, T (&v)[AV]) {
+#pragma unroll
+        for (int u = 0; u < AV; ++u) {
+            const int idx = tid + 256 * u, i = idx / KT, k = idx - i * KT;
+            const int64_t row = (int64_t)rb * BM + i;
+            v[u] = (rb < nblk && row < M) ? A[row * lda + k] : T(0);
+        }
+    };
+    auto store_slab = [&](T *dst, const T (&v)[AV]) {
+#pragma unroll
+        for (int u = 0; u < AV; ++u) {
+            const int idx = tid + 256 * u, i = idx / KT, k = idx - i * KT;
+            dst[k * APAD + i] = v[u];
+        }
+    };
+    auto load_c = [&](int rb, T (&cv)[TM][TN]) {
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int64_t row = (int64_t)rb * BM + ty * TM + i;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int col = tx * TN + j;
+                cv[i][j] = (rb < nblk && row < M && col < N) ? C[row * ldc + col] : T(0);
+            }
+        }
+    };
+    int rb = blockIdx.x;
+    T av[AV], cv[TM][TN];
+    load_slab(rb, av);
+    load_c(rb, cv);
+    // ---- B = A12, L11 (every CTA), then U12 = L11^-1 A12 in place (the order of K4)
+    for (int idx = tid; idx < KT * NMAX; idx += 256) {
+        const int k = idx / NMAX, j = idx - k * NMAX;
+        Bs[k * BPAD + j] = j < N ? B[(int64_t)k * ldb + j] : T(0);
+    }
+    for (int idx = tid; idx < KT * KT; idx += 256) {
+        const int i = idx / KT, k = idx - i * KT;
+        Ls[idx] = i > k ? L11[(int64_t)i * lda + k] : T(0);
+    }
+    store_slab(As, av);
+    __syncthreads();
+    if (tid < N) {
+        T x[KT];
+#pragma unroll
+        for (int i = 0; i < KT; ++i) x[i] = Bs[i * BPAD + tid];
+#pragma unroll
+        for (int k = 0; k < KT; ++k)
+#pragma unroll
+            for (int i = k + 1; i < KT; ++i) x[i] = fma(-Ls[i * KT + k], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < KT; ++i) Bs[i * BPAD + tid] = x[i];
+    }
+    __shared__ int s_last;
+    if (tid == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;   // this CTA's A12 reads are done
+    __syncthreads();
+    if (s_last) {
+        for (int idx = tid; idx < KT * N; idx += 256) {
+            const int k = idx / N, j = idx - k * N;
+            B[(int64_t)k * ldb + j] = Bs[k * BPAD + j];
+        }
+        if (tid == 0) *ticket = 0;
+    }
+    // ---- the row blocks of this CTA, next block's loads in flight during the current multiply
+    for (int it = 0; rb < nblk; ++it, rb += gridDim.x) {
+        const int rbn = rb + gridDim.x;
+        T avn[AV], cvn[TM][TN];
+        load_slab(rbn, avn);
+        load_c(rbn, cvn);
+        const T *Ab = As + (size_t)(it & 1) * KT * APAD;
+        T acc[TM][TN];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+#pragma unroll 8
+        for (int k = 0; k < KT; ++k) {
+            T a[TM], b[TN];
+#pragma unroll
+            for (int i = 0; i < TM; ++i) a[i] = Ab[k * APAD + ty * TM + i];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) b[j] = Bs[k * BPAD + tx * TN + j];
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < TM; ++i) {
+            const int64_t row = (int64_t)rb * BM + ty * TM + i;
+            if (row >= M) continue;
+#pragma unroll
+            for (int j = 0; j < TN; ++j) {
+                const int col = tx * TN + j;
+                if (col < N) C[row * ldc + col] = cv[i][j] - acc[i][j];
+            }
+        }
+        store_slab(As + (size_t)((it + 1) & 1) * KT * APAD, avn);
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) cv[i][j] = cvn[i][j];
+        __syncthreads();
+    }
+}
+
+template <typename T, int BM, int NMAX, int KT>
+void launch_fused_persist(const T *A, int64_t lda, T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
+                          const T *L11, int32_t *ticket, int grid_max, cudaStream_t s)
+{
+    const size_t smem = ((size_t)KT * (NMAX + 4) + (size_t)2 * KT * (BM + 4) + (size_t)KT * KT) * sizeof(T);
+    auto kern = tsgemm_fused_persist_kernel<T, BM, NMAX, KT>;
+    func_smem_once((const void *)kern, smem);
+    const int grid = (int)std::min<int64_t>(ceil_div(M, BM), grid_max);
+    launch_ex(kern, dim3(grid), dim3(256), smem, s, nullptr, A, lda, B, ldb, C, ldc, (int)M, (int)N, L11, ticket);
+}
+
 }  // namespace
 
 // In-panel Schur update with the TRSM fused (K = w1 in {32, 64}, N <= 64): W rows [k0, k0+K)
@@ -312,15 +450,15 @@ bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k
     if (M <= 0 || N <= 0 || N > 64 || !(K == 32 || K == 64)) return false;
     const T *A = W + r0 * ldw + k0, *L11 = W + k0 * ldw + k0;
     T *B = W + k0 * ldw + c0, *C = W + r0 * ldw + c0;
-    static const bool big_bm = [] { const char *e = std::getenv("MP_FUSED_BM128"); return e && e[0] == '1'; }();
+    static const int persist = [] { const char *e = std::getenv("MP_FUSED_GRID"); return e ? std::atoi(e) : 96; }();
     if constexpr (sizeof(T) == 4) {
-        if (big_bm) {
+        if (persist > 0) {                                   // persistent pipelined form (default)
             if (K == 32) {
-                if (N <= 32) launch_ts<T, 128, 32, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
-                else launch_ts<T, 128, 64, 32>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+                if (N <= 32) launch_fused_persist<T, 64, 32, 32>(A, ldw, B, ldw, C, ldw, M, N, L11, ticket, persist, s);
+                else launch_fused_persist<T, 64, 64, 32>(A, ldw, B, ldw, C, ldw, M, N, L11, ticket, persist, s);
             } else {
-                if (N <= 32) launch_ts<T, 128, 32, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
-                else launch_ts<T, 128, 64, 64>(A, ldw, B, ldw, C, ldw, M, N, K, s, L11, ticket);
+                if (N <= 32) launch_fused_persist<T, 64, 32, 64>(A, ldw, B, ldw, C, ldw, M, N, L11, ticket, persist, s);
+                else launch_fused_persist<T, 64, 64, 64>(A, ldw, B, ldw, C, ldw, M, N, L11, ticket, persist, s);
             }
             return true;
         }
