@@ -5,13 +5,11 @@
 // rows of the columns to its right by forward SUBSTITUTION (no explicit
 // inverse, so exact inputs stay exact — pin P2).
 //
-// One CTA per 32-column strip; warp b owns row block b (32 rows x 32 columns
-// in registers, lane = column).  Warp b applies X_b -= L(b, k) X_k for every
-// earlier row block k as soon as warp k has published X_k in shared memory
-// (only k = b-1 is on the dependent chain), then solves its 32 x 32 unit-lower
-// diagonal block column-oriented (x_i final -> x_m -= l_mi x_i, m > i), and
-// publishes X_b.  L blocks are staged transposed in shared memory so every
-// inner step is one broadcast LDS.128 + 4 FMAs.  FMA-bound: w^2 N flops.
+// One CTA per 32-column strip (see the kernel): the strip and the triangle of L11 are staged in
+// shared memory once; per 32-row block, 8 warps subtract the previous block's contribution (older
+// ones were subtracted during the previous diagonal solve) and a ninth warp solves the 32 x 32
+// unit-lower diagonal block.  FMA work w^2 N; the chain is nb = w/32 links of (one 32x32x32
+// contribution over 8 warps + one 32-step substitution).
 #include <algorithm>
 
 #include "internal.h"
@@ -24,22 +22,11 @@ constexpr int CWS = 32;           // columns per CTA (one per lane)
 constexpr int RB = 32;            // rows per warp block
 constexpr int MAXB = 8;           // w <= MAXB * RB = 256
 constexpr int LP = RB + 4;        // padded stride of a transposed L block (16-byte aligned rows)
+constexpr int TW = 9;             // warps per CTA: 8 updaters + 1 diagonal-block solver
 
-template <typename T>
-__device__ __forceinline__ void load_lt(const T *W, int64_t ldw, int64_t r, int64_t c, int nrows, int ncols,
-                                        T *lt, int lane)
+__device__ __forceinline__ void named_bar_sync(int id, int count)
 {
-    // lt[kk * LP + i] = L(r + i, c + kk): lane kk reads column kk of rows i (coalesced row
-    // segments); all 32 loads are issued before the first store (one memory round trip)
-#pragma unroll
-    for (int h = 0; h < RB; h += 16) {
-        T v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            v[i] = (h + i < nrows && lane < ncols) ? __ldg(W + (r + h + i) * ldw + c + lane) : T(0);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) lt[lane * LP + h + i] = v[i];
-    }
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 template <int BYTES>
@@ -50,89 +37,126 @@ __device__ __forceinline__ void cp_async(uint32_t dst, const void *src, bool ok)
 }
 
 // L: top-left of the unit-lower w x w block (row-major, ldl); X: top-left of the w x ncols target.
-// The lower-triangular blocks of L are staged ONCE per CTA, transposed, with cp.async (every
-// element in flight at once, no register staging), so the warp chain below never waits on
-// global memory: Lt[tri(b, k)][kk][i] = L(32b + i, 32k + kk), tri(b, k) = b(b+1)/2 + k.
+// One CTA per 32-column strip (lane = column), 9 warps.  The strip of X and the lower-triangular
+// 32 x 32 blocks of L are staged ONCE with 16-byte cp.async (row-major, rows padded to LP:
+// Ls[tri(b, k)][i][kk] = L(32b + i, 32k + kk), tri(b, k) = b(b+1)/2 + k).  Block b of the chain:
+// warps 0-7 (4 rows each) subtract the contribution of block b-1 (the only one on the chain:
+// older blocks were subtracted while the solver worked on block b-1), then warp 8 solves the
+// 32 x 32 unit-lower diagonal block row by row (x_m -= sum_{i<m} l_mi x_i, four partial sums).
 template <typename T>
-__global__ void __launch_bounds__(MAXB * 32, 1)
+__global__ void __launch_bounds__(TW * 32, 1)
 trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     pdl_trigger();
+    constexpr int EPC = 16 / (int)sizeof(T);                  // elements per 16-byte chunk
     const int nb = (w + RB - 1) / RB;
-    const int lane = threadIdx.x & 31, b = threadIdx.x >> 5;
-    T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb][RB][CWS] published row blocks
-    T *Lt = Xs + (size_t)nb * RB * CWS;                       // [nb(nb+1)/2][RB][LP] transposed L blocks
-    const int ntri = nb * (nb + 1) / 2;
-    volatile int *flag = reinterpret_cast<volatile int *>(Lt + (size_t)ntri * RB * LP);   // [nb]
-    if (threadIdx.x < MAXB) flag[threadIdx.x] = 0;
-    // ---- stage: thread -> (row i, column kk) of a block, consecutive threads along kk (coalesced)
-    for (int bb = 0; bb < nb; ++bb)
-        for (int kb = 0; kb <= bb; ++kb) {
-            const int t = bb * (bb + 1) / 2 + kb;
-            const uint32_t base = (uint32_t)__cvta_generic_to_shared(Lt + (size_t)t * RB * LP);
-            for (int e = threadIdx.x; e < RB * RB; e += blockDim.x) {
-                const int i = e >> 5, kk = e & 31;
-                const int gr = bb * RB + i, gc = kb * RB + kk;
-                const bool ok = gr < w && gc < w && (kb < bb || kk < i);
-                cp_async<(int)sizeof(T)>(base + (uint32_t)(kk * LP + i) * sizeof(T),
-                                         L + (int64_t)(ok ? gr : 0) * ldl + (ok ? gc : 0), ok);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb * RB][CWS] the strip
+    T *Ls = Xs + (size_t)nb * RB * CWS;                       // [nb(nb+1)/2][RB][LP]
+    const int64_t c0 = (int64_t)blockIdx.x * CWS;
+    const bool vec = ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(X)) & 15) == 0 &&
+                     (ldl % EPC) == 0 && (ldx % EPC) == 0;
+    // ---- stage the strip and the triangle (16-byte chunks when aligned, else elements)
+    {
+        const uint32_t xb = (uint32_t)__cvta_generic_to_shared(Xs);
+        constexpr int CPR = CWS / EPC;                        // chunks per strip row
+        for (int e = tid; e < nb * RB * CPR; e += blockDim.x) {
+            const int r = e / CPR, cc = (e - r * CPR) * EPC;
+            if (vec && r < w && c0 + cc + EPC <= ncols) {
+                cp_async<16>(xb + (uint32_t)(r * CWS + cc) * sizeof(T), X + (int64_t)r * ldx + c0 + cc, true);
+            } else {
+#pragma unroll
+                for (int q = 0; q < EPC; ++q) {
+                    const bool ok = r < w && c0 + cc + q < ncols;
+                    cp_async<(int)sizeof(T)>(xb + (uint32_t)(r * CWS + cc + q) * sizeof(T),
+                                             X + (int64_t)(ok ? r : 0) * ldx + (ok ? c0 + cc + q : 0), ok);
+                }
             }
         }
+        const uint32_t lb = (uint32_t)__cvta_generic_to_shared(Ls);
+        constexpr int CPL = RB / EPC;                         // chunks per L block row
+        for (int bb = 0; bb < nb; ++bb)
+            for (int kb = 0; kb <= bb; ++kb) {
+                const int t = bb * (bb + 1) / 2 + kb;
+                for (int e = tid; e < RB * CPL; e += blockDim.x) {
+                    const int i = e / CPL, kk = (e - i * CPL) * EPC;
+                    const int gr = bb * RB + i, gc = kb * RB + kk;
+                    const uint32_t d = lb + (uint32_t)((t * RB + i) * LP + kk) * sizeof(T);
+                    // diagonal blocks need only their strictly lower part; stage all of a chunk
+                    // that touches it and zero the rest in the solver's reads (m > i only)
+                    if (vec && gr < w && gc + EPC <= w) {
+                        cp_async<16>(d, L + (int64_t)gr * ldl + gc, true);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < EPC; ++q) {
+                            const bool ok = gr < w && gc + q < w;
+                            cp_async<(int)sizeof(T)>(d + q * sizeof(T), L + (int64_t)(ok ? gr : 0) * ldl + (ok ? gc + q : 0),
+                                                     ok);
+                        }
+                    }
+                }
+            }
+    }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    if (b >= nb) return;
-    const int64_t col = (int64_t)blockIdx.x * CWS + lane;
-    const bool cvalid = col < ncols;
-    const int rows = (w - b * RB < RB) ? (w - b * RB) : RB;   // rows of this block
-    const int64_t rb0 = (int64_t)b * RB;                       // block row offset inside L / X
-
-    T x[RB];
+    constexpr int NU = TW - 1;                                // updater warps
+    const int r4 = 4 * warp;                                  // updater: rows r4 .. r4+3 of each block
+    T acc[4] = {T(0), T(0), T(0), T(0)};                      // updater: pending sum for the next block
+    auto contrib = [&](int bt, int k) {                       // acc += L(bt, k) X_k for this thread's rows
+        const T *lr = Ls + (size_t)(bt * (bt + 1) / 2 + k) * RB * LP + (size_t)r4 * LP;
+        const T *xk = Xs + (size_t)k * RB * CWS + lane;
+#pragma unroll 2
+        for (int kk = 0; kk < RB; kk += 4) {
+            T xv[4];
 #pragma unroll
-    for (int i = 0; i < RB; ++i) x[i] = (cvalid && i < rows) ? X[(rb0 + i) * ldx + col] : T(0);
-
-    // contributions of the earlier row blocks, in the order they are published
-    for (int k = 0; k < b; ++k) {
-        const T *lt = Lt + (size_t)(b * (b + 1) / 2 + k) * RB * LP;   // L(b, k)
-        while (flag[k] == 0) { }
-        __threadfence_block();
-        __syncwarp();
-        const T *xk = Xs + (size_t)k * RB * CWS;
-#pragma unroll 4
-        for (int kk = 0; kk < RB; ++kk) {
-            const T xv = xk[kk * CWS + lane];
-            const T *lc = lt + kk * LP;
+            for (int j = 0; j < 4; ++j) xv[j] = xk[(kk + j) * CWS];
 #pragma unroll
-            for (int i = 0; i < RB; i += 4) {
-                x[i] = fma(-lc[i], xv, x[i]);
-                x[i + 1] = fma(-lc[i + 1], xv, x[i + 1]);
-                x[i + 2] = fma(-lc[i + 2], xv, x[i + 2]);
-                x[i + 3] = fma(-lc[i + 3], xv, x[i + 3]);
+            for (int i = 0; i < 4; ++i) {
+                const T *l = lr + i * LP + kk;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i] = fma(l[j], xv[j], acc[i]);
             }
         }
-        __syncwarp();
-    }
-    // the 32 x 32 unit-lower diagonal block (strictly lower part staged; zeros elsewhere)
-    {
-        const T *lt = Lt + (size_t)(b * (b + 1) / 2 + b) * RB * LP;
+    };
+    for (int b = 0; b < nb; ++b) {
+        if (warp < NU) {
+            if (b > 0) {
+                contrib(b, b - 1);                            // the chain's contribution
+                T *xr = Xs + (size_t)(b * RB + r4) * CWS + lane;
 #pragma unroll
-        for (int i = 0; i < RB; ++i) {
-            const T *lc = lt + i * LP;
+                for (int i = 0; i < 4; ++i) { xr[i * CWS] -= acc[i]; acc[i] = T(0); }
+            }
+            named_bar_sync(1, TW * 32);                       // rows of block b ready for the solver
+            if (b + 1 < nb)
+                for (int k = 0; k < b; ++k) contrib(b + 1, k); // block b+1, everything but X_b
+            named_bar_sync(2, TW * 32);                       // X_b published
+        } else {
+            named_bar_sync(1, TW * 32);
+            const T *ld = Ls + (size_t)(b * (b + 1) / 2 + b) * RB * LP;
+            T *xb = Xs + (size_t)b * RB * CWS + lane;
+            T x[RB];
 #pragma unroll
-            for (int m = i + 1; m < RB; ++m) x[m] = fma(-lc[m], x[i], x[m]);
+            for (int i = 0; i < RB; ++i) x[i] = xb[i * CWS];
+#pragma unroll
+            for (int m = 1; m < RB; ++m) {
+                const T *lm = ld + m * LP;
+                T p[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll
+                for (int i = 0; i < m; ++i) p[i & 3] = fma(lm[i], x[i], p[i & 3]);
+                x[m] -= (p[0] + p[1]) + (p[2] + p[3]);
+            }
+#pragma unroll
+            for (int i = 0; i < RB; ++i) xb[i * CWS] = x[i];
+            named_bar_sync(2, TW * 32);
         }
     }
-    // publish X_b (shared, for later blocks) and store U12 rows
-    T *xb = Xs + (size_t)b * RB * CWS;
-#pragma unroll
-    for (int i = 0; i < RB; ++i) xb[i * CWS + lane] = x[i];
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) flag[b] = 1;
-#pragma unroll
-    for (int i = 0; i < RB; ++i)
-        if (cvalid && i < rows) X[(rb0 + i) * ldx + col] = x[i];
+    // ---- U12 back to global memory (coalesced rows)
+    for (int e = tid; e < nb * RB * CWS; e += blockDim.x) {
+        const int r = e >> 5, cc = e & 31;
+        if (r < w && c0 + cc < ncols) X[(int64_t)r * ldx + c0 + cc] = Xs[e];
+    }
 }
 
 }  // namespace
@@ -141,7 +165,7 @@ template <typename T>
 size_t trsm_smem(int w)
 {
     const int nb = (w + RB - 1) / RB;
-    return ((size_t)nb * RB * CWS + (size_t)(nb * (nb + 1) / 2) * RB * LP) * sizeof(T) + MAXB * sizeof(int) + 16;
+    return ((size_t)nb * RB * CWS + (size_t)(nb * (nb + 1) / 2) * RB * LP) * sizeof(T) + 16;
 }
 
 template <typename T>
@@ -161,7 +185,7 @@ void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t 
     const int grid = (int)ceil_div(ncols, CWS);
     auto kern = trsm_lower_unit_kernel<T>;
     func_smem_once((const void *)kern, trsm_smem<T>(WMAX));   // the largest request, set once
-    launch_ex(kern, dim3(grid), dim3(nb * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols);
+    launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols);
 }
 
 template <typename T>
