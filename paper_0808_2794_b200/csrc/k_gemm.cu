@@ -352,14 +352,22 @@ tsgemm_fused_persist_kernel(const T *__restrict__ A, int64_t lda, T *__restrict_
     T av[AV], cv[TM][TN];
     load_slab(rb, av);
     load_c(rb, cv);
-    // ---- B = A12, L11 (every CTA), then U12 = L11^-1 A12 in place (the order of K4)
-    for (int idx = tid; idx < KT * NMAX; idx += 256) {
-        const int k = idx / NMAX, j = idx - k * NMAX;
-        Bs[k * BPAD + j] = j < N ? B[(int64_t)k * ldb + j] : T(0);
-    }
-    for (int idx = tid; idx < KT * KT; idx += 256) {
-        const int i = idx / KT, k = idx - i * KT;
-        Ls[idx] = i > k ? L11[(int64_t)i * lda + k] : T(0);
+    // ---- B = A12, L11 (every CTA; cp.async: every element in flight at once), then
+    // U12 = L11^-1 A12 in place (the order of K4; only the strictly lower part of L11 is read)
+    {
+        const uint32_t bsb = (uint32_t)__cvta_generic_to_shared(Bs), lsb = (uint32_t)__cvta_generic_to_shared(Ls);
+        for (int idx = tid; idx < KT * NMAX; idx += 256) {
+            const int k = idx / NMAX, j = idx - k * NMAX;
+            const bool ok = j < N;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(bsb + (uint32_t)(k * BPAD + j) * (uint32_t)sizeof(T)),
+                         "l"(B + (int64_t)k * ldb + (ok ? j : 0)), "n"((int)sizeof(T)), "r"(ok ? (int)sizeof(T) : 0) : "memory");
+        }
+        for (int idx = tid; idx < KT * KT; idx += 256) {
+            const int i = idx / KT, k = idx - i * KT;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(lsb + (uint32_t)idx * (uint32_t)sizeof(T)),
+                         "l"(L11 + (int64_t)i * lda + k), "n"((int)sizeof(T)) : "memory");
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
     }
     store_slab(As, av);
     __syncthreads();
