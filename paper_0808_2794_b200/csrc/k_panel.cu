@@ -241,8 +241,9 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     cluster.sync();
 
     T x[RPT][W];
-    int org[RPT], cur[RPT];
-    bool act[RPT];
+    // cs[q]: the row's current logical position; bitwise-complemented (negative) once the row is
+    // no longer active (it became a pivot row, or does not exist)
+    int org[RPT], cs[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
@@ -261,8 +262,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
             for (int s = 0; s < W; ++s) x[q][s] = (valid && s < w) ? row[s] : T(0);
         }
         org[q] = valid ? a.orig[base + li] : -1;
-        cur[q] = (int)(base + li);
-        act[q] = valid;
+        cs[q] = valid ? (int)(base + li) : ~(int)(base + li);
     }
 
     // push plan of the leader warp (loop invariant): lane handles chunks idx = lane + 32 j of the
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     K ck = K::none();
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
-        if (act[q]) ck.take(K::make(x[q][0], cur[q]));
+        if (cs[q] >= 0) ck.take(K::make(x[q][0], cs[q]));
 
     // One group of UG columns.  LM: slots >= LM are dead in every column of the group (live <= LM),
     // so the rank-1 update stops there (the second half of the leaf runs half-width FMAs).
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                     int qs = -1;
 #pragma unroll
                     for (int q = RPT - 1; q >= 0; --q)
-                        if (act[q] && cur[q] == wp) qs = q;
+                        if (cs[q] == wp) qs = q;
                     if (qs >= 0) {                       // one lane per warp: a divergent, short branch
 #pragma unroll
                         for (int q = 0; q < RPT; ++q)
@@ -405,10 +405,10 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                 ck = K::none();
 #pragma unroll
                 for (int q = 0; q < RPT; ++q) {
-                    const bool is_piv = act[q] && cur[q] == p;
-                    const bool upd = act[q] && cur[q] != p;
-                    cur[q] = is_piv ? (int)kc : ((upd && cur[q] == (int)kc) ? p : cur[q]);
-                    act[q] = upd;
+                    const int cq = cs[q];
+                    const bool is_piv = cq == p;
+                    const bool upd = cq >= 0 && !is_piv;
+                    cs[q] = is_piv ? ~(int)kc : (cq == (int)kc ? p : cq);
                     const T xv = x[q][u];
                     const T xs = xv * sc;
                     T l = xs * rinv;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 #pragma unroll
                     for (int s2 = u + 1; s2 < LM; ++s2) x[q][s2] = fma(-l, win->row[s2], x[q][s2]);
                     if (u + 1 < W) {
-                        const K kq = K::make(x[q][(u + 1) % W], cur[q]);
+                        const K kq = K::make(x[q][(u + 1) % W], cs[q]);
                         ck.take(upd ? kq : K::none());
                     }
                 }
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
         if (li < nn) {
-            const long long pos = cur[q];
+            const long long pos = cs[q] >= 0 ? cs[q] : ~cs[q];
             T *row = a.W + pos * ldw + c0;
             if (w == W && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
