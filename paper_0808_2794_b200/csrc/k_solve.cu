@@ -69,6 +69,11 @@ template <> struct SCfg<double> {
 template <typename T>
 constexpr size_t tile_bytes() { return (size_t)BS * BS * sizeof(T); }
 
+// near tiles handled by the chain CTA (per right-hand-side count: the per-block buffers are
+// sized by R; DN = 5 for a single binary32 right-hand side fits but measured slower, 9.6 vs 9.4 ms)
+template <typename T, int R>
+constexpr int sweep_dn() { return SCfg<T>::DN; }
+
 // Tiles land in shared memory through TMA with SWIZZLE_128B: a 64 x 64 tile is NBOX boxes
 // of 64 rows x 128 bytes; inside a box the 16-byte chunk c of row r is stored at chunk
 // c ^ (r & 7).  Rows read by consecutive lanes then fall in different banks.
@@ -84,22 +89,26 @@ template <typename T> struct Sw {
     }
 };
 
-template <typename T>
+template <typename T, int R>
 constexpr size_t chain_smem()
 {
     using C = SCfg<T>;
-    return (size_t)C::CHB * (1 + C::DN) * tile_bytes<T>() + (size_t)(C::DN + 1) * MAXR * BS * sizeof(T) +
-           4 * (size_t)MAXR * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T) + (size_t)MAXR * BS * sizeof(T) +
-           2 * (size_t)MAXR * BS * sizeof(double);
+    constexpr int DN = sweep_dn<T, R>();
+    return (size_t)C::CHB * (1 + DN) * tile_bytes<T>() + (size_t)(DN + 1) * R * BS * sizeof(T) +
+           4 * (size_t)R * BS * sizeof(T) + (size_t)NCW * BS * sizeof(T) + (size_t)R * BS * sizeof(T) +
+           2 * (size_t)R * BS * sizeof(double);
 }
-template <typename T>
+template <typename T, int R>
 constexpr size_t helper_smem()
 {
-    return (size_t)SCfg<T>::HS * tile_bytes<T>() + (size_t)SCfg<T>::YB * MAXR * BS * sizeof(T) +
-           (size_t)SCfg<T>::MAXOWN * MAXR * BS * sizeof(T);
+    return (size_t)SCfg<T>::HS * tile_bytes<T>() + (size_t)SCfg<T>::YB * R * BS * sizeof(T) +
+           (size_t)SCfg<T>::MAXOWN * R * BS * sizeof(T);
 }
-template <typename T>
-constexpr size_t sweep_smem() { return (chain_smem<T>() > helper_smem<T>() ? chain_smem<T>() : helper_smem<T>()) + 1024; }
+template <typename T, int R>
+constexpr size_t sweep_smem()
+{
+    return (chain_smem<T, R>() > helper_smem<T, R>() ? chain_smem<T, R>() : helper_smem<T, R>()) + 1024;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
@@ -251,10 +260,9 @@ __device__ __forceinline__ void reduce_sub(T (&acc)[NP][R], int r0, int rstep, i
 }
 
 // rsb = Y - F for block t (one warp)
-template <typename T, bool LOWER>
+template <typename T, bool LOWER, int DN>
 __device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane, T *rsb)
 {
-    constexpr int DN = SCfg<T>::DN;
     const int I = blk_of<LOWER>(t, a.nblk);
     const int64_t i0 = (int64_t)I * BS, n = a.n;
     const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
@@ -391,7 +399,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                                                            const __grid_constant__ CUtensorMap tmM, SweepArgs<T> a)
 {
     using C = SCfg<T>;
-    constexpr int DN = C::DN;
+    constexpr int DN = sweep_dn<T, R>();
     constexpr int TILE = BS * BS;
     constexpr uint32_t TB = (uint32_t)tile_bytes<T>();
     extern __shared__ unsigned char smem_raw[];
@@ -412,18 +420,18 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         constexpr int NST = C::CHB * (1 + DN);
         constexpr int NCH = (NCW + 2) * 32;                   // compute + publisher + prep threads
         T *tiles = sm;                                        // [NST][TILE] (1 KB aligned)
-        T *ys = tiles + (size_t)NST * TILE;                   // [DN+1][MAXR][BS] last solved blocks
-        T *rs = ys + (size_t)(DN + 1) * MAXR * BS;            // [2][MAXR][BS]  right-hand sides
-        T *nacc = rs + 2 * (size_t)MAXR * BS;                 // [2][MAXR][BS]  near tiles d >= 2, precomputed
-        T *rinvs = nacc + 2 * (size_t)MAXR * BS;              // [NCW][BS] reciprocals of the U diagonal
-        T *sbuf = rinvs + (size_t)NCW * BS;                   // [MAXR][BS] (INV) s of the next block
-        double *xs = reinterpret_cast<double *>(sbuf + (size_t)MAXR * BS);   // [2][MAXR][BS] (INV) x of the next block
+        T *ys = tiles + (size_t)NST * TILE;                   // [DN+1][R][BS] last solved blocks
+        T *rs = ys + (size_t)(DN + 1) * R * BS;            // [2][R][BS]  right-hand sides
+        T *nacc = rs + 2 * (size_t)R * BS;                 // [2][R][BS]  near tiles d >= 2, precomputed
+        T *rinvs = nacc + 2 * (size_t)R * BS;              // [NCW][BS] reciprocals of the U diagonal
+        T *sbuf = rinvs + (size_t)NCW * BS;                   // [R][BS] (INV) s of the next block
+        double *xs = reinterpret_cast<double *>(sbuf + (size_t)R * BS);   // [2][R][BS] (INV) x of the next block
         if (tid == 0) {
             // INV: a stage is released by the 4 chain warps right after their GEMV (count 4)
             for (int s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], INV ? 4 : 1); }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
-        for (int i = tid; i < (DN + 1) * MAXR * BS + 5 * MAXR * BS + NCW * BS; i += NTH) ys[i] = T(0);
+        for (int i = tid; i < (DN + 1) * R * BS + 5 * R * BS + NCW * BS; i += NTH) ys[i] = T(0);
         __syncthreads();
         if (warp == WPROD) {
             // ---------------- producer: diagonal + DN near tiles of every block, in order
@@ -448,7 +456,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             }
             return;
         }
-        if (warp == WPREP) prep_rhs<T, LOWER>(a, 0, lane, rs);
+        if (warp == WPREP) prep_rhs<T, LOWER, DN>(a, 0, lane, rs);
         nbar_sync(1, NCH);
         if constexpr (INV) {
             // ---------------- inverted-diagonal-block chain (reading A-19):
@@ -456,7 +464,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             //   w_{t+1} = D_{t+1}^-1 (rs_{t+1} - sum_{d=2..DN} T(t+1, t+1-d) y_{t+1-d}) (group L, warps 4-7)
             // so the dependent chain per block is ONE 64 x 64 GEMV; w_{t+1} only needs y up to
             // y_{t-1} and is formed while block t runs.
-            T *wbuf = nacc;                                   // [2][MAXR][BS]
+            T *wbuf = nacc;                                   // [2][R][BS]
             const int lt = tid & 127, gr = lt >> 3, gq = lt & 7;   // rows gr + 16p, cols gq*4 + 32m
             auto make_w = [&](int tt, bool prep_sync) {
                 const int b1 = tt % C::CHB;
@@ -470,11 +478,11 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     const int s = b1 * (1 + DN) + d;
                     mbar_wait_idle(&full[s], ph1);
                     __syncwarp();
-                    tile_gemv<T, R, 4>(tiles + (size_t)s * TILE, ys + (size_t)((tt - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS,
+                    tile_gemv<T, R, 4>(tiles + (size_t)s * TILE, ys + (size_t)((tt - d + 2 * (DN + 1)) % (DN + 1)) * R * BS,
                                        gr, 16, gq, nrhs, acc);
                 }
                 if (prep_sync) nbar_sync(3, 160);             // rs_tt prepared by the prep warp
-                const T *r1 = rs + (size_t)(tt & 1) * MAXR * BS;
+                const T *r1 = rs + (size_t)(tt & 1) * R * BS;
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -492,7 +500,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 mbar_wait_idle(&full[s0], ph1);
                 __syncwarp();
                 tile_gemv<T, R, 4>(tiles + (size_t)s0 * TILE, sbuf, gr, 16, gq, nrhs, acc);
-                T *wb = wbuf + (size_t)(tt & 1) * MAXR * BS;
+                T *wb = wbuf + (size_t)(tt & 1) * R * BS;
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 }
             };
             auto prep_x_store = [&](int tt, const double (&v)[XR]) {
-                double *xb = xs + (size_t)(tt & 1) * MAXR * BS;
+                double *xb = xs + (size_t)(tt & 1) * R * BS;
 #pragma unroll
                 for (int u = 0; u < XR; ++u) xb[lane + 32 * u] = v[u];
             };
@@ -538,7 +546,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 const int slot = t % (DN + 1);
                 STRACE(t, 0);
                 if (warp < 4) {
-                    const double *xb = xs + (size_t)(t & 1) * MAXR * BS;   // x of this block (prep warp)
+                    const double *xb = xs + (size_t)(t & 1) * R * BS;   // x of this block (prep warp)
                     T acc[4][R];
 #pragma unroll
                     for (int p = 0; p < 4; ++p)
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
 #ifdef MP_SOLVE_TRACE
                     if (tid == 0 && t < 4096) g_strace[t][1] = (unsigned long long)clock64();
 #endif
-                    tile_gemv<T, R, 4>(tiles + (size_t)s1 * TILE, ys + (size_t)((t + DN) % (DN + 1)) * MAXR * BS, gr, 16,
+                    tile_gemv<T, R, 4>(tiles + (size_t)s1 * TILE, ys + (size_t)((t + DN) % (DN + 1)) * R * BS, gr, 16,
                                        gq, nrhs, acc);
                     STRACEV(t, 8, (float)acc[0][0]);
                     // every tile of stage b is consumed (L read D_t, T(t, t-d) during block t-1)
@@ -573,8 +581,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                         for (int c = 0; c < R; ++c)
                             if (c < nrhs) acc[p][c] += __shfl_xor_sync(0xffffffffu, acc[p][c], 4);
                     STRACEV(t, 9, (float)acc[3][0]);
-                    const T *wb = wbuf + (size_t)(t & 1) * MAXR * BS;
-                    T *yo = ys + (size_t)slot * MAXR * BS;
+                    const T *wb = wbuf + (size_t)(t & 1) * R * BS;
+                    T *yo = ys + (size_t)slot * R * BS;
                     if (gq == 0) {
 #pragma unroll
                         for (int p = 0; p < 4; ++p)
@@ -611,7 +619,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     if (t + 1 < nblk) {
                         double xv[XR];
                         prep_x_load(t + 1, xv);
-                        prep_rhs<T, LOWER>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * MAXR * BS);
+                        prep_rhs<T, LOWER, DN>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
                         prep_x_store(t + 1, xv);
                         __syncwarp();
 #ifdef MP_SOLVE_TRACE
@@ -636,7 +644,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             const int b = t % C::CHB;
             const uint32_t ph = (uint32_t)((t / C::CHB) & 1);
             const int slot = t % (DN + 1);
-            T *rsb = rs + (size_t)(t & 1) * MAXR * BS;
+            T *rsb = rs + (size_t)(t & 1) * R * BS;
             const T *dg = tiles + (size_t)(b * (1 + DN)) * TILE;
             STRACE(t, 0);
             // ---- phase A: near tile d = 1 (all DN when not split): rs -= T(I, J_d) y_{t-d} (+ nacc)
@@ -650,11 +658,11 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 for (int d = 1; d <= dmax; ++d) {
                     const int s = b * (1 + DN) + d;
                     mbar_wait(&full[s], ph);
-                    tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, ys + (size_t)((t - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS,
+                    tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, ys + (size_t)((t - d + 2 * (DN + 1)) % (DN + 1)) * R * BS,
                                        tr, 32, tq, nrhs, acc);
                 }
                 if (split && tq == 0) {
-                    const T *nb = nacc + (size_t)(t & 1) * MAXR * BS;
+                    const T *nb = nacc + (size_t)(t & 1) * R * BS;
 #pragma unroll
                     for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -683,8 +691,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     if (tid == 0 && t < 4096) g_strace[t][7] = (unsigned long long)clock64() + (unsigned long long)(__float_as_int((float)v0) & 0);
 #endif
                     // y (or z) to shared (near tiles of later blocks) and global; x (+)= z
-                    ys[(size_t)slot * MAXR * BS + c * BS + lane] = v0;
-                    ys[(size_t)slot * MAXR * BS + c * BS + lane + 32] = v1;
+                    ys[(size_t)slot * R * BS + c * BS + lane] = v0;
+                    ys[(size_t)slot * R * BS + c * BS + lane + 32] = v1;
                     if (lane < nr) {
                         a.Y[(int64_t)c * n + i0 + lane] = v0;
                         if (!LOWER) a.X[(int64_t)c * n + i0 + lane] = xo0 + (double)v0;
@@ -705,7 +713,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     st_release_u32(a.yflag + I, a.epoch);
                 }
             } else if (warp == WPREP) {
-                if (t + 1 < nblk) prep_rhs<T, LOWER>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * MAXR * BS);
+                if (t + 1 < nblk) prep_rhs<T, LOWER, DN>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
             } else if (split && warp >= NCW / 2 && warp < NCW && t + 1 < nblk) {
                 // next block's near tiles d = 2..DN (their y blocks are all solved)
                 const int lt = tid - (NCW / 2) * 32;          // 0..127: rows (lt>>3) + 16p, cols (lt&7)*4 + 32m
@@ -721,10 +729,10 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     mbar_wait_idle(&full[s], ph1);
                     __syncwarp();
                     tile_gemv<T, R, 4>(tiles + (size_t)s * TILE,
-                                       ys + (size_t)((t + 1 - d + 2 * (DN + 1)) % (DN + 1)) * MAXR * BS, lt >> 3, 16,
+                                       ys + (size_t)((t + 1 - d + 2 * (DN + 1)) % (DN + 1)) * R * BS, lt >> 3, 16,
                                        lt & 7, nrhs, acc);
                 }
-                T *nb = nacc + (size_t)((t + 1) & 1) * MAXR * BS;
+                T *nb = nacc + (size_t)((t + 1) & 1) * R * BS;
 #pragma unroll
                 for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -750,8 +758,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
     constexpr int HS = C::HS, YB = C::YB, MAXOWN = C::MAXOWN;
     constexpr int NHC = NCW * 32;
     T *tiles = sm;                                            // [HS][TILE]
-    T *yb = tiles + (size_t)HS * TILE;                        // [YB][MAXR][BS]
-    T *accs = yb + (size_t)YB * MAXR * BS;                    // [MAXOWN][MAXR][BS]
+    T *yb = tiles + (size_t)HS * TILE;                        // [YB][R][BS]
+    T *accs = yb + (size_t)YB * R * BS;                    // [MAXOWN][R][BS]
     int town[MAXOWN];
     int nown = 0;
     for (int t = DN + 1 + h; t < nblk && nown < MAXOWN; t += H) town[nown++] = t;
@@ -761,7 +769,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         for (int s = 0; s < HS; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    for (int i = tid; i < MAXOWN * MAXR * BS; i += NTH) accs[i] = T(0);
+    for (int i = tid; i < MAXOWN * R * BS; i += NTH) accs[i] = T(0);
     __syncthreads();
     if (warp == WPROD) {
         // ---------------- producer: tiles (I_o, J_tp) in consumption order
@@ -800,11 +808,11 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             const int k = idx / (nrhs * BS), rem = idx - k * nrhs * BS;
             const int c = rem / BS, r = rem - c * BS;
             const int64_t j = (int64_t)blk_of<LOWER>(tp + k, nblk) * BS + r;
-            yb[(size_t)k * MAXR * BS + c * BS + r] = j < n ? __ldcg(a.Y + (int64_t)c * n + j) : T(0);
+            yb[(size_t)k * R * BS + c * BS + r] = j < n ? __ldcg(a.Y + (int64_t)c * n + j) : T(0);
         }
         nbar_sync(1, NHC);
         for (int k = 0; k < nb; ++k, ++tp) {
-            const T *yv = yb + (size_t)k * MAXR * BS;
+            const T *yv = yb + (size_t)k * R * BS;
             for (int o = 0; o < nown; ++o) {
                 if (town[o] < tp + DN + 1) continue;
                 const int s = seq % HS;
@@ -824,7 +832,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                             v += __shfl_xor_sync(0xffffffffu, v, 1);
                             v += __shfl_xor_sync(0xffffffffu, v, 2);
                             v += __shfl_xor_sync(0xffffffffu, v, 4);
-                            if (tq == 0) accs[((size_t)o * MAXR + c) * BS + tr + 32 * p] += v;
+                            if (tq == 0) accs[((size_t)o * R + c) * BS + tr + 32 * p] += v;
                         }
                 nbar_sync(1, NHC);
                 if (tid == 0) mbar_arrive(&empty[s]);
@@ -833,7 +841,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     const int64_t i0 = (int64_t)blk_of<LOWER>(town[o], nblk) * BS;
                     for (int idx = tid; idx < nrhs * BS; idx += NHC) {
                         const int c = idx / BS, r = idx - c * BS;
-                        if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * MAXR + c) * BS + r];
+                        if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * R + c) * BS + r];
                     }
                     // the barrier orders every thread's F stores before thread 0's fence + release
                     // (cumulativity): one fence per publish instead of one per thread
@@ -880,9 +888,10 @@ void launch_sweep(const CUtensorMap &tm, const CUtensorMap &tD, const CUtensorMa
         a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1, false> : tri_sweep_kernel<T, LOWER, MAXR, false>;
     if constexpr (sizeof(T) == 4)
         if (inv) kern = a.nrhs == 1 ? tri_sweep_kernel<T, LOWER, 1, true> : tri_sweep_kernel<T, LOWER, MAXR, true>;
-    func_smem_once((const void *)kern, sweep_smem<T>());
+    const size_t smem = a.nrhs == 1 ? sweep_smem<T, 1>() : sweep_smem<T, MAXR>();
+    func_smem_once((const void *)kern, smem);
     void *args[] = {(void *)&tm, (void *)&tD, (void *)&tM, (void *)&a};
-    MP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(NTH), args, sweep_smem<T>(), s));
+    MP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(NTH), args, smem, s));
 }
 
 // Inverted diagonal blocks for the INV sweeps (reading A-19), once per factorisation.
@@ -1021,8 +1030,9 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     int dev = 0, sms = 0;
     MP_CUDA(cudaGetDevice(&dev));
     MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int helpers = std::max(1, std::min(sms - 1, nblk - SCfg<T>::DN - 1));
-    if (ceil_div(std::max(0, nblk - SCfg<T>::DN - 1), helpers) > SCfg<T>::MAXOWN)
+    const int dnmin = std::min(sweep_dn<T, 1>(), sweep_dn<T, MAXR>());
+    const int helpers = std::max(1, std::min(sms - 1, nblk - dnmin - 1));
+    if (ceil_div(std::max(0, nblk - dnmin - 1), helpers) > SCfg<T>::MAXOWN)
         throw CudaError{cudaErrorInvalidValue, "matrix too large for the triangular-solve helper grid", __LINE__};
     for (int64_t c0 = 0; c0 < nrhs; c0 += MAXR) {
         const int nc = (int)std::min<int64_t>(MAXR, nrhs - c0);

@@ -172,7 +172,6 @@ template <typename T>
 void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s)
 {
     if (ncols <= 0 || w <= 0) return;
-    if (w > MAXB * RB) throw CudaError{cudaErrorInvalidValue, "trsm block wider than 256", __LINE__};
     constexpr int WMAX = sizeof(T) == 4 ? 256 : 128;          // staged triangle must fit shared memory
     if (w > WMAX) {                                            // [L11 0; L21 L22]: X1, X2 -= L21 X1, X2
         const int w1 = WMAX;
