@@ -27,6 +27,10 @@
 
 #include "internal.h"
 
+#ifndef MP_TF32_TERMS
+#define MP_TF32_TERMS 3
+#endif
+
 namespace mp {
 
 namespace {
@@ -221,7 +225,12 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
                         const uint32_t off = ks * 32;                  // 8 tf32 = 32 B along the swizzled row
                         const uint64_t dAh = umma_desc_sw128(sAh + off), dAl = umma_desc_sw128(sAl + off);
                         const uint64_t dBh = umma_desc_sw128(sBh + off), dBl = umma_desc_sw128(sBl + off);
+#if MP_TF32_TERMS == 4
+                        umma_tf32(tacc, dAl, dBl, (kc | ks) ? 1u : 0u);  // lo*lo (4xTF32)
+                        umma_tf32(tacc, dAl, dBh, 1u);
+#else
                         umma_tf32(tacc, dAl, dBh, (kc | ks) ? 1u : 0u);  // small terms first
+#endif
                         umma_tf32(tacc, dAh, dBl, 1u);
                         umma_tf32(tacc, dAh, dBh, 1u);
                     }
