@@ -76,7 +76,7 @@ def gpu_solve(mp, A, B, **kw):
 
 
 # --------------------------------------------------------------------------- EXACT (P2)
-@pytest.mark.parametrize("n,nb", [(1, 0), (7, 0), (64, 0), (200, 32), (513, 64), (1000, 0), (1536, 128),
+@pytest.mark.parametrize("n,nb", [(1, 0), (7, 0), (64, 0), (200, 32), (513, 64), (1000, 0), (1536, 128), (1300, 384),
                                   (2100, 256)])
 def test_exact_lu_factors_bitwise(mp, orc, n, nb):
     A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n)
@@ -207,7 +207,7 @@ def test_factor_parity_gaussian(mp, orc):
     assert np.abs(np.tril(LU, -1)).max() <= 1.0
 
 
-@pytest.mark.parametrize("nb", [8, 32, 48, 96, 256])
+@pytest.mark.parametrize("nb", [8, 32, 48, 96, 256, 320, 512])
 def test_panel_width_invariance(mp, orc, nb):
     n = 900
     A, B, X = inputs.gaussian(n, nrhs=2, seed=21)
