@@ -369,11 +369,11 @@ struct Factor {
     // Schur update C -= L U.  big: the trailing update or the next panel's columns
     // (tensor-core variant when selected); scratch / nsm: the launching stream's.
     void gemm(cudaStream_t q, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool big,
-              int cls, float *scratch, int nsm) {
+              int cls, float *scratch, int nsm, bool reuse_a = false) {
         prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
             if (big && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
-                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q);
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a);
             else
                 launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
@@ -466,7 +466,9 @@ struct Factor {
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w - wn) * sizeof(T), sU);
             if (kn < n && kn + wn < n) {
                 trsm(sU, k, w, kn + wn, n);
-                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], ex.smsU);
+                // same L21 as the next panel's update just before: its hi/lo split is reused
+                const bool reuse = kn < n && n - kn >= 256 && wn >= 128;
+                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], ex.smsU, reuse);
             }
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
