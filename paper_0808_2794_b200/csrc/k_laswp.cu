@@ -9,6 +9,7 @@
 // contiguous 128 B segment per strip: coalesced, HBM/L2-bound, 2 x 4 B x
 // (#pairs) x (#columns) algorithmic bytes.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -105,7 +106,8 @@ void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *
                         int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm, cudaStream_t s)
 {
     // narrow column ranges (one panel's columns): 8-column strips, 4x the CTAs
-    const bool narrow = c_hi - c_lo <= 1024;
+    static const bool allnarrow = [] { const char *e = std::getenv("MP_LASWP_WIDE"); return !(e && e[0] == '1'); }();
+    const bool narrow = allnarrow || c_hi - c_lo <= 1024;
     const int sw = narrow ? 8 : 32;
     const int nstrips = c_hi > c_lo ? (int)ceil_div(c_hi - c_lo, sw) : 0;
     const int grid = nstrips + (perm ? 1 : 0);
