@@ -247,6 +247,11 @@ struct ExecRes {
     bool ok = false;
     cudaStream_t sP = nullptr, sU = nullptr;
     int smsP = 0, smsU = 0;
+    // a second, larger update partition for the early steps (the trailing update is then the
+    // critical path); sU2 == nullptr: not available
+    cudaStream_t sU2 = nullptr;
+    int smsU2 = 0;
+    double big_frac = 0.0;      // steps with n - k > big_frac * n use sU2
 };
 
 ExecRes make_exec_res(int dev)
@@ -284,6 +289,27 @@ ExecRes make_exec_res(int dev)
     if (mkCtx(&gP, dP, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
     if (mkCtx(&gU, dU, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
     if (mkStream(&sU, gU, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return r;
+    {
+        unsigned psms2 = 32;                  // SMs kept free during the early steps (MP_PANEL_SMS_EARLY)
+        if (const char *e = std::getenv("MP_PANEL_SMS_EARLY")) psms2 = (unsigned)std::max(16, std::atoi(e));
+        double frac = 0.75;                   // MP_EARLY_FRAC: trailing size above which they are "early"
+        if (const char *e = std::getenv("MP_EARLY_FRAC")) frac = std::atof(e);
+        CUdevResource grp2[1], rest2;
+        unsigned ng2 = 1;
+        CUdevResourceDesc dU2;
+        CUgreenCtx gU2;
+        CUstream sU2;
+        if (psms2 < psms && frac < 1.0 &&
+            split(grp2, &ng2, &all, &rest2, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, psms2) == CUDA_SUCCESS &&
+            ng2 == 1 && grp2[0].sm.smCount >= 16 && genDesc(&dU2, &rest2, 1) == CUDA_SUCCESS &&
+            mkCtx(&gU2, dU2, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+            mkStream(&sU2, gU2, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+            r.sU2 = (cudaStream_t)sU2;
+            r.smsU2 = (int)rest2.sm.smCount;
+            r.big_frac = frac;
+        }
+        cudaGetLastError();
+    }
     // The panel stream is an ordinary (full-device, highest-priority) stream: its kernels run on
     // the SMs the update partition leaves free (a cluster-capable 16-SM group) while the
     // trailing update runs, and on the whole GPU otherwise.
@@ -431,14 +457,14 @@ struct Factor {
     // so the factorisation of panel kn overlaps the trailing update of the rest; concurrent
     // work touches disjoint column sets; pair lists alternate between two buffers.
     void run_lookahead(const ExecRes &ex) {
-        cudaStream_t sP = ex.sP, sU = ex.sU;
+        cudaStream_t sP = ex.sP, cur = ex.sU;
         psms = std::max(8, sms - ex.smsU);
         cudaEvent_t e0 = la_event(0), eP[2] = {la_event(1), la_event(2)}, eN = la_event(3);
-        cudaEvent_t eEndP = la_event(4), eEndU = la_event(5);
+        cudaEvent_t eEndP = la_event(4), eEndU = la_event(5), eSw = la_event(6);
         MP_CUDA(cudaEventRecord(e0, s));
         MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
-        MP_CUDA(cudaStreamWaitEvent(sU, e0, 0));
-        launch_init_perm(perm, n, sU);
+        MP_CUDA(cudaStreamWaitEvent(cur, e0, 0));
+        launch_init_perm(perm, n, cur);
         factor_panel(sP, 0, (int)std::min<int64_t>(nb, n), 0);
         MP_CUDA(cudaEventRecord(eP[0], sP));
         int idx = 0;
@@ -447,6 +473,15 @@ struct Factor {
             const int64_t kn = k + w;
             const int wn = kn < n ? (int)std::min<int64_t>(nb, n - kn) : 0;
             const int b = idx & 1;
+            // early steps (large trailing matrix): the larger update partition
+            const bool early = ex.sU2 && (double)(n - kn) > ex.big_frac * (double)n;
+            cudaStream_t sU = early ? ex.sU2 : ex.sU;
+            const int smsu = early ? ex.smsU2 : ex.smsU;
+            if (sU != cur) {                                   // keep the update work in order
+                MP_CUDA(cudaEventRecord(eSw, cur));
+                MP_CUDA(cudaStreamWaitEvent(sU, eSw, 0));
+                cur = sU;
+            }
             MP_CUDA(cudaStreamWaitEvent(sU, eP[b], 0));
             if (kn < n) {
                 // the next panel's columns first (on the panel's critical path) ...
@@ -454,9 +489,10 @@ struct Factor {
                 launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
                 prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sU);
                 trsm(sU, k, w, kn, kn + wn);
-                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], ex.smsU);
+                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], smsu);
                 MP_CUDA(cudaEventRecord(eN, sU));
                 MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
+                psms = std::max(8, sms - smsu);
                 factor_panel(sP, kn, wn, b ^ 1);
                 MP_CUDA(cudaEventRecord(eP[b ^ 1], sP));
             }
@@ -468,11 +504,11 @@ struct Factor {
                 trsm(sU, k, w, kn + wn, n);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
                 const bool reuse = kn < n && n - kn >= 256 && wn >= 128;
-                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], ex.smsU, reuse);
+                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], smsu, reuse);
             }
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
-        MP_CUDA(cudaEventRecord(eEndU, sU));
+        MP_CUDA(cudaEventRecord(eEndU, cur));
         MP_CUDA(cudaStreamWaitEvent(s, eEndP, 0));
         MP_CUDA(cudaStreamWaitEvent(s, eEndU, 0));
     }

@@ -54,3 +54,10 @@ if ps and len(streams) > 1:
         t_next = r[starts[k + 1]][1]
         between = [(n, round(1e3 * (a - t_end), 1), round(1e3 * (b - a), 1)) for n, a, b, _ in u if b > t_end - 0.05 and a < t_next]
         print(f"  update stream between panel {k} end and panel {k + 1} start ({1e3 * (t_next - t_end):.1f} us):", between)
+if ps:
+    ws = []
+    for k in range(len(starts) - 1):
+        seg = r[starts[k]:starts[k + 1]]
+        ws.append((round(1e3 * (seg[-1][2] - seg[0][1])), round(1e3 * (r[starts[k + 1]][1] - seg[-1][2]))))
+    print("  (span, wait) per panel, first 12:", ws[:12])
+    print("  (span, wait) per panel, last 12:", ws[-12:])
