@@ -252,6 +252,10 @@ struct ExecRes {
     cudaStream_t sU2 = nullptr;
     int smsU2 = 0;
     double big_frac = 0.0;      // steps with n - k > big_frac * n use sU2
+    // and a smaller one for the late steps (the panel is then the critical path)
+    cudaStream_t sU3 = nullptr;
+    int smsU3 = 0;
+    double small_frac = 0.0;    // steps with n - k < small_frac * n use sU3
 };
 
 ExecRes make_exec_res(int dev)
@@ -307,6 +311,27 @@ ExecRes make_exec_res(int dev)
             r.sU2 = (cudaStream_t)sU2;
             r.smsU2 = (int)rest2.sm.smCount;
             r.big_frac = frac;
+        }
+        cudaGetLastError();
+    }
+    {
+        unsigned psms3 = 48;                  // SMs kept free during the late steps (MP_PANEL_SMS_LATE)
+        if (const char *e = std::getenv("MP_PANEL_SMS_LATE")) psms3 = (unsigned)std::max(16, std::atoi(e));
+        double frac = 0.0;                    // MP_LATE_FRAC: trailing size below which they are "late"
+        if (const char *e = std::getenv("MP_LATE_FRAC")) frac = std::atof(e);
+        CUdevResource grp3[1], rest3;
+        unsigned ng3 = 1;
+        CUdevResourceDesc dU3;
+        CUgreenCtx gU3;
+        CUstream sU3;
+        if (psms3 > psms && frac > 0.0 &&
+            split(grp3, &ng3, &all, &rest3, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, psms3) == CUDA_SUCCESS &&
+            ng3 == 1 && rest3.sm.smCount >= 32 && genDesc(&dU3, &rest3, 1) == CUDA_SUCCESS &&
+            mkCtx(&gU3, dU3, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+            mkStream(&sU3, gU3, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+            r.sU3 = (cudaStream_t)sU3;
+            r.smsU3 = (int)rest3.sm.smCount;
+            r.small_frac = frac;
         }
         cudaGetLastError();
     }
@@ -475,8 +500,9 @@ struct Factor {
             const int b = idx & 1;
             // early steps (large trailing matrix): the larger update partition
             const bool early = ex.sU2 && (double)(n - kn) > ex.big_frac * (double)n;
-            cudaStream_t sU = early ? ex.sU2 : ex.sU;
-            const int smsu = early ? ex.smsU2 : ex.smsU;
+            const bool late = !early && ex.sU3 && (double)(n - kn) < ex.small_frac * (double)n;
+            cudaStream_t sU = early ? ex.sU2 : (late ? ex.sU3 : ex.sU);
+            const int smsu = early ? ex.smsU2 : (late ? ex.smsU3 : ex.smsU);
             if (sU != cur) {                                   // keep the update work in order
                 MP_CUDA(cudaEventRecord(eSw, cur));
                 MP_CUDA(cudaStreamWaitEvent(sU, eSw, 0));
