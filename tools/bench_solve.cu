@@ -10,6 +10,7 @@ thread_local int64_t g_launches = 0;
 void func_smem_once(const void *fn, size_t bytes) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes); }
 void func_cluster16_once(const void *fn) { cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1); }
 bool pdl_enabled() { return false; }
+
 }
 #include "../paper_0808_2794_b200/csrc/k_solve.cu"
 using namespace mp;
