@@ -54,8 +54,14 @@ template <typename T> struct SCfg;
 template <> struct SCfg<float> {
     static constexpr int DN = 4;                  // near tiles handled by the chain CTA
     static constexpr int CHB = 2;                 // chain ring: blocks in flight
-    static constexpr int HS = 8;                  // helper ring stages
-    static constexpr int YB = 8;                  // y blocks fetched per helper batch
+#ifndef MP_HS
+#define MP_HS 8
+#endif
+#ifndef MP_YB
+#define MP_YB 8
+#endif
+    static constexpr int HS = MP_HS;              // helper ring stages
+    static constexpr int YB = MP_YB;              // y blocks fetched per helper batch
     static constexpr int MAXOWN = 12;             // far blocks owned by one helper CTA
 };
 template <> struct SCfg<double> {
