@@ -397,6 +397,7 @@ struct Factor {
     bool fuse_trsm = true;                 // MP_NO_FUSED_TRSM=1: separate K4 + K5 in the panel
     bool tc_inpanel = true;                // MP_NO_TC_INPANEL=1: FFMA tall-skinny GEMM for every in-panel level
     int psms = 148;                        // SMs the panel stream can count on
+    double terms4_frac = 0.0;              // MP_TF32_TERMS4_FRAC: steps with n - k below this * n use 4 MMAs
     float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
     cudaStream_t s;
@@ -420,11 +421,11 @@ struct Factor {
     // Schur update C -= L U.  big: the trailing update or the next panel's columns
     // (tensor-core variant when selected); scratch / nsm: the launching stream's.
     void gemm(cudaStream_t q, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool big,
-              int cls, float *scratch, int nsm, bool reuse_a = false) {
+              int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3) {
         prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
             if (big && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
-                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a);
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a, terms);
             else
                 launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
@@ -515,7 +516,9 @@ struct Factor {
                 launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
                 prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sU);
                 trsm(sU, k, w, kn, kn + wn);
-                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], smsu);
+                // late steps (trailing matrix < terms4_frac n, off the critical path): a fourth MMA
+                const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
+                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], smsu, false, terms);
                 MP_CUDA(cudaEventRecord(eN, sU));
                 MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
                 psms = std::max(8, sms - smsu);
@@ -530,7 +533,8 @@ struct Factor {
                 trsm(sU, k, w, kn + wn, n);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
                 const bool reuse = kn < n && n - kn >= 256 && wn >= 128;
-                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], smsu, reuse);
+                const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
+                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], smsu, reuse, terms);
             }
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
@@ -566,6 +570,7 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
     MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
     if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
     if (const char *e = std::getenv("MP_NO_TC_INPANEL")) f.tc_inpanel = e[0] != '1';
+    if (const char *e = std::getenv("MP_TF32_TERMS4_FRAC")) f.terms4_frac = std::atof(e);
     for (int b = 0; b < 2; ++b) {
         f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nb);
         f.nppairs[b] = pool.get<int32_t>(1);
@@ -1022,6 +1027,7 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
     if (const char *e = std::getenv("MP_NO_FUSED_TRSM")) f.fuse_trsm = e[0] != '1';
     if (const char *e = std::getenv("MP_NO_TC_INPANEL")) f.tc_inpanel = e[0] != '1';
+    if (const char *e = std::getenv("MP_TF32_TERMS4_FRAC")) f.terms4_frac = std::atof(e);
     f.ppairs[0] = pool.get<int32_t>(4 * (size_t)nb);
     f.nppairs[0] = pool.get<int32_t>(1);
     f.ps.ppairs = f.ppairs[0];

@@ -153,7 +153,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
 __global__ void __launch_bounds__(GT, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_constant__ CUtensorMap tmUl,
                    const __grid_constant__ CUtensorMap tmLh, const __grid_constant__ CUtensorMap tmLl,
-                   float *__restrict__ C, int64_t ldc, int M, int N, int K)
+                   float *__restrict__ C, int64_t ldc, int M, int N, int K, int terms)
 {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned ring (SWIZZLE_128B atoms)
@@ -225,12 +225,12 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
                         const uint32_t off = ks * 32;                  // 8 tf32 = 32 B along the swizzled row
                         const uint64_t dAh = umma_desc_sw128(sAh + off), dAl = umma_desc_sw128(sAl + off);
                         const uint64_t dBh = umma_desc_sw128(sBh + off), dBl = umma_desc_sw128(sBl + off);
-#if MP_TF32_TERMS == 4
-                        umma_tf32(tacc, dAl, dBl, (kc | ks) ? 1u : 0u);  // lo*lo (4xTF32)
-                        umma_tf32(tacc, dAl, dBh, 1u);
-#else
-                        umma_tf32(tacc, dAl, dBh, (kc | ks) ? 1u : 0u);  // small terms first
-#endif
+                        if (MP_TF32_TERMS == 4 || terms == 4) {
+                            umma_tf32(tacc, dAl, dBl, (kc | ks) ? 1u : 0u);  // lo*lo (4xTF32)
+                            umma_tf32(tacc, dAl, dBh, 1u);
+                        } else {
+                            umma_tf32(tacc, dAl, dBh, (kc | ks) ? 1u : 0u);  // small terms first
+                        }
                         umma_tf32(tacc, dAh, dBl, 1u);
                         umma_tf32(tacc, dAh, dBh, 1u);
                     }
@@ -371,7 +371,7 @@ size_t tf32_scratch_floats(int64_t n, int nbmax)
 }
 
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
-                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a)
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int kp = (int)round_up(K, 4);
@@ -395,14 +395,14 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
     func_smem_once((const void *)gemm_3xtf32_kernel, smem);
     launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N,
-              (int)K);
+              (int)K, terms);
 }
 
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a)
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms)
 {
     launch_gemm_ops_3xtf32(W + r0 * ldw + k0, ldw, W + k0 * ldw + c0, ldw, W + r0 * ldw + c0, ldw, M, N, K, scratch,
-                           num_sms, s, reuse_a);
+                           num_sms, s, reuse_a, terms);
 }
 
 }  // namespace mp
