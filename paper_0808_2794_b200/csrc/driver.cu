@@ -397,6 +397,7 @@ struct Factor {
     bool fuse_trsm = true;                 // MP_NO_FUSED_TRSM=1: separate K4 + K5 in the panel
     bool tc_inpanel = true;                // MP_NO_TC_INPANEL=1: FFMA tall-skinny GEMM for every in-panel level
     int psms = 148;                        // SMs the panel stream can count on
+    int32_t *cur_np = nullptr;             // panel-level pair counter of the panel being factored
     double terms4_frac = 0.0;              // MP_TF32_TERMS4_FRAC: steps with n - k below this * n use 4 MMAs
     float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
@@ -405,7 +406,7 @@ struct Factor {
     void leaf(cudaStream_t q, int64_t c0, int w, int64_t klo, int64_t khi) {
         const double m = (double)(n - c0);
         prof_begin(KC_PANEL, q);
-        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, q);
+        launch_panel_leaf<T>(W, ldw, n, c0, w, ipiv, ps, st, q, c0 == klo ? cur_np : nullptr);
         prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, q);
         if (khi - klo > w) {   // the leaf's interchanges, on the rest of its panel
             prof_begin(KC_LASWP, q);
@@ -455,7 +456,7 @@ struct Factor {
     }
     // panel [k, k+w) on stream q, its panel-level pairs into buffer b
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
-        launch_orig_init(ps.orig, k, n, nppairs[b], q);
+        cur_np = nppairs[b];                 // the first leaf zeroes it and starts orig[] as the identity
         panel(q, k, w, k, k + w);
         launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
     }

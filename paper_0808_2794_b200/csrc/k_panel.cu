@@ -189,6 +189,8 @@ struct LeafArgs {
     int32_t *pairs;        // leaf-level (position, origin-at-leaf-start) pairs, [2w][2]
     int32_t *npairs;
     DevStatus *st;
+    int32_t *first_np;     // first leaf of a panel: orig[] is the identity (not read) and this
+                           // panel-level pair counter is zeroed here (replaces orig_init_kernel)
 };
 
 // RPT rows per thread, leaf width W, column loop unrolled in groups of UG columns.
@@ -236,6 +238,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         if (g == 0) *a.npairs = 0;
+        if (g == 0 && a.first_np) *a.first_np = 0;
     }
     // every CTA's mbarriers must be initialised before anyone pushes into them
     cluster.sync();
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 #pragma unroll
             for (int s = 0; s < W; ++s) x[q][s] = (valid && s < w) ? row[s] : T(0);
         }
-        org[q] = valid ? a.orig[base + li] : -1;
+        org[q] = !valid ? -1 : (a.first_np ? (int)(base + li) : a.orig[base + li]);
         cs[q] = valid ? (int)(base + li) : ~(int)(base + li);
     }
 
@@ -589,7 +592,7 @@ int panel_leaf_width(int64_t m)
 
 template <typename T>
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
-                       DevStatus *st, cudaStream_t s)
+                       DevStatus *st, cudaStream_t s, int32_t *first_np)
 {
     const int clmax = cluster_size();
     const int64_t m = n - c0;
@@ -600,7 +603,7 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
     const int cl = (int)std::max<int64_t>(1, ceil_div(m, (int64_t)cfgs[sel].nt * cfgs[sel].rpt));
     LeafArgs<T> a;
     a.W = W; a.ldw = ldw; a.n = n; a.c0 = c0; a.w = w; a.ipiv = ipiv;
-    a.orig = ps.orig; a.pairs = ps.pairs; a.npairs = ps.npairs; a.st = st;
+    a.orig = ps.orig; a.pairs = ps.pairs; a.npairs = ps.npairs; a.st = st; a.first_np = first_np;
     if constexpr (sizeof(T) == 4) {
         switch (sel) {
         case 0: launch_cfg<T, MP_LEAF_C0>(a, cl, s); break;
@@ -633,8 +636,8 @@ void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs
 template int panel_leaf_width<float>(int64_t);
 template int panel_leaf_width<double>(int64_t);
 template void launch_panel_leaf<float>(float *, int64_t, int64_t, int64_t, int, int32_t *, PanelScratch &,
-                                       DevStatus *, cudaStream_t);
+                                       DevStatus *, cudaStream_t, int32_t *);
 template void launch_panel_leaf<double>(double *, int64_t, int64_t, int64_t, int, int32_t *, PanelScratch &,
-                                        DevStatus *, cudaStream_t);
+                                        DevStatus *, cudaStream_t, int32_t *);
 
 }  // namespace mp
