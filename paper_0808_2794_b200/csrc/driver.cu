@@ -398,6 +398,8 @@ struct Factor {
     bool tc_inpanel = true;                // MP_NO_TC_INPANEL=1: FFMA tall-skinny GEMM for every in-panel level
     int psms = 148;                        // SMs the panel stream can count on
     int32_t *cur_np = nullptr;             // panel-level pair counter of the panel being factored
+    EmitJob emit_job;                      // its pair emission, folded into the last leaf's laswp
+    bool emitted = false;
     double terms4_frac = 0.0;              // MP_TF32_TERMS4_FRAC: steps with n - k below this * n use 4 MMAs
     float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
@@ -410,7 +412,11 @@ struct Factor {
         prof_end(KC_PANEL, m * w * w - (double)w * w * w / 3.0, q);
         if (khi - klo > w) {   // the leaf's interchanges, on the rest of its panel
             prof_begin(KC_LASWP, q);
-            launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, klo, khi, c0, c0 + w, nullptr, q);
+            // the panel's last leaf: the same launch emits the panel-level pairs
+            const bool last = c0 + w == khi;
+            launch_laswp_pairs<T>(W, ldw, ps.pairs, ps.npairs, 2 * w, klo, khi, c0, c0 + w, nullptr, q,
+                                  last ? emit_job : EmitJob{});
+            if (last) emitted = true;
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(khi - klo - w) * sizeof(T), q);
         }
     }
@@ -457,8 +463,10 @@ struct Factor {
     // panel [k, k+w) on stream q, its panel-level pairs into buffer b
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
         cur_np = nppairs[b];                 // the first leaf zeroes it and starts orig[] as the identity
+        emit_job = EmitJob{ps.orig, k, n, ppairs[b], nppairs[b]};
+        emitted = false;
         panel(q, k, w, k, k + w);
-        launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
+        if (!emitted) launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
     }
     void run_sequential() {
         psms = sms;

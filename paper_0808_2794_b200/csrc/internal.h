@@ -158,10 +158,17 @@ void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs
 // ---------------------------------------------------------------- K3 laswp (k_laswp.cu)
 // Apply a (position <- origin row) pair list to columns [c_lo, c_hi) minus
 // [x_lo, x_hi); optionally also perm[pos] <- perm[orig] (perm != nullptr).
+// Optional extra work of a laswp launch: the panel-level pair emission of emit_pairs_kernel
+// (rows [k, n) whose origin orig[i] != i -> (i, orig[i]) appended at *npairs).
+struct EmitJob {
+    const int32_t *orig = nullptr;
+    int64_t k = 0, n = 0;
+    int32_t *pairs = nullptr, *npairs = nullptr;
+};
 template <typename T>
 void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *npairs, int max_pairs,
                         int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm,
-                        cudaStream_t s);
+                        cudaStream_t s, const EmitJob &ej = EmitJob{});
 void launch_init_perm(int32_t *perm, int64_t n, cudaStream_t s);
 void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStream_t s);
 

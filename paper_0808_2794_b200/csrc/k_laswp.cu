@@ -25,13 +25,26 @@ template <typename T, int SW>
 __global__ void __launch_bounds__(LT)
 laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ pairs,
                    const int32_t *__restrict__ npairs, int64_t c_lo, int64_t c_hi, int64_t x_lo,
-                   int64_t x_hi, int32_t *__restrict__ perm, int nstrips)
+                   int64_t x_hi, int32_t *__restrict__ perm, int nstrips, EmitJob ej)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
     pdl_trigger();
     const int np = *npairs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nfirst = nstrips + (perm ? 1 : 0);
+    if ((int)blockIdx.x >= nfirst) {           // extra CTAs: the panel-level pair emission (emit_pairs)
+        const int64_t stride = (int64_t)(gridDim.x - nfirst) * LT;
+        for (int64_t i = ej.k + (int64_t)(blockIdx.x - nfirst) * LT + threadIdx.x; i < ej.n; i += stride) {
+            const int32_t o = ej.orig[i];
+            if (o != (int32_t)i) {
+                const int slot = atomicAdd(ej.npairs, 1);
+                ej.pairs[2 * slot] = (int32_t)i;
+                ej.pairs[2 * slot + 1] = o;
+            }
+        }
+        return;
+    }
     if ((int)blockIdx.x == nstrips) {          // extra CTA: compose the running permutation
         int32_t *tmp = reinterpret_cast<int32_t *>(smem_raw);
         for (int i = threadIdx.x; i < np; i += LT) tmp[i] = perm[pairs[2 * i + 1]];
@@ -103,20 +116,21 @@ __global__ void invert_perm_kernel(const int32_t *perm, int32_t *pinv, int64_t n
 
 template <typename T>
 void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *npairs, int max_pairs,
-                        int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm, cudaStream_t s)
+                        int64_t c_lo, int64_t c_hi, int64_t x_lo, int64_t x_hi, int32_t *perm, cudaStream_t s, const EmitJob &ej)
 {
     // narrow column ranges (one panel's columns): 8-column strips, 4x the CTAs
     static const bool allnarrow = [] { const char *e = std::getenv("MP_LASWP_WIDE"); return !(e && e[0] == '1'); }();
     const bool narrow = allnarrow || c_hi - c_lo <= 1024;
     const int sw = narrow ? 8 : 32;
     const int nstrips = c_hi > c_lo ? (int)ceil_div(c_hi - c_lo, sw) : 0;
-    const int grid = nstrips + (perm ? 1 : 0);
+    const int nemit = ej.orig ? (int)std::min<int64_t>(ceil_div(ej.n - ej.k, LT), 64) : 0;
+    const int grid = nstrips + (perm ? 1 : 0) + nemit;
     if (grid == 0) return;
     const size_t smem = std::max<size_t>((size_t)max_pairs * sw * sizeof(T), (size_t)max_pairs * 4);
     auto kern = narrow ? laswp_pairs_kernel<T, 8> : laswp_pairs_kernel<T, 32>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
     launch_ex(kern, dim3(grid), dim3(LT), smem, s, nullptr, W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm,
-              nstrips);
+              nstrips, ej);
 }
 
 void launch_init_perm(int32_t *perm, int64_t n, cudaStream_t s)
@@ -132,8 +146,8 @@ void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStrea
 }
 
 template void launch_laswp_pairs<float>(float *, int64_t, const int32_t *, const int32_t *, int, int64_t, int64_t,
-                                        int64_t, int64_t, int32_t *, cudaStream_t);
+                                        int64_t, int64_t, int32_t *, cudaStream_t, const EmitJob &);
 template void launch_laswp_pairs<double>(double *, int64_t, const int32_t *, const int32_t *, int, int64_t,
-                                         int64_t, int64_t, int64_t, int32_t *, cudaStream_t);
+                                         int64_t, int64_t, int64_t, int32_t *, cudaStream_t, const EmitJob &);
 
 }  // namespace mp
