@@ -53,18 +53,24 @@ def peaks():
 
 # --------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms around the timed region.
+
+    nvidia-smi needs a few hundred ms to start, longer than a short timed region, so the sampler
+    is started before the warm-up (start()); the summary uses the samples stamped inside the timed
+    window [begin, end] widened by 150 ms on each side, and waits (up to 2 s) for one sample after
+    the window so that a short region is never unsampled."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
         self.index, self.rows, self.proc = index, [], None
+        self.t_begin = self.t_end = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -76,9 +82,20 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 8:
-                self.rows.append(parts)
+                self.rows.append((time.perf_counter(), parts))
+
+    # timed window
+    def __enter__(self):
+        if self.proc is None:
+            self.start()
+        self.t_begin = time.perf_counter()
+        return self
 
     def __exit__(self, *exc):
+        self.t_end = time.perf_counter()
+        deadline = self.t_end + 2.0
+        while self.proc and time.perf_counter() < deadline and not any(t > self.t_end for t, _ in self.rows):
+            time.sleep(0.02)
         if self.proc:
             self.proc.terminate()
             try:
@@ -87,14 +104,17 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        lo = (self.t_begin or 0.0) - 0.15
+        hi = (self.t_end or 1e30) + 0.15
+        rows = [r for t, r in self.rows if lo <= t <= hi]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(rows)}
 
 
 # --------------------------------------------------------------------------- reference arm (the oracle)
@@ -156,6 +176,7 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
     def solve(o=opts, report=True):
         return mp.mp_dsgesv_1dbc_ex(comm, n, nb, Al, B, X, o, report)
 
+    clk = ClockSampler(dev.index).start()                         # running before the warm-up
     for _ in range(args.warmup):
         _, it, info, _ = solve()
     assert info == 0 and it >= 0, (it, info)
@@ -165,7 +186,7 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
     reps = []
     barrier()
     torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clk:
+    with clk:
         e0.record(stream)
         for _ in range(args.steps):
             _, it, info, rep = solve()
@@ -332,6 +353,7 @@ def main():
         _, it, info, rep = mp.mp_dsgesv_ex(dA, dB, dX, opts)
         return it, info, rep
 
+    clk = ClockSampler(dev.index).start()                         # running before the warm-up
     for _ in range(args.warmup):
         it, info, rep = solve()
     assert info == 0 and it >= 0, (it, info)
@@ -343,7 +365,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     walls = []
-    with ClockSampler(dev.index) as clk:
+    with clk:
         e0.record(stream)
         for _ in range(args.steps):
             w0 = time.perf_counter()
