@@ -209,6 +209,7 @@ void make_loopback_comms(int nranks, Comm **out)
         c->rank = r;
         c->size = nranks;
         c->sh = sh;
+        c->shared_device = true;
         out[r] = c;
     }
 }

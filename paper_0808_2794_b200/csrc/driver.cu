@@ -1041,64 +1041,148 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     f.nppairs[0] = pool.get<int32_t>(1);
     f.ps.ppairs = f.ppairs[0];
     f.ps.nppairs = f.nppairs[0];
-    float *tf = nullptr;
-    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) tf = pool.get<float>(tf32_scratch_floats(n, (int)nb));
-    f.tf32[0] = f.tf32[1] = tf;                                  // one stream: panel and update share it
-    // broadcast buffer: [npairs][pairs 4nb][ipiv nb] then the panel rows (n - k) x nb
+    float *tf = nullptr, *tfp = nullptr;
+    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) {
+        tf = pool.get<float>(tf32_scratch_floats(n, (int)nb));
+        tfp = pool.get<float>(tf32_scratch_floats(n, (int)nb));
+    }
+    f.tf32[0] = tf;                                              // update stream
+    f.tf32[1] = tfp;                                             // panel stream (in-panel K = 128 level)
+    f.ppairs[1] = pool.get<int32_t>(4 * (size_t)nb);
+    f.nppairs[1] = pool.get<int32_t>(1);
+    // broadcast buffers (double-buffered for the look-ahead):
+    // [npairs][pairs 4nb][ipiv nb] then the panel rows (n - k) x nb
     const size_t hdr = (1 + 4 * (size_t)nb + (size_t)nb) * sizeof(int32_t);
     const size_t hdr_al = round_up((int64_t)hdr, 256);
-    char *buf = pool.get<char>(hdr_al + (size_t)n * nb * sizeof(T));
-    int32_t *b_np = reinterpret_cast<int32_t *>(buf), *b_pairs = b_np + 1, *b_ipiv = b_pairs + 4 * nb;
-    T *b_panel = reinterpret_cast<T *>(buf + hdr_al);
+    char *bufs[2] = {pool.get<char>(hdr_al + (size_t)n * nb * sizeof(T)), pool.get<char>(hdr_al + (size_t)n * nb * sizeof(T))};
+    // look-ahead (depth 1): the panel stream sP factors panel k+1 on its owner and carries every
+    // broadcast; the update stream s applies panel k to the local columns, the next panel's
+    // columns first.  MP_NO_LOOKAHEAD=1: everything on s, in order.
+    // With the single-GPU execution resources: the update on the 100-SM green context, the panel
+    // (and the broadcasts) on the high-priority panel stream; the caller's stream joins both.
+    const bool la = !(std::getenv("MP_NO_LOOKAHEAD") && std::getenv("MP_NO_LOOKAHEAD")[0] == '1');
+    // (loopback ranks share one GPU and must not share these per-device streams)
+    const ExecRes &ex = cm.shared_device ? ExecRes{} : exec_res();
+    const cudaStream_t s_caller = s;
+    cudaStream_t sP = s;
+    bool own_sP = false;
+    int sms_upd = f.sms;
+    if (la && ex.ok) {
+        sP = ex.sP;
+        s = ex.sU;
+        sms_upd = ex.smsU;
+        f.psms = std::max(8, f.sms - ex.smsU);
+    } else if (la) {
+        int lo = 0, hi = 0;
+        MP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        MP_CUDA(cudaStreamCreateWithPriority(&sP, cudaStreamNonBlocking, hi));
+        own_sP = true;
+    }
+    cudaEvent_t eB[2], eU[2], eN, e0;
+    for (int i = 0; i < 2; ++i) {
+        MP_CUDA(cudaEventCreateWithFlags(&eB[i], cudaEventDisableTiming));
+        MP_CUDA(cudaEventCreateWithFlags(&eU[i], cudaEventDisableTiming));
+        MP_CUDA(cudaEventRecord(eU[i], s));                     // both buffers free at the start
+    }
+    MP_CUDA(cudaEventCreateWithFlags(&eN, cudaEventDisableTiming));
+    MP_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    if (s != s_caller) {                                         // the set-up above ran on the caller's stream
+        MP_CUDA(cudaEventRecord(e0, s_caller));
+        MP_CUDA(cudaStreamWaitEvent(s, e0, 0));
+        for (int i = 0; i < 2; ++i) MP_CUDA(cudaEventRecord(eU[i], s));
+    }
     launch_init_perm(perm, n, s);
-    for (int64_t k = 0, j = 0; k < n; k += nb, ++j) {
+    MP_CUDA(cudaEventRecord(e0, s));
+    MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));                     // workspace set-up done
+    const int64_t nblk = d.nblk;
+    auto lcol = [&](int64_t j) { return (j / d.P) * nb; };        // owner's local column of block j
+    // panel j on its owner (stream sP, after the owner's update of its columns)
+    auto factor_on_owner = [&](int64_t j) {
+        const int64_t k = j * nb;
         const int w = (int)std::min<int64_t>(nb, n - k);
-        const int o = d.owner(j);
-        const int64_t lc0 = (j / d.P) * nb;                      // owner's local column of the panel
-        if (d.r == o) {
-            f.W = Wl + (lc0 - k);                                // global column c <-> local lc0 + (c - k)
-            f.factor_panel(s, k, w, 0);
-            MP_CUDA(cudaMemcpyAsync(b_np, f.nppairs[0], sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            MP_CUDA(cudaMemcpyAsync(b_pairs, f.ppairs[0], 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            MP_CUDA(cudaMemcpyAsync(b_ipiv, ipiv + k, w * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            MP_CUDA(cudaMemcpy2DAsync(b_panel, nb * sizeof(T), Wl + k * ldw + lc0, ldw * sizeof(T), w * sizeof(T),
-                                      n - k, cudaMemcpyDeviceToDevice, s));
+        f.W = Wl + (lcol(j) - k);                                // global column c <-> local lcol + (c - k)
+        f.factor_panel(sP, k, w, (int)(j & 1));
+    };
+    // C(local cols [c_lo, c_hi)) -= L21 U12 with U12 = L11^-1 A12, panel k (Lp: its column 0)
+    auto update_cols = [&](const T *Lp, int64_t k, int w, int64_t c_lo, int64_t c_hi) {
+        const int64_t ncol = c_hi - c_lo;
+        if (ncol <= 0 || k + w >= n) return;
+        prof_begin(KC_TRSM, s);
+        launch_trsm_ops<T>(Lp + k * ldw, ldw, Wl + k * ldw + c_lo, ldw, w, ncol, s);
+        prof_end(KC_TRSM, (double)w * w * (double)ncol, s);
+        const int64_t M = n - k - w;
+        prof_begin(KC_TRAIL, s);
+        if constexpr (sizeof(T) == 4) {
+            if (tf && M >= 256 && ncol >= 128)
+                launch_gemm_ops_3xtf32(Lp + (k + w) * ldw, ldw, Wl + k * ldw + c_lo, ldw, Wl + (k + w) * ldw + c_lo, ldw,
+                                       M, ncol, w, tf, sms_upd, s);
+            else
+                launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + c_lo, ldw, Wl + (k + w) * ldw + c_lo, ldw, M,
+                                   ncol, w, s);
+        } else {
+            launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + c_lo, ldw, Wl + (k + w) * ldw + c_lo, ldw, M, ncol,
+                               w, s);
         }
-        if (d.P > 1) cm.bcast(buf, hdr_al + (size_t)(n - k) * nb * sizeof(T), o, s);
+        prof_end(KC_TRAIL, 2.0 * M * ncol * w, s);
+    };
+    if (d.r == d.owner(0)) factor_on_owner(0);
+    for (int64_t j = 0; j < nblk; ++j) {
+        const int64_t k = j * nb;
+        const int w = (int)std::min<int64_t>(nb, n - k);
+        const int o = d.owner(j), bi = (int)(j & 1);
+        char *buf = bufs[bi];
+        int32_t *b_np = reinterpret_cast<int32_t *>(buf), *b_pairs = b_np + 1, *b_ipiv = b_pairs + 4 * nb;
+        T *b_panel = reinterpret_cast<T *>(buf + hdr_al);
+        // ---- pack (owner) and broadcast panel j, on sP (the buffer is free once s unpacked j - 2)
+        MP_CUDA(cudaStreamWaitEvent(sP, eU[bi], 0));
+        if (d.r == o) {
+            MP_CUDA(cudaMemcpyAsync(b_np, f.nppairs[bi], sizeof(int32_t), cudaMemcpyDeviceToDevice, sP));
+            MP_CUDA(cudaMemcpyAsync(b_pairs, f.ppairs[bi], 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, sP));
+            MP_CUDA(cudaMemcpyAsync(b_ipiv, ipiv + k, w * sizeof(int32_t), cudaMemcpyDeviceToDevice, sP));
+            MP_CUDA(cudaMemcpy2DAsync(b_panel, nb * sizeof(T), Wl + k * ldw + lcol(j), ldw * sizeof(T), w * sizeof(T),
+                                      n - k, cudaMemcpyDeviceToDevice, sP));
+        }
+        if (d.P > 1) cm.bcast(buf, hdr_al + (size_t)(n - k) * nb * sizeof(T), o, sP);
+        MP_CUDA(cudaEventRecord(eB[bi], sP));
+        // ---- update stream: unpack (non-owners), interchanges, next panel's columns, the rest
+        MP_CUDA(cudaStreamWaitEvent(s, eB[bi], 0));
         if (d.r != o) {
-            MP_CUDA(cudaMemcpyAsync(f.nppairs[0], b_np, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-            MP_CUDA(cudaMemcpyAsync(f.ppairs[0], b_pairs, 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(f.nppairs[bi], b_np, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(f.ppairs[bi], b_pairs, 4 * nb * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
             MP_CUDA(cudaMemcpyAsync(ipiv + k, b_ipiv, w * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
             MP_CUDA(cudaMemcpy2DAsync(Wl + k * ldw + d.nloc, ldw * sizeof(T), b_panel, nb * sizeof(T), w * sizeof(T),
                                       n - k, cudaMemcpyDeviceToDevice, s));
         }
+        MP_CUDA(cudaEventRecord(eU[bi], s));
         // the panel's interchanges on this rank's other columns (+ the replicated permutation)
-        const int64_t xlo = d.r == o ? lc0 : 0, xhi = d.r == o ? lc0 + w : 0;
+        const int64_t xlo = d.r == o ? lcol(j) : 0, xhi = d.r == o ? lcol(j) + w : 0;
         prof_begin(KC_LASWP, s);
-        launch_laswp_pairs<T>(Wl, ldw, f.ppairs[0], f.nppairs[0], 2 * w, 0, d.nloc, xlo, xhi, perm, s);
+        launch_laswp_pairs<T>(Wl, ldw, f.ppairs[bi], f.nppairs[bi], 2 * w, 0, d.nloc, xlo, xhi, perm, s);
         prof_end(KC_LASWP, 2.0 * 2 * w * (double)d.nloc * sizeof(T), s);
-        const T *Lp = d.r == o ? Wl + lc0 : Wl + d.nloc;        // column 0 of the panel
-        const int64_t lt0 = d.local_after(j), ntr = d.nloc - lt0;
-        if (ntr > 0 && k + w < n) {
-            prof_begin(KC_TRSM, s);
-            launch_trsm_ops<T>(Lp + k * ldw, ldw, Wl + k * ldw + lt0, ldw, w, ntr, s);
-            prof_end(KC_TRSM, (double)w * w * (double)ntr, s);
-            const int64_t M = n - k - w;
-            prof_begin(KC_TRAIL, s);
-            if constexpr (sizeof(T) == 4) {
-                if (tf && M >= 256 && ntr >= 128)
-                    launch_gemm_ops_3xtf32(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0,
-                                           ldw, M, ntr, w, tf, f.sms, s);
-                else
-                    launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0,
-                                       ldw, M, ntr, w, s);
-            } else {
-                launch_gemm_ops<T>(Lp + (k + w) * ldw, ldw, Wl + k * ldw + lt0, ldw, Wl + (k + w) * ldw + lt0, ldw, M,
-                                   ntr, w, s);
-            }
-            prof_end(KC_TRAIL, 2.0 * M * ntr * w, s);
+        const T *Lp = d.r == o ? Wl + lcol(j) : Wl + d.nloc;    // column 0 of the panel
+        const int64_t lt0 = d.local_after(j);
+        int64_t rest0 = lt0;
+        if (j + 1 < nblk && d.r == d.owner(j + 1)) {
+            // this rank factors the next panel: its columns first, then the panel on sP
+            const int wn = (int)std::min<int64_t>(nb, n - k - nb);
+            update_cols(Lp, k, w, lt0, lt0 + wn);
+            rest0 = lt0 + wn;
+            MP_CUDA(cudaEventRecord(eN, s));
+            MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
+            factor_on_owner(j + 1);
         }
+        update_cols(Lp, k, w, rest0, d.nloc);
     }
+    // join: the caller's stream waits for the panel and update streams' last work
+    MP_CUDA(cudaEventRecord(e0, sP));
+    MP_CUDA(cudaStreamWaitEvent(s_caller, e0, 0));
+    MP_CUDA(cudaEventRecord(eN, s));
+    MP_CUDA(cudaStreamWaitEvent(s_caller, eN, 0));
+    MP_CUDA(cudaStreamSynchronize(s_caller));
+    if (own_sP) MP_CUDA(cudaStreamDestroy(sP));
+    for (int i = 0; i < 2; ++i) { MP_CUDA(cudaEventDestroy(eB[i])); MP_CUDA(cudaEventDestroy(eU[i])); }
+    MP_CUDA(cudaEventDestroy(eN));
+    MP_CUDA(cudaEventDestroy(e0));
 }
 
 // all-gather the distributed factors into the full row-major working copy Wf (n x ldf)

@@ -251,6 +251,7 @@ struct CommError {
 // Collectives of the 1D block-cyclic path, enqueued on (or synchronised with) stream s.
 struct Comm {
     int rank = 0, size = 1;
+    bool shared_device = false;   // loopback: every rank on this process's GPU (no shared streams)
     virtual ~Comm() {}
     virtual void bcast(void *buf, size_t bytes, int root, cudaStream_t s) = 0;
     virtual void allreduce_sum(double *buf, size_t count, cudaStream_t s) = 0;
