@@ -152,7 +152,6 @@ template <typename T>
 // first_np != nullptr: the panel's first leaf (orig[] taken as the identity, *first_np zeroed)
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
                        DevStatus *st, cudaStream_t s, int32_t *first_np = nullptr);
-void launch_orig_init(int32_t *orig, int64_t k, int64_t n, int32_t *npairs, cudaStream_t s);   // also zeroes *npairs
 void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 laswp (k_laswp.cu)

@@ -190,7 +190,7 @@ struct LeafArgs {
     int32_t *npairs;
     DevStatus *st;
     int32_t *first_np;     // first leaf of a panel: orig[] is the identity (not read) and this
-                           // panel-level pair counter is zeroed here (replaces orig_init_kernel)
+                           // panel-level pair counter is zeroed here
 };
 
 // RPT rows per thread, leaf width W, column loop unrolled in groups of UG columns.
@@ -482,15 +482,6 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     }
 }
 
-__global__ void orig_init_kernel(int32_t *orig, int64_t k, int64_t n, int32_t *npairs)
-{
-    pdl_wait();
-    pdl_trigger();
-    if (blockIdx.x == 0 && threadIdx.x == 0) *npairs = 0;     // emit_pairs_kernel's counter
-    for (int64_t i = k + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        orig[i] = (int32_t)i;
-}
-
 __global__ void emit_pairs_kernel(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs)
 {
     pdl_wait();
@@ -619,12 +610,6 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
         default: launch_cfg<T, 512, 8, 4>(a, cl, s); break;
         }
     }
-}
-
-void launch_orig_init(int32_t *orig, int64_t k, int64_t n, int32_t *npairs, cudaStream_t s)
-{
-    launch_ex(orig_init_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(n - k, 256), 512)), dim3(256), 0, s,
-              nullptr, orig, k, n, npairs);
 }
 
 void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s)
