@@ -401,7 +401,9 @@ struct Factor {
     EmitJob emit_job;                      // its pair emission, folded into the last leaf's laswp
     bool emitted = false;
     double terms4_frac = 0.0;              // MP_TF32_TERMS4_FRAC: steps with n - k below this * n use 4 MMAs
-    float *tf32[2] = {nullptr, nullptr};   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
+    float *tf32[2] = {nullptr, nullptr};
+    float *tfU[2] = {nullptr, nullptr};    // look-ahead: update-stream scratch per step parity (the panel
+                                           // stream writes step k+1's L21 split while step k still runs)   // 3xTF32 split scratch: [0] trailing stream, [1] panel stream
     int sms = 148;
     cudaStream_t s;
 
@@ -495,13 +497,27 @@ struct Factor {
         cudaStream_t sP = ex.sP, cur = ex.sU;
         psms = std::max(8, sms - ex.smsU);
         cudaEvent_t e0 = la_event(0), eP[2] = {la_event(1), la_event(2)}, eN = la_event(3);
-        cudaEvent_t eEndP = la_event(4), eEndU = la_event(5), eSw = la_event(6);
+        cudaEvent_t eEndP = la_event(4), eEndU = la_event(5), eSw = la_event(6), eS[2] = {la_event(7), la_event(8)};
+        // L21 of panel j (rows [j + w, n) x its columns) split hi/lo on the panel stream right after
+        // the panel, into the update scratch of that step's parity: the update stream's interchanges
+        // and TRSM of the next panel's columns run meanwhile (the split is off its critical path)
+        const bool presplit = sizeof(T) == 4 && variant == MP_VARIANT_3XTF32 && tfU[1] != nullptr;
+        auto split_l21 = [&](int64_t kp0, int wp, int bb) -> bool {
+            const int64_t M = n - kp0 - wp;
+            if (!presplit || M < 256) return false;
+            if constexpr (sizeof(T) == 4)
+                launch_split_a_3xtf32(W + (kp0 + wp) * ldw + kp0, ldw, M, wp, tfU[bb], sP);
+            MP_CUDA(cudaEventRecord(eS[bb], sP));
+            return true;
+        };
+        bool split_ok[2] = {false, false};
         MP_CUDA(cudaEventRecord(e0, s));
         MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
         MP_CUDA(cudaStreamWaitEvent(cur, e0, 0));
         launch_init_perm(perm, n, cur);
         factor_panel(sP, 0, (int)std::min<int64_t>(nb, n), 0);
         MP_CUDA(cudaEventRecord(eP[0], sP));
+        split_ok[0] = split_l21(0, (int)std::min<int64_t>(nb, n), 0);
         int idx = 0;
         for (int64_t k = 0; k < n; k += nb, ++idx) {
             const int w = (int)std::min<int64_t>(nb, n - k);
@@ -525,14 +541,17 @@ struct Factor {
                 launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
                 prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sU);
                 trsm(sU, k, w, kn, kn + wn);
+                if (split_ok[b]) MP_CUDA(cudaStreamWaitEvent(sU, eS[b], 0));
                 // late steps (trailing matrix < terms4_frac n, off the critical path): a fourth MMA
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
-                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, tf32[0], smsu, false, terms);
+                gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu, split_ok[b],
+                     terms);
                 MP_CUDA(cudaEventRecord(eN, sU));
                 MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
                 psms = std::max(8, sms - smsu);
                 factor_panel(sP, kn, wn, b ^ 1);
                 MP_CUDA(cudaEventRecord(eP[b ^ 1], sP));
+                split_ok[b ^ 1] = split_l21(kn, wn, b ^ 1);
             }
             // ... then every other column (left factors, rest of the trailing matrix), off it
             prof_begin(KC_LASWP, sU);
@@ -541,9 +560,10 @@ struct Factor {
             if (kn < n && kn + wn < n) {
                 trsm(sU, k, w, kn + wn, n);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
-                const bool reuse = kn < n && n - kn >= 256 && wn >= 128;
+                const bool reuse = split_ok[b] || (kn < n && n - kn >= 256 && wn >= 128);
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
-                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, tf32[0], smsu, reuse, terms);
+                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
+                     reuse, terms);
             }
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
@@ -571,6 +591,8 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
     if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) {
         f.tf32[0] = pool.get<float>(tf32_scratch_floats(n, nb));
         f.tf32[1] = pool.get<float>(tf32_scratch_floats(n, nb));
+        f.tfU[0] = f.tf32[0];
+        f.tfU[1] = pool.get<float>(tf32_scratch_floats(n, nb));
     }
     f.ps.orig = pool.get<int32_t>(n);
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);

@@ -398,6 +398,17 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
               (int)K, terms);
 }
 
+// The hi/lo split of the A operand alone (M x K rows at A, lda) into scratch, in the layout
+// launch_gemm_ops_3xtf32 expects (so a later call with reuse_a = true and the same M, K uses it).
+void launch_split_a_3xtf32(const float *A, int64_t lda, int64_t M, int64_t K, float *scratch, cudaStream_t s)
+{
+    if (M <= 0 || K <= 0) return;
+    const int kp = (int)round_up(K, 4);
+    const int64_t tot = M * kp;
+    launch_ex(split_rows_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(tot, 256), 4096)), dim3(256), 0, s, nullptr,
+              A, lda, (int)M, (int)K, scratch, scratch + (size_t)M * kp, kp);
+}
+
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                                int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms)
 {
