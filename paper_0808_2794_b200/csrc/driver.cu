@@ -422,19 +422,20 @@ struct Factor {
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(khi - klo - w) * sizeof(T), q);
         }
     }
-    void trsm(cudaStream_t q, int64_t r0, int w, int64_t c_lo, int64_t c_hi) {
+    void trsm(cudaStream_t q, int64_t r0, int w, int64_t c_lo, int64_t c_hi, float *sh = nullptr, float *sl = nullptr,
+              int kp = 0) {
         prof_begin(KC_TRSM, q);
-        launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, q);
+        launch_trsm_lower_unit<T>(W, ldw, r0, w, c_lo, c_hi, q, sh, sl, kp);
         prof_end(KC_TRSM, (double)w * w * (double)(c_hi - c_lo), q);
     }
     // Schur update C -= L U.  big: the trailing update or the next panel's columns
     // (tensor-core variant when selected); scratch / nsm: the launching stream's.
     void gemm(cudaStream_t q, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool big,
-              int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3) {
+              int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3, bool reuse_b = false) {
         prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
             if (big && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
-                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a, terms);
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a, terms, reuse_b);
             else
                 launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
@@ -540,12 +541,16 @@ struct Factor {
                 prof_begin(KC_LASWP, sU);
                 launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
                 prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sU);
-                trsm(sU, k, w, kn, kn + wn);
+                // the TRSM also writes U12's hi/lo split when the update takes the 3xTF32 path
+                const int kp = (int)round_up(w, 4);
+                const bool bsplit = split_ok[b] && wn >= 128 && w <= 256;   // (the TRSM writes it for w <= 256)
+                float *bh = bsplit ? tfU[b] + 2 * (size_t)(n - kn) * kp : nullptr;
+                trsm(sU, k, w, kn, kn + wn, bh, bsplit ? bh + (size_t)wn * kp : nullptr, kp);
                 if (split_ok[b]) MP_CUDA(cudaStreamWaitEvent(sU, eS[b], 0));
                 // late steps (trailing matrix < terms4_frac n, off the critical path): a fourth MMA
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
                 gemm(sU, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu, split_ok[b],
-                     terms);
+                     terms, bsplit);
                 MP_CUDA(cudaEventRecord(eN, sU));
                 MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
                 psms = std::max(8, sms - smsu);
@@ -558,12 +563,16 @@ struct Factor {
             launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, n, k, kn + wn, perm, sU);
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w - wn) * sizeof(T), sU);
             if (kn < n && kn + wn < n) {
-                trsm(sU, k, w, kn + wn, n);
+                const int kp = (int)round_up(w, 4);
+                const int64_t nr = n - kn - wn;
+                const bool bsplit = split_ok[b] && nr >= 128 && w <= 256;
+                float *bh = bsplit ? tfU[b] + 2 * (size_t)(n - kn) * kp : nullptr;
+                trsm(sU, k, w, kn + wn, n, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
                 const bool reuse = split_ok[b] || (kn < n && n - kn >= 256 && wn >= 128);
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
                 gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
-                     reuse, terms);
+                     reuse, terms, bsplit);
             }
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));

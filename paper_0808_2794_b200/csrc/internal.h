@@ -173,12 +173,15 @@ void launch_invert_perm(const int32_t *perm, int32_t *pinv, int64_t n, cudaStrea
 
 // ---------------------------------------------------------------- K4 trsm (k_trsm.cu)
 // U12 <- L11^{-1} A12: rows [r0, r0+w), columns [c_lo, c_hi), L11 = unit lower of W[r0.., r0..].
+// sh/sl (binary32, optional): also write U12's 3xTF32 hi/lo split, K-major with row stride kp (the
+// B operand layout of launch_gemm_ops_3xtf32; then call it with reuse_b).
 template <typename T>
 void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi,
-                            cudaStream_t s);
+                            cudaStream_t s, float *sh = nullptr, float *sl = nullptr, int kp = 0);
 // Same with separate operands: X[w x ncols] <- L^{-1} X, L = unit lower w x w (row-major, ldl).
 template <typename T>
-void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s);
+void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s,
+                     float *sh = nullptr, float *sl = nullptr, int kp = 0);
 
 // ---------------------------------------------------------------- K5 Schur update (k_gemm.cu)
 // C[M x N] -= A[M x K] * B[K x N], all row-major views into W with stride ldw:
@@ -202,11 +205,11 @@ template <typename T>
 bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
                             int32_t *ticket, cudaStream_t s);
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3);
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false);
 // split of the A operand only (see launch_gemm_ops_3xtf32's reuse_a)
 void launch_split_a_3xtf32(const float *A, int64_t lda, int64_t M, int64_t K, float *scratch, cudaStream_t s);
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
-                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3);
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false);
 
 // ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
 struct SolveScratch {

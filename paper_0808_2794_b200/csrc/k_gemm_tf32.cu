@@ -371,7 +371,7 @@ size_t tf32_scratch_floats(int64_t n, int nbmax)
 }
 
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
-                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms)
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms, bool reuse_b)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int kp = (int)round_up(K, 4);
@@ -383,7 +383,8 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
             launch_ex(split_rows_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(tot, 256), 4096)), dim3(256), 0, s,
                       nullptr, A, lda, (int)M, (int)K, Lh, Ll, kp);
         dim3 g((unsigned)ceil_div(N, 32), (unsigned)ceil_div(kp, 32));
-        launch_ex(split_cols_T_kernel, g, dim3(32, 8), 0, s, nullptr, B, ldb, (int)N, (int)K, Uh, Ul, kp);
+        if (!reuse_b)                       // reuse_b: Uh/Ul written by the TRSM that produced B
+            launch_ex(split_cols_T_kernel, g, dim3(32, 8), 0, s, nullptr, B, ldb, (int)N, (int)K, Uh, Ul, kp);
     }
     CUtensorMap mUh, mUl, mLh, mLl;
     encode_kmajor(&mUh, Uh, (int)N, (int)K, kp, TM_COLS);
@@ -410,10 +411,11 @@ void launch_split_a_3xtf32(const float *A, int64_t lda, int64_t M, int64_t K, fl
 }
 
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms)
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms,
+                               bool reuse_b)
 {
     launch_gemm_ops_3xtf32(W + r0 * ldw + k0, ldw, W + k0 * ldw + c0, ldw, W + r0 * ldw + c0, ldw, M, N, K, scratch,
-                           num_sms, s, reuse_a, terms);
+                           num_sms, s, reuse_a, terms, reuse_b);
 }
 
 }  // namespace mp

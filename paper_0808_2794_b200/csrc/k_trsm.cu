@@ -43,9 +43,19 @@ __device__ __forceinline__ void cp_async(uint32_t dst, const void *src, bool ok)
 // warps 0-7 (4 rows each) subtract the contribution of block b-1 (the only one on the chain:
 // older blocks were subtracted while the solver worked on block b-1), then warp 8 solves the
 // 32 x 32 unit-lower diagonal block row by row (x_m -= sum_{i<m} l_mi x_i, four partial sums).
+__device__ __forceinline__ float rna_tf32(float x)
+{
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// sh/sl (binary32 only, optional): also write U12 split for the 3xTF32 update, transposed K-major
+// (sh[j * kp + k] = rna_tf32(U12(k, j)), sl = rna_tf32(U12 - sh)) — split_cols_T_kernel's output
 template <typename T>
 __global__ void __launch_bounds__(TW * 32, 1)
-trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols)
+trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols,
+                       float *__restrict__ sh, float *__restrict__ sl, int kp)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     pdl_wait();
@@ -157,6 +167,37 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
         const int r = e >> 5, cc = e & 31;
         if (r < w && c0 + cc < ncols) X[(int64_t)r * ldx + c0 + cc] = Xs[e];
     }
+    if constexpr (sizeof(T) == 4) {
+        if (sh) {
+            // the hi/lo split: warp-strided 32-row blocks, lane = column (conflict-free shared reads);
+            // each lane then writes 32 consecutive k of its column (16-byte stores)
+            const int nwarp = blockDim.x >> 5;
+            const bool cok = c0 + lane < ncols;
+            for (int rb = warp; rb * 32 < kp; rb += nwarp) {
+                const int r0 = rb * 32;
+                float h[32], l[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float x = r0 + i < w ? (float)Xs[(size_t)(r0 + i) * CWS + lane] : 0.f;
+                    h[i] = rna_tf32(x);
+                    l[i] = rna_tf32(x - h[i]);
+                }
+                if (!cok) continue;
+                float *ph = sh + (c0 + lane) * (int64_t)kp + r0, *pl = sl + (c0 + lane) * (int64_t)kp + r0;
+                if (r0 + 32 <= kp && (kp & 3) == 0) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        *reinterpret_cast<float4 *>(ph + i) = make_float4(h[i], h[i + 1], h[i + 2], h[i + 3]);
+                        *reinterpret_cast<float4 *>(pl + i) = make_float4(l[i], l[i + 1], l[i + 2], l[i + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (r0 + i < kp) { ph[i] = h[i]; pl[i] = l[i]; }
+                }
+            }
+        }
+    }
 }
 
 }  // namespace
@@ -169,7 +210,8 @@ size_t trsm_smem(int w)
 }
 
 template <typename T>
-void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s)
+void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t ncols, cudaStream_t s, float *sh,
+                     float *sl, int kp)
 {
     if (ncols <= 0 || w <= 0) return;
     constexpr int WMAX = sizeof(T) == 4 ? 256 : 128;          // staged triangle must fit shared memory
@@ -184,18 +226,24 @@ void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t 
     const int grid = (int)ceil_div(ncols, CWS);
     auto kern = trsm_lower_unit_kernel<T>;
     func_smem_once((const void *)kern, trsm_smem<T>(WMAX));   // the largest request, set once
-    launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols);
+    if (w > (sizeof(T) == 4 ? 256 : 128)) sh = sl = nullptr;
+    launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols, sh, sl, kp);
 }
 
 template <typename T>
-void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi, cudaStream_t s)
+void launch_trsm_lower_unit(T *W, int64_t ldw, int64_t r0, int w, int64_t c_lo, int64_t c_hi, cudaStream_t s,
+                            float *sh, float *sl, int kp)
 {
-    launch_trsm_ops<T>(W + r0 * ldw + r0, ldw, W + r0 * ldw + c_lo, ldw, w, c_hi - c_lo, s);
+    launch_trsm_ops<T>(W + r0 * ldw + r0, ldw, W + r0 * ldw + c_lo, ldw, w, c_hi - c_lo, s, sh, sl, kp);
 }
 
-template void launch_trsm_ops<float>(const float *, int64_t, float *, int64_t, int, int64_t, cudaStream_t);
-template void launch_trsm_ops<double>(const double *, int64_t, double *, int64_t, int, int64_t, cudaStream_t);
-template void launch_trsm_lower_unit<float>(float *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t);
-template void launch_trsm_lower_unit<double>(double *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t);
+template void launch_trsm_ops<float>(const float *, int64_t, float *, int64_t, int, int64_t, cudaStream_t, float *,
+                                     float *, int);
+template void launch_trsm_ops<double>(const double *, int64_t, double *, int64_t, int, int64_t, cudaStream_t, float *,
+                                      float *, int);
+template void launch_trsm_lower_unit<float>(float *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t, float *,
+                                            float *, int);
+template void launch_trsm_lower_unit<double>(double *, int64_t, int64_t, int, int64_t, int64_t, cudaStream_t, float *,
+                                             float *, int);
 
 }  // namespace mp
