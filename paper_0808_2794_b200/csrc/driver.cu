@@ -456,10 +456,16 @@ struct Factor {
                            launch_trsm_gemm_fused<T>(W, ldw, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, ps.ticket, q);
         prof_end(KC_GEMM, fused ? 2.0 * (n - c0 - w1) * (w - w1) * w1 + (double)w1 * w1 * (w - w1) : 0.0, q);
         if (!fused) {
-            trsm(q, c0, w1, c0 + w1, c0 + w);
-            // the widest in-panel level (K >= 128) on the tensor cores too, on the SMs the update leaves
+            // the widest in-panel level (K >= 128) on the tensor cores too, on the SMs the update leaves;
+            // its TRSM writes U12's hi/lo split when the GEMM takes the 3xTF32 path
             const bool tc = tc_inpanel && w1 >= 128;
-            gemm(q, c0 + w1, c0 + w1, c0, n - c0 - w1, w - w1, w1, tc, KC_GEMM, tc ? tf32[1] : nullptr, psms);
+            const int64_t M = n - c0 - w1;
+            const int kp = (int)round_up(w1, 4);
+            const bool bsplit = sizeof(T) == 4 && tc && variant == MP_VARIANT_3XTF32 && tf32[1] && M >= 256 &&
+                                w - w1 >= 128 && w1 <= 256;
+            float *bh = bsplit ? tf32[1] + 2 * (size_t)M * kp : nullptr;
+            trsm(q, c0, w1, c0 + w1, c0 + w, bh, bsplit ? bh + (size_t)(w - w1) * kp : nullptr, kp);
+            gemm(q, c0 + w1, c0 + w1, c0, M, w - w1, w1, tc, KC_GEMM, tc ? tf32[1] : nullptr, psms, false, 3, bsplit);
         }
         panel(q, c0 + w1, w - w1, klo, khi);
     }
