@@ -161,6 +161,16 @@ def test_solve_inv_vs_substitution(mp, orc, n, nrhs, seed):
     assert certificate_ok(A, Xi, B) and certificate_ok(A, Xs, B)
 
 
+@pytest.mark.parametrize("n,nrhs,seed", [(700, 20, 61), (1100, 33, 62)])
+def test_many_rhs(mp, orc, n, nrhs, seed):
+    """nrhs above one solve launch's 16 columns (chunked sweeps, multi-column residual)."""
+    A, B, X = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+    ro = orc.dsgesv(A, B)
+    Xg, it, info, rep = gpu_solve(mp, A, B)
+    assert info == ro.info == 0 and it >= 0 and abs(it - ro.iters) <= 1, (it, ro.iters)
+    assert certificate_ok(A, Xg, B)
+
+
 def block_kappa_max(L, U, bs=64):
     """max over the 64-row diagonal blocks of L and U of kappa_inf = ||T||_inf ||T^-1||_inf."""
     n = L.shape[0]
