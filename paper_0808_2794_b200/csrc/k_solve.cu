@@ -52,8 +52,14 @@ constexpr int MAXR = 16;               // right-hand sides per launch
 
 template <typename T> struct SCfg;
 template <> struct SCfg<float> {
-    static constexpr int DN = 4;                  // near tiles handled by the chain CTA
-    static constexpr int CHB = 2;                 // chain ring: blocks in flight
+#ifndef MP_SOLVE_DN
+#define MP_SOLVE_DN 3                 // swept 2..5: 3 is best (1.13 vs 1.17 ms per pair at n = 16384)
+#endif
+#ifndef MP_SOLVE_CHB
+#define MP_SOLVE_CHB 2
+#endif
+    static constexpr int DN = MP_SOLVE_DN;        // near tiles handled by the chain CTA
+    static constexpr int CHB = MP_SOLVE_CHB;      // chain ring: blocks in flight
 #ifndef MP_HS
 #define MP_HS 8
 #endif
