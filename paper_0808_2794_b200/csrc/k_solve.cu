@@ -151,7 +151,11 @@ __device__ __forceinline__ bool mbar_try(uint64_t *bar, uint32_t parity)
 }
 __device__ __forceinline__ void mbar_wait_idle(uint64_t *bar, uint32_t parity)
 {
-    while (!mbar_try(bar, parity)) __nanosleep(100);
+#ifndef MP_IDLE_NS
+#define MP_IDLE_NS 0                  // swept 0/20/100 ns: plain polling is ~1 % faster
+#endif
+    while (!mbar_try(bar, parity))
+        if (MP_IDLE_NS > 0) __nanosleep(MP_IDLE_NS);
 }
 // Spin-wait on an mbarrier phase.  The loop is C++ (not a branch inside inline asm), so the
 // compiler places the reconvergence point after it: lanes that leave the loop in different
