@@ -34,6 +34,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -1047,7 +1048,9 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     MP_CUDA(cudaGetDevice(&dev));
     MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int dnmin = std::min(sweep_dn<T, 1>(), sweep_dn<T, MAXR>());
-    const int helpers = std::max(1, std::min(sms - 1, nblk - dnmin - 1));
+    static const int hmax = [] { const char *e = std::getenv("MP_SOLVE_HELPERS"); return e ? std::atoi(e) : 0; }();
+    const int hcap = hmax > 0 ? std::min(hmax, sms - 1) : sms - 1;
+    const int helpers = std::max(1, std::min(hcap, nblk - dnmin - 1));
     if (ceil_div(std::max(0, nblk - dnmin - 1), helpers) > SCfg<T>::MAXOWN)
         throw CudaError{cudaErrorInvalidValue, "matrix too large for the triangular-solve helper grid", __LINE__};
     for (int64_t c0 = 0; c0 < nrhs; c0 += MAXR) {
