@@ -772,6 +772,9 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     rs.counter = pool.get<unsigned>(1);
     SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<float>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
     MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    ss.tags = pool.get<uint64_t>(solve_tag_words(n, nrhs));
+    ss.tag_cols = (int)std::min<int64_t>(nrhs, 16);
+    MP_CUDA(cudaMemsetAsync(ss.tags, 0, solve_tag_words(n, nrhs) * sizeof(uint64_t), s));
     double *dpart = pool.get<double>((size_t)sms * 8);
     unsigned *dcnt = pool.get<unsigned>(1);
     MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));
@@ -1319,6 +1322,9 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
     rs.counter = pool.get<unsigned>(1);
     SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<float>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
     MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    ss.tags = pool.get<uint64_t>(solve_tag_words(n, nrhs));
+    ss.tag_cols = (int)std::min<int64_t>(nrhs, 16);
+    MP_CUDA(cudaMemsetAsync(ss.tags, 0, solve_tag_words(n, nrhs) * sizeof(uint64_t), s));
     double *dpart = pool.get<double>((size_t)sms * 8);
     unsigned *dcnt = pool.get<unsigned>(1);
     MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));

@@ -216,7 +216,12 @@ struct SolveScratch {
     unsigned *flags;      // [4][nblk] y / F ready flags (forward, backward), epoch-tagged, zeroed once
     void *F;              // [min(nrhs,16)][n] far partial sums (element type of the solve)
     unsigned epoch;       // last epoch used (incremented per sweep)
+    // binary32 solves: [2][tag_cols][n] 64-bit words {value bits, sweep tag} for the y (chain ->
+    // helpers) and F (helpers -> chain) exchanges, zeroed once; nullptr = flag exchange
+    uint64_t *tags = nullptr;
+    int tag_cols = 0;
 };
+size_t solve_tag_words(int64_t n, int64_t nrhs);
 // Forward (unit L) then backward (U) substitution on Y (n x nrhs, T, column-major
 // with ld n) with the packed LU in W; then X (double, ld n) = (mode 0) or += (mode 1) Y.
 // inv (binary32 solves only; nullptr = substitution): the inverted diagonal blocks and the

@@ -192,6 +192,19 @@ __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v)
 {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// tagged exchange word {value bits (low), sweep tag (high)}: one 64-bit access is single-copy
+// atomic, so a consumer that sees the tag sees the value; no flag, no fence
+__device__ __forceinline__ unsigned long long ld_tag(const uint64_t *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_tag(uint64_t *p, float v, unsigned tag)
+{
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
 __device__ __forceinline__ void spin_until(const unsigned *flag, unsigned epoch)
 {
     while (ld_relaxed_u32(flag) != epoch) { }
@@ -217,9 +230,11 @@ struct SweepArgs {
     double *X;             // [nrhs][n] binary64 solution (upper sweep only)
     T *F;                  // [nrhs][n] far partial sums
     unsigned *yflag, *fflag;
+    uint64_t *tY, *tF;     // binary32 only: tagged y / F words [nrhs][n], nullptr = flags
     int64_t n;
     int nrhs, nblk, accumulate;
     unsigned epoch;
+    unsigned tag;          // this sweep's tag in tY / tF
 };
 
 __device__ __forceinline__ float rcp_rn(float v) { return __frcp_rn(v); }
@@ -287,6 +302,42 @@ __device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane,
 #ifdef MP_SOLVE_TRACE
     if (lane == 0 && t < 4096) g_strace[t][4] = (unsigned long long)clock64();
 #endif
+    if constexpr (sizeof(T) == 4) {
+        if (far && a.tF != nullptr) {
+            // poll the tagged F words of the block directly: one round trip, no flag
+            for (int i0b = 0; i0b < a.nrhs * BS; i0b += 128) {
+                T yv[4], fv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = i0b + lane + 32 * u, c = idx / BS, r = idx - c * BS;
+                    yv[u] = (idx < a.nrhs * BS && r < nr) ? a.Y[(int64_t)c * n + i0 + r] : T(0);
+                }
+                for (;;) {
+                    bool ok = true;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int idx = i0b + lane + 32 * u, c = idx / BS, r = idx - c * BS;
+                        fv[u] = T(0);
+                        if (idx < a.nrhs * BS && r < nr) {
+                            const unsigned long long w = ld_tag(a.tF + (int64_t)c * n + i0 + r);
+                            fv[u] = __uint_as_float((unsigned)w);
+                            ok &= (unsigned)(w >> 32) == a.tag;
+                        }
+                    }
+                    if (__all_sync(0xffffffffu, ok)) break;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int idx = i0b + lane + 32 * u;
+                    if (idx < a.nrhs * BS) rsb[idx] = yv[u] - fv[u];
+                }
+            }
+#ifdef MP_SOLVE_TRACE
+            if (lane == 0 && t < 4096) g_strace[t][5] = (unsigned long long)clock64();
+#endif
+            return;
+        }
+    }
     if (far && lane == 0) spin_until(a.fflag + I, a.epoch);
     __syncwarp();
 #ifdef MP_SOLVE_TRACE
@@ -424,6 +475,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
     T *sm = reinterpret_cast<T *>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     __shared__ __align__(8) uint64_t full[16], empty[16];
     __shared__ int s_nready;
+    __shared__ unsigned s_ymask[3];
 #ifdef MP_SOLVE_TRACE
     __shared__ float s_tv;
 #endif
@@ -612,6 +664,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                                     if (row < nr) {
                                         const int64_t gi = (int64_t)c * n + i0 + row;
                                         a.Y[gi] = y;
+                                        if constexpr (sizeof(T) == 4)
+                                            if (a.tY != nullptr) st_tag(a.tY + gi, y, a.tag);
                                         if (!LOWER) {
                                             const double xv = a.accumulate ? xb[c * BS + row] : 0.0;
                                             a.X[gi] = xv + (double)y;
@@ -712,10 +766,14 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     ys[(size_t)slot * R * BS + c * BS + lane + 32] = v1;
                     if (lane < nr) {
                         a.Y[(int64_t)c * n + i0 + lane] = v0;
+                        if constexpr (sizeof(T) == 4)
+                            if (a.tY != nullptr) st_tag(a.tY + (int64_t)c * n + i0 + lane, v0, a.tag);
                         if (!LOWER) a.X[(int64_t)c * n + i0 + lane] = xo0 + (double)v0;
                     }
                     if (lane + 32 < nr) {
                         a.Y[(int64_t)c * n + i0 + lane + 32] = v1;
+                        if constexpr (sizeof(T) == 4)
+                            if (a.tY != nullptr) st_tag(a.tY + (int64_t)c * n + i0 + lane + 32, v1, a.tag);
                         if (!LOWER) a.X[(int64_t)c * n + i0 + lane + 32] = xo1 + (double)v1;
                     }
                 }
@@ -787,6 +845,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < MAXOWN * R * BS; i += NTH) accs[i] = T(0);
+    if (tid < 3) s_ymask[tid] = ~0u;
     __syncthreads();
     if (warp == WPROD) {
         // ---------------- producer: tiles (I_o, J_tp) in consumption order
@@ -810,7 +869,92 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
     const int tr = tid >> 3, tq = tid & 7;
     int seq = 0;
     int tp = 0;
+    unsigned round = 0;
+    const bool tagged = sizeof(T) == 4 && a.tY != nullptr;
+    auto helper_block = [&](int k) {
+        const T *yv = yb + (size_t)k * R * BS;
+        for (int o = 0; o < nown; ++o) {
+            if (town[o] < tp + DN + 1) continue;
+            const int s = seq % HS;
+            mbar_wait(&full[s], (uint32_t)((seq / HS) & 1));
+            T acc[2][R];
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int c = 0; c < R; ++c) acc[p][c] = T(0);
+            tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, yv, tr, 32, tq, nrhs, acc);
+#pragma unroll
+            for (int p = 0; p < 2; ++p)
+#pragma unroll
+                for (int c = 0; c < R; ++c)
+                    if (c < nrhs) {
+                        T v = acc[p][c];
+                        v += __shfl_xor_sync(0xffffffffu, v, 1);
+                        v += __shfl_xor_sync(0xffffffffu, v, 2);
+                        v += __shfl_xor_sync(0xffffffffu, v, 4);
+                        if (tq == 0) accs[((size_t)o * R + c) * BS + tr + 32 * p] += v;
+                    }
+            nbar_sync(1, NHC);
+            if (tid == 0) mbar_arrive(&empty[s]);
+            ++seq;
+            if (town[o] == tp + DN + 1) {                 // F of block o complete: publish
+                const int64_t i0 = (int64_t)blk_of<LOWER>(town[o], nblk) * BS;
+                if constexpr (sizeof(T) == 4) {
+                    if (tagged) {
+                        for (int idx = tid; idx < nrhs * BS; idx += NHC) {
+                            const int c = idx / BS, r = idx - c * BS;
+                            if (i0 + r < n) st_tag(a.tF + (int64_t)c * n + i0 + r, accs[((size_t)o * R + c) * BS + r], a.tag);
+                        }
+                        continue;
+                    }
+                }
+                for (int idx = tid; idx < nrhs * BS; idx += NHC) {
+                    const int c = idx / BS, r = idx - c * BS;
+                    if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * R + c) * BS + r];
+                }
+                // the barrier orders every thread's F stores before thread 0's fence + release
+                // (cumulativity): one fence per publish instead of one per thread
+                nbar_sync(1, NHC);
+                if (tid == 0) {
+                    __threadfence();
+                    st_release_u32(a.fflag + blk_of<LOWER>(town[o], nblk), a.epoch);
+                }
+            }
+        }
+    };
     while (tp <= tmax) {
+        if (tagged) {
+            // read up to YB y blocks straight from their tagged words; the AND over all
+            // threads of the per-block validity masks gives the published prefix
+            const int nbmax = min(YB, tmax - tp + 1);
+            int nb = 0;
+            while (nb == 0) {
+                unsigned mine = (1u << nbmax) - 1u;
+                for (int idx = tid; idx < nbmax * nrhs * BS; idx += NHC) {
+                    const int k = idx / (nrhs * BS), rem = idx - k * nrhs * BS;
+                    const int c = rem / BS, r = rem - c * BS;
+                    const int64_t j = (int64_t)blk_of<LOWER>(tp + k, nblk) * BS + r;
+                    T v = T(0);
+                    if (j < n) {
+                        const unsigned long long w = ld_tag(a.tY + (int64_t)c * n + j);
+                        v = __uint_as_float((unsigned)w);
+                        if ((unsigned)(w >> 32) != a.tag) mine &= ~(1u << k);
+                    }
+                    yb[(size_t)k * R * BS + c * BS + r] = v;
+                }
+                mine = __reduce_and_sync(0xffffffffu, mine);
+                unsigned *mk = s_ymask + round % 3;
+                if (lane == 0) atomicAnd(mk, mine);
+                nbar_sync(1, NHC);
+                const unsigned m = *mk;
+                if (tid == 0) s_ymask[(round + 2) % 3] = ~0u;   // read last in round - 1
+                ++round;
+                nb = __ffs(~m) - 1;
+                if (nb > nbmax) nb = nbmax;
+            }
+            for (int k = 0; k < nb; ++k, ++tp) helper_block(k);
+            continue;
+        }
         // how many consecutive y blocks are published (at least one: wait for it)
         if (tid == 0) {
             spin_until(a.yflag + blk_of<LOWER>(tp, nblk), a.epoch);
@@ -828,48 +972,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             yb[(size_t)k * R * BS + c * BS + r] = j < n ? __ldcg(a.Y + (int64_t)c * n + j) : T(0);
         }
         nbar_sync(1, NHC);
-        for (int k = 0; k < nb; ++k, ++tp) {
-            const T *yv = yb + (size_t)k * R * BS;
-            for (int o = 0; o < nown; ++o) {
-                if (town[o] < tp + DN + 1) continue;
-                const int s = seq % HS;
-                mbar_wait(&full[s], (uint32_t)((seq / HS) & 1));
-                T acc[2][R];
-#pragma unroll
-                for (int p = 0; p < 2; ++p)
-#pragma unroll
-                    for (int c = 0; c < R; ++c) acc[p][c] = T(0);
-                tile_gemv<T, R, 2>(tiles + (size_t)s * TILE, yv, tr, 32, tq, nrhs, acc);
-#pragma unroll
-                for (int p = 0; p < 2; ++p)
-#pragma unroll
-                    for (int c = 0; c < R; ++c)
-                        if (c < nrhs) {
-                            T v = acc[p][c];
-                            v += __shfl_xor_sync(0xffffffffu, v, 1);
-                            v += __shfl_xor_sync(0xffffffffu, v, 2);
-                            v += __shfl_xor_sync(0xffffffffu, v, 4);
-                            if (tq == 0) accs[((size_t)o * R + c) * BS + tr + 32 * p] += v;
-                        }
-                nbar_sync(1, NHC);
-                if (tid == 0) mbar_arrive(&empty[s]);
-                ++seq;
-                if (town[o] == tp + DN + 1) {                 // F of block o complete: publish
-                    const int64_t i0 = (int64_t)blk_of<LOWER>(town[o], nblk) * BS;
-                    for (int idx = tid; idx < nrhs * BS; idx += NHC) {
-                        const int c = idx / BS, r = idx - c * BS;
-                        if (i0 + r < n) a.F[(int64_t)c * n + i0 + r] = accs[((size_t)o * R + c) * BS + r];
-                    }
-                    // the barrier orders every thread's F stores before thread 0's fence + release
-                    // (cumulativity): one fence per publish instead of one per thread
-                    nbar_sync(1, NHC);
-                    if (tid == 0) {
-                        __threadfence();
-                        st_release_u32(a.fflag + blk_of<LOWER>(town[o], nblk), a.epoch);
-                    }
-                }
-            }
-        }
+        for (int k = 0; k < nb; ++k, ++tp) helper_block(k);
     }
 }
 
@@ -995,6 +1098,7 @@ __global__ void __launch_bounds__(256) diag_inv_kernel(const float *__restrict__
 int solve_block_rows() { return BS; }
 
 size_t solve_flag_words(int64_t n) { return 4 * (size_t)ceil_div(n, BS); }
+size_t solve_tag_words(int64_t n, int64_t nrhs) { return 2 * (size_t)std::min<int64_t>(std::max<int64_t>(nrhs, 1), MAXR) * n; }
 
 size_t solve_inv_floats(int64_t n) { return (size_t)4 * (size_t)ceil_div(n, BS) * BS * BS + 2; }
 
@@ -1048,6 +1152,7 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     MP_CUDA(cudaGetDevice(&dev));
     MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     const int dnmin = std::min(sweep_dn<T, 1>(), sweep_dn<T, MAXR>());
+    static const bool tags_off = std::getenv("MP_SOLVE_FLAGS") != nullptr;   // A/B: flag exchange
     static const int hmax = [] { const char *e = std::getenv("MP_SOLVE_HELPERS"); return e ? std::atoi(e) : 0; }();
     const int hcap = hmax > 0 ? std::min(hmax, sms - 1) : sms - 1;
     const int helpers = std::max(1, std::min(hcap, nblk - dnmin - 1));
@@ -1066,9 +1171,14 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
         a.yflag = ss.flags;
         a.fflag = ss.flags + nblk;
         a.epoch = ++ss.epoch;
+        const bool tagged = sizeof(T) == 4 && ss.tags != nullptr && nc <= ss.tag_cols && !tags_off;
+        a.tY = tagged ? ss.tags : nullptr;
+        a.tF = tagged ? ss.tags + (size_t)ss.tag_cols * n : nullptr;
+        a.tag = 2u * a.epoch;
         launch_sweep<T, true>(tm, tDL, tML, use_inv, a, 1 + helpers, s);
         a.yflag = ss.flags + 2 * nblk;
         a.fflag = ss.flags + 3 * nblk;
+        a.tag = 2u * a.epoch + 1u;
         launch_sweep<T, false>(tm, tDU, tMU, use_inv, a, 1 + helpers, s);
         g_launches += 2;
     }

@@ -26,6 +26,9 @@ int main(int argc, char **argv) {
     cudaMalloc(&fl, solve_flag_words(n) * 4); cudaMemset(fl, 0, solve_flag_words(n) * 4);
     cudaMemcpy(W, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
     SolveScratch ss{fl, F, 0u};
+    if (!getenv("NOTAGS")) {
+      cudaMalloc(&ss.tags, solve_tag_words(n, 1) * 8); cudaMemset(ss.tags, 0, solve_tag_words(n, 1) * 8); ss.tag_cols = 1;
+    }
     float *inv = nullptr;
     if (getenv("INV")) { cudaMalloc(&inv, solve_inv_floats(n) * 4); launch_solve_inverses(W, ldw, n, inv, 0); }
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
