@@ -54,7 +54,7 @@ constexpr int MAXR = 16;               // right-hand sides per launch
 template <typename T> struct SCfg;
 template <> struct SCfg<float> {
 #ifndef MP_SOLVE_DN
-#define MP_SOLVE_DN 3                 // swept 2..5: 3 is best (1.13 vs 1.17 ms per pair at n = 16384)
+#define MP_SOLVE_DN 2                 // swept 1..5: with tagged exchanges 2 is best (0.77 vs 0.83 ms per pair at n = 16384)
 #endif
 #ifndef MP_SOLVE_CHB
 #define MP_SOLVE_CHB 2
