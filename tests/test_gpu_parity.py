@@ -388,3 +388,40 @@ def test_strict_parity_ffma(mp, orc):
     Xg, it, info, rep = gpu_solve(mp, A, B, variant=mp.MP_VARIANT_FFMA)
     assert info == 0 and abs(it - ro.iters) <= 1
     assert np.abs(Xg - ro.X).max() / np.abs(ro.X).max() <= 1e-12
+
+
+_EXCHANGE_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_0808_2794_b200 import binding as mp, inputs
+n, nrhs, seed = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+A, B, _ = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+X, it, info, rep = mp.mp_dsgesv_ex(mp.colmajor_cuda(A), mp.colmajor_cuda(B))
+torch.cuda.synchronize()
+np.save(sys.argv[5], X.cpu().numpy())
+print(it, info)
+"""
+
+
+@pytest.mark.parametrize("n,nrhs,seed", [(1500, 3, 71), (700, 20, 72)])
+def test_solve_exchange_modes_bitwise(mp, tmp_path, n, nrhs, seed):
+    """The tagged {value, tag} y/F exchange of the binary32 sweeps and the epoch-flag exchange
+    (MP_SOLVE_FLAGS=1, read once per process: run in a child) move the same values, so the
+    whole solve is bitwise identical."""
+    import os
+    import subprocess
+    import sys
+    import torch
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    A, B, _ = inputs.gaussian(n, nrhs=nrhs, seed=seed)
+    X, it, info, rep = mp.mp_dsgesv_ex(mp.colmajor_cuda(A), mp.colmajor_cuda(B))
+    torch.cuda.synchronize()
+    Xt = X.cpu().numpy()
+    out = str(tmp_path / "x_flags.npy")
+    env = dict(os.environ, MP_SOLVE_FLAGS="1")
+    r = subprocess.run([sys.executable, "-c", _EXCHANGE_CHILD, root, str(n), str(nrhs), str(seed), out],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    it_f, info_f = map(int, r.stdout.split()[-2:])
+    assert info == info_f == 0 and it == it_f
+    assert np.array_equal(Xt.view(np.uint64), np.load(out).view(np.uint64))
