@@ -1022,9 +1022,9 @@ void launch_sweep(const CUtensorMap &tm, const CUtensorMap &tD, const CUtensorMa
 // sweep's padded rows stay zero.  A zero u_ii (only with a recorded zero pivot, which
 // sends the driver to the fallback before any solve) gives a zero row.
 template <bool LOWER>
-__global__ void __launch_bounds__(256) diag_inv_kernel(const float *__restrict__ W, int64_t ldw, int64_t n,
-                                                       float *__restrict__ Dinv, float *__restrict__ Mo,
-                                                       unsigned long long *__restrict__ cond_max)
+__device__ __forceinline__ void diag_inv_block(const float *__restrict__ W, int64_t ldw, int64_t n,
+                                               float *__restrict__ Dinv, float *__restrict__ Mo,
+                                               unsigned long long *__restrict__ cond_max)
 {
     constexpr int LD = BS + 1;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1093,6 +1093,15 @@ __global__ void __launch_bounds__(256) diag_inv_kernel(const float *__restrict__
     }
 }
 
+// blockIdx.y = 0: L blocks, 1: U blocks (one launch: the two sets are independent)
+__global__ void __launch_bounds__(256) diag_inv_kernel(const float *__restrict__ W, int64_t ldw, int64_t n,
+                                                       float *__restrict__ inv, size_t blk,
+                                                       unsigned long long *__restrict__ cond_max)
+{
+    if (blockIdx.y == 0) diag_inv_block<true>(W, ldw, n, inv, inv + blk, cond_max);
+    else diag_inv_block<false>(W, ldw, n, inv + 2 * blk, inv + 3 * blk, cond_max);
+}
+
 }  // namespace
 
 int solve_block_rows() { return BS; }
@@ -1110,11 +1119,8 @@ void launch_solve_inverses(const float *W, int64_t ldw, int64_t n, float *inv, c
     const int nblk = (int)ceil_div(n, BS);
     const size_t blk = (size_t)nblk * BS * BS;
     const size_t smem = (size_t)3 * BS * (BS + 1) * sizeof(double);
-    func_smem_once((const void *)diag_inv_kernel<true>, smem);
-    func_smem_once((const void *)diag_inv_kernel<false>, smem);
-    launch_ex(diag_inv_kernel<true>, dim3(nblk), dim3(256), smem, s, nullptr, W, ldw, n, inv, inv + blk, cond);
-    launch_ex(diag_inv_kernel<false>, dim3(nblk), dim3(256), smem, s, nullptr, W, ldw, n, inv + 2 * blk, inv + 3 * blk,
-              cond);
+    func_smem_once((const void *)diag_inv_kernel, smem);
+    launch_ex(diag_inv_kernel, dim3(nblk, 2), dim3(256), smem, s, nullptr, W, ldw, n, inv, blk, cond);
 }
 
 double solve_inverses_cond(const float *inv, int64_t n, cudaStream_t s)
