@@ -11,6 +11,7 @@
 // unit-lower diagonal block.  FMA work w^2 N; the chain is nb = w/32 links of (one 32x32x32
 // contribution over 8 warps + one 32-step substitution).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -52,7 +53,9 @@ __device__ __forceinline__ float rna_tf32(float x)
 
 // sh/sl (binary32 only, optional): also write U12 split for the 3xTF32 update, transposed K-major
 // (sh[j * kp + k] = rna_tf32(U12(k, j)), sl = rna_tf32(U12 - sh)) — split_cols_T_kernel's output
-template <typename T>
+// CW = 16 (narrow column ranges: twice the CTAs): lanes l and l + 16 share column l & 15 and
+// split each warp's 4 update rows (2 each); the solver's upper half-warp recomputes, writes nothing
+template <typename T, int CW>
 __global__ void __launch_bounds__(TW * 32, 1)
 trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, int w, int64_t ncols,
                        float *__restrict__ sh, float *__restrict__ sl, int kp)
@@ -63,24 +66,26 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
     constexpr int EPC = 16 / (int)sizeof(T);                  // elements per 16-byte chunk
     const int nb = (w + RB - 1) / RB;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb * RB][CWS] the strip
-    T *Ls = Xs + (size_t)nb * RB * CWS;                       // [nb(nb+1)/2][RB][LP]
-    const int64_t c0 = (int64_t)blockIdx.x * CWS;
+    T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb * RB][CW] the strip
+    T *Ls = Xs + (size_t)nb * RB * CW;                        // [nb(nb+1)/2][RB][LP]
+    const int64_t c0 = (int64_t)blockIdx.x * CW;
+    constexpr int NR = CW == 32 ? 4 : 2;                      // update rows per thread
+    const int cl = lane % CW, hr = lane / CW;                 // column, row half
     const bool vec = ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(X)) & 15) == 0 &&
                      (ldl % EPC) == 0 && (ldx % EPC) == 0;
     // ---- stage the strip and the triangle (16-byte chunks when aligned, else elements)
     {
         const uint32_t xb = (uint32_t)__cvta_generic_to_shared(Xs);
-        constexpr int CPR = CWS / EPC;                        // chunks per strip row
+        constexpr int CPR = CW / EPC;                         // chunks per strip row
         for (int e = tid; e < nb * RB * CPR; e += blockDim.x) {
             const int r = e / CPR, cc = (e - r * CPR) * EPC;
             if (vec && r < w && c0 + cc + EPC <= ncols) {
-                cp_async<16>(xb + (uint32_t)(r * CWS + cc) * sizeof(T), X + (int64_t)r * ldx + c0 + cc, true);
+                cp_async<16>(xb + (uint32_t)(r * CW + cc) * sizeof(T), X + (int64_t)r * ldx + c0 + cc, true);
             } else {
 #pragma unroll
                 for (int q = 0; q < EPC; ++q) {
                     const bool ok = r < w && c0 + cc + q < ncols;
-                    cp_async<(int)sizeof(T)>(xb + (uint32_t)(r * CWS + cc + q) * sizeof(T),
+                    cp_async<(int)sizeof(T)>(xb + (uint32_t)(r * CW + cc + q) * sizeof(T),
                                              X + (int64_t)(ok ? r : 0) * ldx + (ok ? c0 + cc + q : 0), ok);
                 }
             }
@@ -112,18 +117,20 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     constexpr int NU = TW - 1;                                // updater warps
-    const int r4 = 4 * warp;                                  // updater: rows r4 .. r4+3 of each block
-    T acc[4] = {T(0), T(0), T(0), T(0)};                      // updater: pending sum for the next block
+    const int r4 = 4 * warp + NR * hr;                        // updater: rows r4 .. r4+NR-1 of each block
+    T acc[NR];                                                // updater: pending sum for the next block
+#pragma unroll
+    for (int i = 0; i < NR; ++i) acc[i] = T(0);
     auto contrib = [&](int bt, int k) {                       // acc += L(bt, k) X_k for this thread's rows
         const T *lr = Ls + (size_t)(bt * (bt + 1) / 2 + k) * RB * LP + (size_t)r4 * LP;
-        const T *xk = Xs + (size_t)k * RB * CWS + lane;
+        const T *xk = Xs + (size_t)k * RB * CW + cl;
 #pragma unroll 2
         for (int kk = 0; kk < RB; kk += 4) {
             T xv[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) xv[j] = xk[(kk + j) * CWS];
+            for (int j = 0; j < 4; ++j) xv[j] = xk[(kk + j) * CW];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < NR; ++i) {
                 const T *l = lr + i * LP + kk;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) acc[i] = fma(l[j], xv[j], acc[i]);
@@ -134,9 +141,9 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
         if (warp < NU) {
             if (b > 0) {
                 contrib(b, b - 1);                            // the chain's contribution
-                T *xr = Xs + (size_t)(b * RB + r4) * CWS + lane;
+                T *xr = Xs + (size_t)(b * RB + r4) * CW + cl;
 #pragma unroll
-                for (int i = 0; i < 4; ++i) { xr[i * CWS] -= acc[i]; acc[i] = T(0); }
+                for (int i = 0; i < NR; ++i) { xr[i * CW] -= acc[i]; acc[i] = T(0); }
             }
             named_bar_sync(1, TW * 32);                       // rows of block b ready for the solver
             if (b + 1 < nb)
@@ -145,10 +152,10 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
         } else {
             named_bar_sync(1, TW * 32);
             const T *ld = Ls + (size_t)(b * (b + 1) / 2 + b) * RB * LP;
-            T *xb = Xs + (size_t)b * RB * CWS + lane;
+            T *xb = Xs + (size_t)b * RB * CW + cl;
             T x[RB];
 #pragma unroll
-            for (int i = 0; i < RB; ++i) x[i] = xb[i * CWS];
+            for (int i = 0; i < RB; ++i) x[i] = xb[i * CW];
 #pragma unroll
             for (int m = 1; m < RB; ++m) {
                 const T *lm = ld + m * LP;
@@ -157,14 +164,16 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
                 for (int i = 0; i < m; ++i) p[i & 3] = fma(lm[i], x[i], p[i & 3]);
                 x[m] -= (p[0] + p[1]) + (p[2] + p[3]);
             }
+            if (hr == 0) {
 #pragma unroll
-            for (int i = 0; i < RB; ++i) xb[i * CWS] = x[i];
+                for (int i = 0; i < RB; ++i) xb[i * CW] = x[i];
+            }
             named_bar_sync(2, TW * 32);
         }
     }
     // ---- U12 back to global memory (coalesced rows)
-    for (int e = tid; e < nb * RB * CWS; e += blockDim.x) {
-        const int r = e >> 5, cc = e & 31;
+    for (int e = tid; e < nb * RB * CW; e += blockDim.x) {
+        const int r = e / CW, cc = e % CW;
         if (r < w && c0 + cc < ncols) X[(int64_t)r * ldx + c0 + cc] = Xs[e];
     }
     if constexpr (sizeof(T) == 4) {
@@ -172,13 +181,13 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
             // the hi/lo split: warp-strided 32-row blocks, lane = column (conflict-free shared reads);
             // each lane then writes 32 consecutive k of its column (16-byte stores)
             const int nwarp = blockDim.x >> 5;
-            const bool cok = c0 + lane < ncols;
+            const bool cok = lane < CW && c0 + lane < ncols;
             for (int rb = warp; rb * 32 < kp; rb += nwarp) {
                 const int r0 = rb * 32;
                 float h[32], l[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const float x = r0 + i < w ? (float)Xs[(size_t)(r0 + i) * CWS + lane] : 0.f;
+                    const float x = r0 + i < w ? (float)Xs[(size_t)(r0 + i) * CW + cl] : 0.f;
                     h[i] = rna_tf32(x);
                     l[i] = rna_tf32(x - h[i]);
                 }
@@ -203,10 +212,10 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
 }  // namespace
 
 template <typename T>
-size_t trsm_smem(int w)
+size_t trsm_smem(int w, int cw = CWS)
 {
     const int nb = (w + RB - 1) / RB;
-    return ((size_t)nb * RB * CWS + (size_t)(nb * (nb + 1) / 2) * RB * LP) * sizeof(T) + 16;
+    return ((size_t)nb * RB * cw + (size_t)(nb * (nb + 1) / 2) * RB * LP) * sizeof(T) + 16;
 }
 
 template <typename T>
@@ -222,12 +231,16 @@ void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t 
         launch_trsm_ops<T>(L + (int64_t)w1 * ldl + w1, ldl, X + (int64_t)w1 * ldx, ldx, w - w1, ncols, s);
         return;
     }
-    const int nb = (w + RB - 1) / RB;
-    const int grid = (int)ceil_div(ncols, CWS);
-    auto kern = trsm_lower_unit_kernel<T>;
-    func_smem_once((const void *)kern, trsm_smem<T>(WMAX));   // the largest request, set once
+    // narrow ranges (a panel's columns): 16-column strips while twice the CTAs still fit one wave
+    static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
+    static const bool cw16_off = std::getenv("MP_TRSM_CW32") != nullptr;
+    const bool cw16 = !cw16_off && ceil_div(ncols, 16) <= std::min(96, sms);
+    const int cw = cw16 ? 16 : CWS;
+    const int grid = (int)ceil_div(ncols, cw);
+    auto kern = cw16 ? trsm_lower_unit_kernel<T, 16> : trsm_lower_unit_kernel<T, CWS>;
+    func_smem_once((const void *)kern, trsm_smem<T>(WMAX, cw));   // the largest request, set once per kernel
     if (w > (sizeof(T) == 4 ? 256 : 128)) sh = sl = nullptr;
-    launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w), s, nullptr, L, ldl, X, ldx, w, ncols, sh, sl, kp);
+    launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w, cw), s, nullptr, L, ldl, X, ldx, w, ncols, sh, sl, kp);
 }
 
 template <typename T>
