@@ -69,7 +69,7 @@ trsm_lower_unit_kernel(const T *L, int64_t ldl, T *__restrict__ X, int64_t ldx, 
     T *Xs = reinterpret_cast<T *>(smem_raw);                  // [nb * RB][CW] the strip
     T *Ls = Xs + (size_t)nb * RB * CW;                        // [nb(nb+1)/2][RB][LP]
     const int64_t c0 = (int64_t)blockIdx.x * CW;
-    constexpr int NR = CW == 32 ? 4 : 2;                      // update rows per thread
+    constexpr int NR = 4 * CW / 32;                           // update rows per thread
     const int cl = lane % CW, hr = lane / CW;                 // column, row half
     const bool vec = ((reinterpret_cast<uintptr_t>(L) | reinterpret_cast<uintptr_t>(X)) & 15) == 0 &&
                      (ldl % EPC) == 0 && (ldx % EPC) == 0;
@@ -233,11 +233,12 @@ void launch_trsm_ops(const T *L, int64_t ldl, T *X, int64_t ldx, int w, int64_t 
     }
     // narrow ranges (a panel's columns): 16-column strips while twice the CTAs still fit one wave
     static const int sms = [] { int d = 0, v = 0; cudaGetDevice(&d); cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d); return v; }();
-    static const bool cw16_off = std::getenv("MP_TRSM_CW32") != nullptr;
-    const bool cw16 = !cw16_off && ceil_div(ncols, 16) <= std::min(96, sms);
-    const int cw = cw16 ? 16 : CWS;
+    static const int cwn = [] { const char *e = std::getenv("MP_TRSM_CW"); return e ? std::atoi(e) : 16; }();
+    int cw = CWS;
+    if (cwn == 8 && ceil_div(ncols, 8) <= std::min(96, sms)) cw = 8;
+    else if (cwn <= 16 && ceil_div(ncols, 16) <= std::min(96, sms)) cw = 16;
     const int grid = (int)ceil_div(ncols, cw);
-    auto kern = cw16 ? trsm_lower_unit_kernel<T, 16> : trsm_lower_unit_kernel<T, CWS>;
+    auto kern = cw == 8 ? trsm_lower_unit_kernel<T, 8> : cw == 16 ? trsm_lower_unit_kernel<T, 16> : trsm_lower_unit_kernel<T, CWS>;
     func_smem_once((const void *)kern, trsm_smem<T>(WMAX, cw));   // the largest request, set once per kernel
     if (w > (sizeof(T) == 4 ? 256 : 128)) sh = sl = nullptr;
     launch_ex(kern, dim3(grid), dim3(TW * 32), trsm_smem<T>(w, cw), s, nullptr, L, ldl, X, ldx, w, ncols, sh, sl, kp);
