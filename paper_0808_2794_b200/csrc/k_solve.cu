@@ -291,9 +291,10 @@ __device__ __forceinline__ void reduce_sub(T (&acc)[NP][R], int r0, int rstep, i
             }
 }
 
-// rsb = Y - F for block t (one warp)
+// rsb = Y - F for block t (one warp), several right-hand sides: rounds of 4 rows per lane (issuing
+// every round's loads at once measured slower for R = 16: register pressure)
 template <typename T, bool LOWER, int DN>
-__device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane, T *rsb)
+__device__ __forceinline__ void prep_rhs_rounds(const SweepArgs<T> &a, int t, int lane, T *rsb)
 {
     const int I = blk_of<LOWER>(t, a.nblk);
     const int64_t i0 = (int64_t)I * BS, n = a.n;
@@ -358,6 +359,69 @@ __device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane,
             const int idx = i0b + lane + 32 * u;
             if (idx < a.nrhs * BS) rsb[idx] = yv[u] - fv[u];
         }
+    }
+}
+
+// rsb = Y - F for block t (one warp).  One right-hand side: every load of the block is issued before
+// any is consumed (NU = BS / 32 per lane), one memory round trip per block; the tagged F words are
+// re-polled together until all carry the sweep's tag.
+template <typename T, bool LOWER, int DN, int R>
+__device__ __forceinline__ void prep_rhs(const SweepArgs<T> &a, int t, int lane, T *rsb)
+{
+    if constexpr (R > 1) {
+        prep_rhs_rounds<T, LOWER, DN>(a, t, lane, rsb);
+        return;
+    }
+    constexpr int NU = R * BS / 32;
+    const int I = blk_of<LOWER>(t, a.nblk);
+    const int64_t i0 = (int64_t)I * BS, n = a.n;
+    const int nr = (int)((n - i0 < (int64_t)BS) ? (n - i0) : (int64_t)BS);
+    const bool far = t >= DN + 1;
+    const int tot = a.nrhs * BS;
+#ifdef MP_SOLVE_TRACE
+    if (lane == 0 && t < 4096) g_strace[t][4] = (unsigned long long)clock64();
+#endif
+    T yv[NU], fv[NU];
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int idx = lane + 32 * u, c = idx / BS, r = idx - c * BS;
+        yv[u] = (idx < tot && r < nr) ? a.Y[(int64_t)c * n + i0 + r] : T(0);
+        fv[u] = T(0);
+    }
+    bool tagged = false;
+    if constexpr (sizeof(T) == 4) tagged = a.tF != nullptr;
+    if (far && tagged) {
+        if constexpr (sizeof(T) == 4) {
+            for (;;) {
+                bool ok = true;
+#pragma unroll
+                for (int u = 0; u < NU; ++u) {
+                    const int idx = lane + 32 * u, c = idx / BS, r = idx - c * BS;
+                    if (idx < tot && r < nr) {
+                        const unsigned long long w = ld_tag(a.tF + (int64_t)c * n + i0 + r);
+                        fv[u] = __uint_as_float((unsigned)w);
+                        ok &= (unsigned)(w >> 32) == a.tag;
+                    }
+                }
+                if (__all_sync(0xffffffffu, ok)) break;
+            }
+        }
+    } else if (far) {
+        if (lane == 0) spin_until(a.fflag + I, a.epoch);
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < NU; ++u) {
+            const int idx = lane + 32 * u, c = idx / BS, r = idx - c * BS;
+            if (idx < tot && r < nr) fv[u] = __ldcg(a.F + (int64_t)c * n + i0 + r);
+        }
+    }
+#ifdef MP_SOLVE_TRACE
+    if (lane == 0 && t < 4096) g_strace[t][5] = (unsigned long long)clock64();
+#endif
+#pragma unroll
+    for (int u = 0; u < NU; ++u) {
+        const int idx = lane + 32 * u;
+        if (idx < tot) rsb[idx] = yv[u] - fv[u];
     }
 }
 
@@ -525,7 +589,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
             }
             return;
         }
-        if (warp == WPREP) prep_rhs<T, LOWER, DN>(a, 0, lane, rs);
+        if (warp == WPREP) prep_rhs<T, LOWER, DN, R>(a, 0, lane, rs);
         nbar_sync(1, NCH);
         if constexpr (INV) {
             // ---------------- inverted-diagonal-block chain (reading A-19):
@@ -690,7 +754,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     if (t + 1 < nblk) {
                         double xv[XR];
                         prep_x_load(t + 1, xv);
-                        prep_rhs<T, LOWER, DN>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
+                        prep_rhs<T, LOWER, DN, R>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
                         prep_x_store(t + 1, xv);
                         __syncwarp();
 #ifdef MP_SOLVE_TRACE
@@ -788,7 +852,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                     st_release_u32(a.yflag + I, a.epoch);
                 }
             } else if (warp == WPREP) {
-                if (t + 1 < nblk) prep_rhs<T, LOWER, DN>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
+                if (t + 1 < nblk) prep_rhs<T, LOWER, DN, R>(a, t + 1, lane, rs + (size_t)((t + 1) & 1) * R * BS);
             } else if (split && warp >= NCW / 2 && warp < NCW && t + 1 < nblk) {
                 // next block's near tiles d = 2..DN (their y blocks are all solved)
                 const int lt = tid - (NCW / 2) * 32;          // 0..127: rows (lt>>3) + 16p, cols (lt&7)*4 + 32m

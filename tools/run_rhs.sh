@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+timeout 600 python tools/probe_rhs.py 2>&1 | tail -3
+MP_SOLVE_FLAGS=1 timeout 600 python tools/probe_rhs.py 2>&1 | tail -3
