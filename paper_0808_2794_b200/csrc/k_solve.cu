@@ -1068,16 +1068,19 @@ template <typename T, bool LOWER>
 void launch_sweep(const CUtensorMap &tm, const CUtensorMap &tD, const CUtensorMap &tM, bool inv, SweepArgs<T> &a,
                   int grid, cudaStream_t s)
 {
-    // right-hand sides per launch: 1, up to 4, up to MAXR (the per-block chain work scales with R)
-    const int rk = a.nrhs == 1 ? 0 : a.nrhs <= 4 ? 1 : 2;
-    void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, SweepArgs<T>) =
-        rk == 0 ? tri_sweep_kernel<T, LOWER, 1, false>
-                : rk == 1 ? tri_sweep_kernel<T, LOWER, 4, false> : tri_sweep_kernel<T, LOWER, MAXR, false>;
-    if constexpr (sizeof(T) == 4)
-        if (inv)
-            kern = rk == 0 ? tri_sweep_kernel<T, LOWER, 1, true>
-                           : rk == 1 ? tri_sweep_kernel<T, LOWER, 4, true> : tri_sweep_kernel<T, LOWER, MAXR, true>;
-    const size_t smem = rk == 0 ? sweep_smem<T, 1>() : rk == 1 ? sweep_smem<T, 4>() : sweep_smem<T, MAXR>();
+    // right-hand sides per launch: 1, up to 4, up to 8, up to MAXR (the per-block chain work scales with R)
+    const int rk = a.nrhs == 1 ? 0 : a.nrhs <= 4 ? 1 : a.nrhs <= 8 ? 2 : 3;
+    using KFn = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, SweepArgs<T>);
+    const KFn sub[4] = {tri_sweep_kernel<T, LOWER, 1, false>, tri_sweep_kernel<T, LOWER, 4, false>,
+                        tri_sweep_kernel<T, LOWER, 8, false>, tri_sweep_kernel<T, LOWER, MAXR, false>};
+    KFn kern = sub[rk];
+    if constexpr (sizeof(T) == 4) {
+        const KFn ik[4] = {tri_sweep_kernel<T, LOWER, 1, true>, tri_sweep_kernel<T, LOWER, 4, true>,
+                           tri_sweep_kernel<T, LOWER, 8, true>, tri_sweep_kernel<T, LOWER, MAXR, true>};
+        if (inv) kern = ik[rk];
+    }
+    const size_t sm[4] = {sweep_smem<T, 1>(), sweep_smem<T, 4>(), sweep_smem<T, 8>(), sweep_smem<T, MAXR>()};
+    const size_t smem = sm[rk];
     func_smem_once((const void *)kern, smem);
     void *args[] = {(void *)&tm, (void *)&tD, (void *)&tM, (void *)&a};
     MP_CUDA(cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(NTH), args, smem, s));

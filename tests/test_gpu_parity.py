@@ -161,9 +161,10 @@ def test_solve_inv_vs_substitution(mp, orc, n, nrhs, seed):
     assert certificate_ok(A, Xi, B) and certificate_ok(A, Xs, B)
 
 
-@pytest.mark.parametrize("n,nrhs,seed", [(700, 20, 61), (1100, 33, 62)])
+@pytest.mark.parametrize("n,nrhs,seed", [(700, 20, 61), (1100, 33, 62), (600, 7, 63), (900, 2, 64)])
 def test_many_rhs(mp, orc, n, nrhs, seed):
-    """nrhs above one solve launch's 16 columns (chunked sweeps, multi-column residual)."""
+    """Several right-hand sides: the R = 4 / 8 / 16 sweep instantiations, and nrhs above one launch's
+    16 columns (chunked sweeps, multi-column residual)."""
     A, B, X = inputs.gaussian(n, nrhs=nrhs, seed=seed)
     ro = orc.dsgesv(A, B)
     Xg, it, info, rep = gpu_solve(mp, A, B)

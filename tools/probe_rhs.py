@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_0808_2794_b200 import binding as mp, inputs
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
-for nrhs in (1, 4, 16):
+for nrhs in (1, 4, 8, 16):
     A, B, _ = inputs.gaussian(n, nrhs=nrhs, seed=2794)
     dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
     for rep in range(2):
