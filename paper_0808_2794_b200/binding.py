@@ -102,22 +102,42 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
-def _ptr_ld(M, name: str, square: bool):
-    """Pointer and leading dimension of a column-major matrix (torch tensor or numpy array)."""
+def _ptr_ld(M, name: str, square: bool, need_ld: int | None = None):
+    """Pointer and leading dimension of a column-major float64 matrix (torch tensor or numpy array).
+
+    The C-ABI reads B and X with leading dimension n (include/mp_solve.h), so callers pass
+    ``need_ld=n`` for them: a row-sliced view (ld > n), a strided 1-D view or a non-float64
+    array is rejected instead of being read (or written) as if it were contiguous."""
     if _is_torch(M):
-        if M.dtype.is_floating_point and M.element_size() != 8:
-            raise TypeError(f"{name} must be float64")
+        import torch
+        if M.dtype != torch.float64:
+            raise TypeError(f"{name} must be float64 (got {M.dtype})")
         if M.dim() == 1:
-            return M.data_ptr(), M.shape[0]
-        if M.stride(0) != 1:
-            raise ValueError(f"{name} must be column-major (stride(0) == 1); use colmajor_cuda()")
-        return M.data_ptr(), max(M.stride(1), 1)
-    A = np.asarray(M)
-    if A.dtype != np.float64:
-        raise TypeError(f"{name} must be float64")
-    if A.ndim == 2 and not A.flags.f_contiguous:
-        raise ValueError(f"{name} must be Fortran-ordered")
-    return A.ctypes.data, A.shape[0]
+            if M.shape[0] > 1 and M.stride(0) != 1:
+                raise ValueError(f"{name}: a 1-D view must be contiguous (stride 1)")
+            ptr, ld = M.data_ptr(), max(M.shape[0], 1)
+        elif M.dim() == 2:
+            if M.shape[0] > 1 and M.shape[1] > 0 and M.stride(0) != 1:
+                raise ValueError(f"{name} must be column-major (stride(0) == 1); use colmajor_cuda()")
+            ptr, ld = M.data_ptr(), (M.stride(1) if M.shape[1] > 1 else max(M.shape[0], 1))
+        else:
+            raise ValueError(f"{name} must be 1-D or 2-D")
+    else:
+        A = np.asarray(M)
+        if A.dtype != np.float64:
+            raise TypeError(f"{name} must be float64 (got {A.dtype})")
+        if A.ndim == 1:
+            if not A.flags.c_contiguous:
+                raise ValueError(f"{name}: a 1-D array must be contiguous")
+        elif A.ndim == 2:
+            if not A.flags.f_contiguous:
+                raise ValueError(f"{name} must be Fortran-ordered (column-major, contiguous)")
+        else:
+            raise ValueError(f"{name} must be 1-D or 2-D")
+        ptr, ld = A.ctypes.data, max(A.shape[0], 1)
+    if need_ld is not None and ld != max(need_ld, 1):
+        raise ValueError(f"{name} must have leading dimension n = {need_ld} (got {ld}); pass a contiguous copy")
+    return ptr, ld
 
 
 def _stream_of(*ts):
@@ -155,8 +175,8 @@ def mp_dsgesv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
     if X is None:
         X = _alloc_like_X(B, n, nrhs)
     pa, lda = _ptr_ld(A, "A", True)
-    pb, _ = _ptr_ld(B, "B", False)
-    px, _ = _ptr_ld(X, "X", False)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
     lib.mp_set_stream(_stream_of(A, B, X))
     it, info = ctypes.c_int(0), ctypes.c_int(0)
     rep = Report() if report else None
@@ -177,8 +197,8 @@ def mp_dgesv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
     if X is None:
         X = _alloc_like_X(B, n, nrhs)
     pa, lda = _ptr_ld(A, "A", True)
-    pb, _ = _ptr_ld(B, "B", False)
-    px, _ = _ptr_ld(X, "X", False)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
     lib.mp_set_stream(_stream_of(A, B, X))
     info = ctypes.c_int(0)
     rep = Report() if report else None
@@ -285,8 +305,8 @@ def mp_dsgesv_1dbc_ex(comm, n: int, nb: int, A_local, B, X=None, opts: Opts | No
         X = _alloc_like_X(B, n, nrhs)
     nloc = A_local.shape[1] if len(A_local.shape) == 2 else 0
     pa, lda = _ptr_ld(A_local, "A_local", False) if nloc > 0 else (None, 1)
-    pb, _ = _ptr_ld(B, "B", False)
-    px, _ = _ptr_ld(X, "X", False)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
     lib.mp_set_stream(_stream_of(B, X))
     it, info = ctypes.c_int(0), ctypes.c_int(0)
     rep = Report() if report else None
@@ -302,8 +322,8 @@ def mp_dgesv_1dbc(comm, n: int, nb: int, A_local, B, X=None):
         X = _alloc_like_X(B, n, nrhs)
     nloc = A_local.shape[1] if len(A_local.shape) == 2 else 0
     pa, lda = _ptr_ld(A_local, "A_local", False) if nloc > 0 else (None, 1)
-    pb, _ = _ptr_ld(B, "B", False)
-    px, _ = _ptr_ld(X, "X", False)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
     lib.mp_set_stream(_stream_of(B, X))
     info = ctypes.c_int(0)
     _check(lib.mp_dgesv_1dbc(comm, n, nrhs, nb, pa, lda, pb, px, ctypes.byref(info)))

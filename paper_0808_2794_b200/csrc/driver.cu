@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <set>
@@ -153,12 +154,21 @@ static void prof_collect(mp_report *rep)
 namespace {
 
 // ------------------------------------------------------------------ memory
+cudaMemPool_t library_pool();
+
 struct Pool {
     cudaStream_t s;
     std::vector<void *> ptrs;
     int64_t bytes = 0;
     explicit Pool(cudaStream_t st) : s(st) {}
-    ~Pool() { release(); }
+    const int exc_at_ctor = std::uncaught_exceptions();
+    ~Pool()
+    {
+        // unwinding from an error: work queued earlier on the look-ahead panel / update streams
+        // may still use these buffers; wait for the device before handing them back
+        if (std::uncaught_exceptions() > exc_at_ctor) cudaDeviceSynchronize();
+        release();
+    }
     void release() {
         for (void *p : ptrs) cudaFreeAsync(p, s);
         ptrs.clear();
@@ -168,7 +178,7 @@ struct Pool {
         if (count == 0) count = 1;
         void *p = nullptr;
         const size_t b = round_up((int64_t)(count * sizeof(T)), 256);
-        cudaError_t e = cudaMallocAsync(&p, b, s);
+        cudaError_t e = cudaMallocFromPoolAsync(&p, b, library_pool(), s);
         if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); throw NoMem{}; }
         MP_CUDA(e);
         ptrs.push_back(p);
@@ -177,17 +187,42 @@ struct Pool {
     }
 };
 
-void configure_mempool_once()
+// The library's own stream-ordered memory pool (one per device), kept warm between calls
+// (release threshold = max) without touching the device's default pool, which other
+// cudaMallocAsync users in the host process own.
+cudaMemPool_t library_pool()
 {
-    static thread_local int done_dev = -1;
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
     int dev = 0;
     MP_CUDA(cudaGetDevice(&dev));
-    if (done_dev == dev) return;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props;
+    std::memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
     cudaMemPool_t pool;
-    MP_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-    uint64_t thr = UINT64_MAX;                 // keep freed workspace cached between calls
+    MP_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t thr = UINT64_MAX;
     MP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    done_dev = dev;
+    pools.emplace(dev, pool);
+    return pool;
+}
+
+// Size limits of the leaf cluster (one panel column fits one thread-block cluster) and of the
+// triangular-solve helper grid, for both precisions (the binary64 fallback may run): checked
+// before any allocation or launch, so an unsupported n fails without queued work.
+void check_size_limits(int64_t n)
+{
+    if (n <= 0) return;
+    if (panel_leaf_width<float>(n) <= 0 || panel_leaf_width<double>(n) <= 0)
+        throw std::runtime_error("n exceeds the rows one panel cluster holds on this device");
+    if (!solve_fits<float>(n) || !solve_fits<double>(n))
+        throw std::runtime_error("n exceeds the triangular-solve helper grid");
 }
 
 bool is_device_ptr(const void *p)
@@ -748,8 +783,8 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
     if (o.variant != MP_VARIANT_FFMA && o.variant != MP_VARIANT_3XTF32) throw std::runtime_error("unknown variant");
     const int64_t n = a.n, nrhs = a.nrhs;
+    check_size_limits(n);
     cudaStream_t s = g_stream;
-    configure_mempool_once();
     g_launches = 0;
     g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
     g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
@@ -881,8 +916,8 @@ int dgesv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
     mp_default_opts(&o);
     if (opts) o = *opts;
     const int nb = o.nb > 0 ? o.nb : default_nb(a.n);
+    check_size_limits(a.n);
     cudaStream_t s = g_stream;
-    configure_mempool_once();
     g_launches = 0;
     g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
     g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
@@ -932,8 +967,8 @@ int getrf_impl(int64_t n, const double *A, int64_t lda, T *LU, int32_t *ipiv_out
     mp_default_opts(&o);
     if (opts) o = *opts;
     const int nb = o.nb > 0 ? o.nb : default_nb(n);
+    check_size_limits(n);
     cudaStream_t s = g_stream;
-    configure_mempool_once();
     g_launches = 0;
     Pool pool(s);
     Args a{n, 0, lda, A, nullptr, nullptr};
@@ -1294,8 +1329,8 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
     mp_default_opts(&o);
     if (opts) o = *opts;
     const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    check_size_limits(n);
     cudaStream_t s = g_stream;
-    configure_mempool_once();
     g_launches = 0;
     g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
     g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
@@ -1519,7 +1554,7 @@ int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_
         if (variant == MP_VARIANT_3XTF32) {
             float *scratch = nullptr;
             const size_t bytes = ((size_t)2 * M * round_up(K, 4) + (size_t)2 * N * round_up(K, 4) + 4096) * 4;
-            MP_CUDA(cudaMallocAsync((void **)&scratch, bytes, s));
+            MP_CUDA(cudaMallocFromPoolAsync((void **)&scratch, bytes, library_pool(), s));
             launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, num_sms(), s);
             MP_CUDA(cudaFreeAsync(scratch, s));
         } else {

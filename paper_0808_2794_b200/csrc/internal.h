@@ -145,6 +145,9 @@ struct PanelScratch {
 // Widest leaf one thread-block cluster can hold for m = n - c0 rows (0: too tall).
 template <typename T>
 int panel_leaf_width(int64_t m);
+// whether the triangular-solve helper grid covers n (checked up front by the drivers)
+template <typename T>
+bool solve_fits(int64_t n);
 // Factor the leaf rows [c0, n) x columns [c0, c0+w) of W in place (GEPP, binary T).
 // Writes ipiv[c0 .. c0+w) (0-based global rows), updates ps.orig for the rows,
 // and emits the leaf's (position <- position-at-leaf-start) pairs.

@@ -1262,6 +1262,23 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     }
 }
 
+template <typename T>
+bool solve_fits(int64_t n)
+{
+    // the same helper-grid arithmetic as launch_lu_solve, checked before any launch
+    const int nblk = (int)ceil_div(n, BS);
+    int dev = 0, sms = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    MP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int dnmin = std::min(sweep_dn<T, 1>(), sweep_dn<T, MAXR>());
+    static const int hmax = [] { const char *e = std::getenv("MP_SOLVE_HELPERS"); return e ? std::atoi(e) : 0; }();
+    const int hcap = hmax > 0 ? std::min(hmax, sms - 1) : sms - 1;
+    const int helpers = std::max(1, std::min(hcap, nblk - dnmin - 1));
+    return ceil_div(std::max(0, nblk - dnmin - 1), helpers) <= SCfg<T>::MAXOWN;
+}
+
+template bool solve_fits<float>(int64_t);
+template bool solve_fits<double>(int64_t);
 template void launch_lu_solve<float>(const float *, int64_t, int64_t, int64_t, float *, double *, int,
                                      SolveScratch &, cudaStream_t, const float *);
 template void launch_lu_solve<double>(const double *, int64_t, int64_t, int64_t, double *, double *, int,

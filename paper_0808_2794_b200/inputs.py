@@ -98,3 +98,45 @@ def small_integer_system(n: int, seed: int, lo: int = -3, hi: int = 3):
     A = np.asfortranarray(r.integers(lo, hi + 1, size=(n, n)).astype(np.float64))
     b = np.asfortranarray(r.integers(lo, hi + 1, size=(n, 1)).astype(np.float64))
     return A, b
+
+
+def exact_lu_device(n: int, nrhs: int = 1, seed: int = BASE_SEED, density: float = 0.5, device="cuda"):
+    """P2 family drawn on the GPU (torch generator) for the full-size configs (C3 16384, C4 49152),
+    where the host construction would take minutes.  Same recipe as ``exact_lu``; different bytes.
+
+    L U is formed in binary32 with TF32 disabled: every entry of L is in {0, +-1/4, +-1/2} and U is
+    integer in [-8, 8], so every partial sum is a multiple of 1/4 far below 2^22 and the product is
+    exact in any summation order.  Returns torch CUDA tensors
+    (A column-major float64 (n, n) stride (1, n), B, X (n, nrhs) stride (1, n), perm int64, L, U float32
+    row-major) with A[perm[t], :] = (L U)[t, :].
+    """
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    s = torch.randint(0, 4, (n, n), device=device, generator=g, dtype=torch.uint8).to(torch.float32)
+    L = (s >= 2).to(torch.float32).add_(1.0).mul_(0.25)          # |l| in {1/4, 1/2}
+    L.mul_(torch.remainder(s, 2).mul_(-2.0).add_(1.0))           # random sign
+    del s
+    L.mul_(torch.rand((n, n), device=device, generator=g) < density)
+    L.tril_(-1)
+    L.diagonal().fill_(1.0)
+    U = torch.randint(-8, 9, (n, n), device=device, generator=g, dtype=torch.int8).to(torch.float32)
+    U.triu_(1)
+    vals_d = torch.tensor([1.0, -1.0, 2.0, -2.0, 4.0, -4.0], device=device)
+    U.diagonal().copy_(vals_d[torch.randint(0, 6, (n,), device=device, generator=g)])
+    perm = torch.randperm(n, device=device, generator=g)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        Mt = U.t() @ L.t()                  # (L U)^T, row-major: Mt[j, t] = (L U)[t, j]
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    At = torch.empty((n, n), dtype=torch.float64, device=device)
+    At[:, perm] = Mt.to(torch.float64)      # At[j, perm[t]] = (L U)[t, j]  ->  A = At^T column-major
+    del Mt
+    A = At.t()
+    Xt = (torch.randint(-4, 5, (nrhs, n), device=device, generator=g).to(torch.float64) / 4.0)
+    X = Xt.t()
+    Bt = (Xt @ At)                           # B^T = X^T A^T, exact (dyadic, < 2^53)
+    B = Bt.t()
+    return A, B, X, perm, L, U

@@ -83,3 +83,25 @@ def test_sass_is_sm100a(binding):
     exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
     out = subprocess.run([exe, "--list-elf", binding.LIB_PATH], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_binding_rejects_bad_layouts(binding):
+    """B / X must have leading dimension n and be float64 (include/mp_solve.h); views that the
+    C-ABI would misread are rejected before any call."""
+    import torch
+    n = 8
+    A = torch.zeros((n, n), dtype=torch.float64).t()              # column-major
+    big = torch.zeros((3, n + 4), dtype=torch.float64).t()         # (n+4, 3) stride (1, n+4)
+    with pytest.raises(ValueError):
+        binding._ptr_ld(big[:n], "B", False, n)                    # row-sliced: ld = n + 4 != n
+    with pytest.raises(ValueError):
+        binding._ptr_ld(torch.zeros(2 * n, dtype=torch.float64)[::2], "B", False, n)   # strided 1-D
+    with pytest.raises(TypeError):
+        binding._ptr_ld(torch.zeros((n, 1), dtype=torch.int64), "B", False, n)
+    with pytest.raises(TypeError):
+        binding._ptr_ld(np.zeros((n, 1), dtype=np.float32), "X", False, n)
+    with pytest.raises(ValueError):
+        binding._ptr_ld(np.zeros((n, 3)), "X", False, n)           # C-ordered 2-D
+    assert binding._ptr_ld(A, "A", True)[1] == n
+    assert binding._ptr_ld(torch.zeros((2, n), dtype=torch.float64).t(), "B", False, n)[1] == n
+    assert binding._ptr_ld(np.zeros(n), "B", False, n)[1] == n

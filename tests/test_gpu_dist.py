@@ -119,3 +119,35 @@ def test_dist_ffma_variant(mp):
     for Xg, it, info in res:
         assert info == 0 and abs(it - ro.iters) <= 1
     assert certificate_ok(A, res[0][0], B)
+
+
+def test_nccl_p1_communicator(mp):
+    """The NCCL data plane on hardware: a real NCCL communicator of one rank (the driver's boxes
+    have one GPU) runs mp_dsgesv_1dbc / mp_dgesv_1dbc, so NcclComm::bcast / allreduce / allgather
+    execute through libnccl (a P = 1 broadcast / all-reduce / all-gather is still a real NCCL
+    kernel on the stream).  Results against the oracle, and bitwise equal to the loopback P = 1
+    run of the same algorithm."""
+    import torch
+    n, nb = 1100, 128
+    A, B, Xt = inputs.gaussian(n, nrhs=2, seed=17)
+    ro = orc_mod.dsgesv(A, B)
+    uid = mp.mp_get_unique_id()
+    comm = mp.mp_comm_init(1, 0, uid)
+    try:
+        dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
+        X, it, info, rep = mp.mp_dsgesv_1dbc_ex(comm, n, nb, dA, dB)
+        torch.cuda.synchronize()
+        Xn = X.cpu().numpy()
+        X64, info64 = mp.mp_dgesv_1dbc(comm, n, nb, dA, dB)
+        torch.cuda.synchronize()
+        X64 = X64.cpu().numpy()
+    finally:
+        mp.mp_comm_destroy(comm)
+    assert info == ro.info == 0 and abs(it - ro.iters) <= 1, (it, ro.iters)
+    assert certificate_ok(A, Xn, B)
+    Xl, itl, infol = run_dist(mp, A, B, 1, nb)[0]
+    assert (itl, infol) == (it, info) and np.array_equal(Xl, Xn)
+    Xo, infoo = orc_mod.dgesv(A, B)
+    kappa = np.linalg.cond(A)
+    assert info64 == infoo == 0
+    assert np.abs(X64 - Xo).max() / np.abs(Xo).max() <= 8 * n * kappa * 2.0 ** -53
