@@ -67,6 +67,7 @@ lib.mp_dgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Op
 lib.mp_sgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_dgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_kernel_schur_update.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
+lib.mp_kernel_schur_update_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_set_stream.argtypes = [_p]
 lib.mp_profile_collect.argtypes = [ctypes.POINTER(Report)]
 lib.mp_last_error.restype = ctypes.c_char_p
@@ -85,6 +86,7 @@ lib.mp_dgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi]
 
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
+            "mp_kernel_schur_update_f64",
             "mp_profile_collect", "mp_exec_info", "mp_get_unique_id", "mp_comm_init", "mp_comm_init_loopback",
             "mp_comm_destroy", "mp_1dbc_local_cols", "mp_dsgesv_1dbc", "mp_dsgesv_1dbc_ex", "mp_dgesv_1dbc")
 
@@ -240,6 +242,17 @@ def mp_kernel_schur_update(W, r0: int, c0: int, k0: int, M: int, N: int, K: int,
         raise TypeError("W must be a row-major float32 CUDA tensor")
     lib.mp_set_stream(_stream_of(W))
     _check(lib.mp_kernel_schur_update(W.data_ptr(), W.stride(0), r0, c0, k0, M, N, K, variant))
+
+
+MP_F64_AUTO, MP_F64_DMMA, MP_F64_DFMA = 0, 1, 2
+
+
+def mp_kernel_schur_update_f64(W, r0: int, c0: int, k0: int, M: int, N: int, K: int, pipe: int = MP_F64_AUTO):
+    """The binary64 trailing update alone on a row-major float64 CUDA tensor W (in place)."""
+    if not (_is_torch(W) and W.is_cuda and W.element_size() == 8 and W.stride(1) == 1):
+        raise TypeError("W must be a row-major float64 CUDA tensor")
+    lib.mp_set_stream(_stream_of(W))
+    _check(lib.mp_kernel_schur_update_f64(W.data_ptr(), W.stride(0), r0, c0, k0, M, N, K, pipe))
 
 
 def mp_profile_collect() -> Report:

@@ -1565,6 +1565,26 @@ int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_
     });
 }
 
+int mp_kernel_schur_update_f64(double *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
+                               int64_t K, int pipe)
+{
+    return guarded([&] {
+        cudaStream_t s = g_stream;
+        const double *A = W + r0 * ldw + k0, *B = W + k0 * ldw + c0;
+        double *C = W + r0 * ldw + c0;
+        if (pipe == MP_F64_DMMA) {
+            if (!launch_dgemm_dmma(A, ldw, B, ldw, C, ldw, M, N, K, s))
+                throw std::runtime_error("DMMA update: N, K and the row starts must be even");
+        } else if (pipe == MP_F64_DFMA) {
+            launch_dgemm_dfma(A, ldw, B, ldw, C, ldw, M, N, K, s);
+        } else {
+            launch_gemm_update<double>(W, ldw, r0, c0, k0, M, N, K, s);
+        }
+        MP_CUDA(cudaStreamSynchronize(s));
+        return MP_OK;
+    });
+}
+
 int mp_profile_collect(mp_report *rep)
 {
     return guarded([&] {

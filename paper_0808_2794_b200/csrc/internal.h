@@ -194,6 +194,12 @@ void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, i
                         int64_t K, cudaStream_t s);
 
 // Same update with separate row-major operands: C[M x N] -= A[M x K] * B[K x N] (lda, ldb, ldc).
+// binary64 trailing update on the FP64 tensor pipe (DMMA, k_gemm_f64.cu); false = shape or
+// alignment not supported (the caller uses the DFMA tile kernel)
+void launch_dgemm_dfma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, cudaStream_t s);
+bool launch_dgemm_dmma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, cudaStream_t s);
 template <typename T>
 void launch_gemm_ops(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
                      int64_t K, cudaStream_t s);

@@ -504,6 +504,16 @@ void launch_gemm_ops<double>(const double *A, int64_t lda, const double *B, int6
     if (M <= 0 || N <= 0 || K <= 0) return;
     if (K <= 128 && N <= 32) return launch_ts<double, 32, 32>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (K <= 128 && N <= 64) return launch_ts<double, 32, 64>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    static const bool no_dmma = std::getenv("MP_NO_DMMA") != nullptr;   // A/B: the DFMA tile kernel
+    if (!no_dmma && launch_dgemm_dmma(A, lda, B, ldb, C, ldc, M, N, K, s)) return;
+    launch_tiles<double, 128, 64, 8, 8, 4>(A, lda, B, ldb, C, ldc, M, N, K, s);
+}
+
+// the binary64 DFMA tile kernel alone (kernel tests / A-B against DMMA)
+void launch_dgemm_dfma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
+                       int64_t M, int64_t N, int64_t K, cudaStream_t s)
+{
+    if (M <= 0 || N <= 0 || K <= 0) return;
     launch_tiles<double, 128, 64, 8, 8, 4>(A, lda, B, ldb, C, ldc, M, N, K, s);
 }
 

@@ -69,3 +69,53 @@ def test_schur_update_gaussian_accuracy(mp, variant):
     assert err.max() <= K * 2.0 ** -24 * 4, err.max()
     # untouched regions stay bitwise
     assert np.array_equal(got[:r0], W0[:r0]) and np.array_equal(got[:, :c0], W0[:, :c0])
+
+
+# --------------------------------------------------------------------------- binary64 update (FP64 path)
+def run64(mp, W0, r0, c0, k0, M, N, K, pipe):
+    import torch
+    W = torch.from_numpy(W0.copy()).cuda()
+    mp.mp_kernel_schur_update_f64(W, r0, c0, k0, M, N, K, pipe)
+    torch.cuda.synchronize()
+    return W.cpu().numpy()
+
+
+SHAPES64 = [(64, 64, 0, 256, 128, 64), (300, 200, 8, 512, 334, 32), (1000, 700, 16, 1400, 1200, 256),
+            (513, 130, 40, 700, 700, 200), (2048, 2048, 256, 2304, 2304, 256), (333, 257, 3, 600, 600, 61)]
+
+
+@pytest.mark.parametrize("pipe", [0, 1, 2])
+@pytest.mark.parametrize("shape", SHAPES64)
+def test_schur_update_f64_exact_integers(mp, pipe, shape):
+    """Integers: every product and partial sum is exact in binary64, so any order gives the same bits.
+    pipe 1 (DMMA) needs even N, K and row starts: the odd last shape must be refused; pipe 0
+    (the library's routing) falls back to the DFMA kernel there."""
+    M, N, k0, rows, cols, K = shape
+    rng = np.random.default_rng(M + N + K + 1)
+    ldw = ((cols + 63) // 64) * 64
+    W0 = rng.integers(-64, 65, size=(rows, ldw)).astype(np.float64)
+    r0, c0 = k0 + K, k0 + K
+    M, N = min(M, rows - r0), min(N, cols - c0)
+    if pipe == 1 and (N % 2 or K % 2 or k0 % 2 or c0 % 2):
+        with pytest.raises(mp.MpError):
+            run64(mp, W0, r0, c0, k0, M, N, K, pipe)
+        return
+    got = run64(mp, W0, r0, c0, k0, M, N, K, pipe)
+    ref = reference(W0, r0, c0, k0, M, N, K)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("pipe", [1, 2])
+def test_schur_update_f64_gaussian_accuracy(mp, pipe):
+    rng = np.random.default_rng(6)
+    rows = cols = 1536
+    W0 = rng.standard_normal((rows, cols))
+    k0, K = 256, 256
+    r0 = c0 = k0 + K
+    M, N = rows - r0, cols - c0
+    got = run64(mp, W0, r0, c0, k0, M, N, K, pipe)
+    exact = W0[r0:, c0:].astype(np.longdouble) - W0[r0:, k0:k0 + K].astype(np.longdouble) @ W0[k0:k0 + K, c0:].astype(np.longdouble)
+    scale = np.abs(W0[r0:, k0:k0 + K]) @ np.abs(W0[k0:k0 + K, c0:]) + np.abs(W0[r0:, c0:])
+    err = np.abs(got[r0:, c0:] - np.asarray(exact, np.float64)) / scale
+    assert err.max() <= (K + 1) * 2.0 ** -53, err.max()         # binary64 accumulation bound
+    assert np.array_equal(got[:r0], W0[:r0]) and np.array_equal(got[:, :c0], W0[:, :c0])
