@@ -141,7 +141,7 @@ def run_reference(args, rank, world):
     v = flops(n_cpu) / t / 1e9
     out = {"metric": METRIC, "value": round(v, 3), "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic", "impl": "reference",
+           "vs_baseline": None, "dtype": "f32+f64 (CPU oracle: plain binary32 GEPP)", "data": "synthetic", "impl": "reference",
            "config": {"workload": WORKLOAD, "n": args.n, "nrhs": 1, "sample_n": n_cpu},
            "cpu_baseline": {"value": round(v, 3), "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
                             "sample": f"one full oracle_dsgesv solve per step at n={n_cpu} (same generator), "
@@ -263,7 +263,7 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
         iters = [r[0] for r in reps]
         out = {"metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64",
+               "scaling": "strong", "vs_baseline": None, "dtype": dtype_label(args.variant),
                "data": "synthetic (per-block seeded N(0,1) columns, x_true U[-1,1], b = A x_true)",
                "config": {"workload": WORKLOAD, "n": n, "nrhs": nrhs, "nb": nb, "variant": args.variant,
                           "iters": iters, "l2": "inputs larger than L2",
@@ -293,7 +293,156 @@ def _gemm_traffic():
             "ratio": d["traffic_over_algorithmic"], "launch": "M=N=%d K=%d (%s)" % (d["M"], d["K"], os.path.basename(p))}
 
 
+def dtype_label(variant: str) -> str:
+    """The arithmetic the path computes in: binary32 LU (its O(n^3) update on 3xTF32 tcgen05 tensor
+    cores, or FP32 FFMA), binary64 residual / update / test."""
+    return "f32 LU (3xtf32 tcgen05 update) + f64 refinement" if variant == "3xtf32" else \
+        "f32 LU (ffma update) + f64 refinement"
+
+
+FP64_PEAK_TF = 37.1   # measured: DFMA 36.9 / DMMA m8n8k4 37.1 TF/s on this pool's B200 (profiles/r02_ubench_fp64_peaks.txt)
+
+
+def cusolver_context(dA, dB, reps: int = 2):
+    """T3's "full double precision solve (reference time)" from the vendor library, for
+    context only: cuSOLVER dgetrf + dgetrs through torch.linalg — never on the product path."""
+    import torch
+    Ac, Bc = dA.contiguous(), dB.contiguous()
+    torch.linalg.lu_solve(*torch.linalg.lu_factor(Ac), Bc)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        LU, piv = torch.linalg.lu_factor(Ac)
+        torch.linalg.lu_solve(LU, piv, Bc)
+    e1.record()
+    torch.cuda.synchronize()
+    del Ac
+    return e0.elapsed_time(e1) / reps
+
+
+def fp64_roofline(mp, dA, dB, nb):
+    """One instrumented binary64 solve: its trailing update (DMMA) against the measured FP64 peak."""
+    import torch
+    _, info, rep = mp.mp_dgesv_ex(dA, dB, None, mp.make_opts(nb=nb, flags=2))
+    torch.cuda.synchronize()
+    k = rep.kernels().get("trail")
+    if not k or k["ms"] <= 0:
+        return None
+    ach = k["work"] / (k["ms"] / 1e3) / 1e12
+    la, sp, su = mp.mp_exec_info()
+    return {"kernel": "binary64 trailing update (DMMA mma.sync m8n8k4 f64)", "bound": "fp64 pipe",
+            "achieved": round(ach, 2), "peak": FP64_PEAK_TF, "unit": "TFLOP/s", "frac": round(ach / FP64_PEAK_TF, 4),
+            "sms": su if la else 148, "frac_of_partition": round(ach / (FP64_PEAK_TF * (su if la else 148) / 148), 4),
+            "peak_source": "measured, tools/ubench_fp64.cu"}
+
+
+def time_solves(mp, dA, dB, opts, steps, fp64=False):
+    import torch
+    if fp64:
+        mp.mp_dgesv_ex(dA, dB, None, opts, report=False)
+    else:
+        mp.mp_dsgesv_ex(dA, dB, None, opts, report=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its = []
+    e0.record()
+    for _ in range(steps):
+        if fp64:
+            _, info, _ = mp.mp_dgesv_ex(dA, dB, None, opts, report=False)
+            its.append(info)
+        else:
+            _, it, info, _ = mp.mp_dsgesv_ex(dA, dB, None, opts, report=False)
+            its.append(it)
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, its
+
+
+def other_configs(mp, args, dev):
+    """BASELINE.json's other configs (B:7-B:11), one or two solves each, reported beside the headline:
+    C3 with the FFMA variant, C2, C4 (n = 49152, nrhs = 16, device-generated), C5 (kappa sweep)."""
+    import torch
+    res = {}
+    # C3, FFMA variant (K5a), on the headline inputs
+    A, B, _ = inputs.gaussian(args.n, nrhs=1, seed=inputs.BASE_SEED)
+    dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
+    ms, its = time_solves(mp, dA, dB, mp.make_opts(variant=mp.MP_VARIANT_FFMA), 2)
+    _, _, _, rep = mp.mp_dsgesv_ex(dA, dB, None, mp.make_opts(variant=mp.MP_VARIANT_FFMA, flags=2))
+    torch.cuda.synchronize()
+    t = rep.kernels().get("trail", {"ms": 0, "work": 0})
+    ffma_peak = 148 * 128 * 2 * peaks()[0].get("sm_max_mhz", 1965.0) * 1e6 / 1e12
+    ach = t["work"] / (t["ms"] / 1e3) / 1e12 if t["ms"] else None
+    res["C3_ffma"] = {"n": args.n, "variant": "ffma", "ms": round(ms, 3), "gflops": round(flops(args.n) / ms / 1e6, 1),
+                      "iters": its, "trail_tflops": round(ach, 2) if ach else None,
+                      "trail_frac_of_ffma_peak": round(ach / ffma_peak, 4) if ach else None,
+                      "ffma_peak_tflops": round(ffma_peak, 1)}
+    del dA, dB
+    log("C2")
+    # C2: n = 4096, nb = 128
+    A, B, _ = inputs.gaussian(4096, nrhs=1, seed=inputs.BASE_SEED)
+    dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
+    ms, its = time_solves(mp, dA, dB, mp.make_opts(nb=128), 5)
+    ms64, _ = time_solves(mp, dA, dB, mp.make_opts(nb=128), 3, fp64=True)
+    res["C2"] = {"n": 4096, "nb": 128, "ms": round(ms, 3), "gflops": round(flops(4096) / ms / 1e6, 1), "iters": its,
+                 "fp64_ms": round(ms64, 3), "speedup_vs_fp64": round(ms64 / ms, 3)}
+    log("C1")
+    # C1: n = 512 (the paper: small n loses, P:426-430)
+    A, B, _ = inputs.gaussian(512, nrhs=1, seed=inputs.BASE_SEED)
+    dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
+    ms, its = time_solves(mp, dA, dB, mp.make_opts(nb=64), 10)
+    ms64, _ = time_solves(mp, dA, dB, mp.make_opts(nb=64), 10, fp64=True)
+    res["C1"] = {"n": 512, "nb": 64, "ms": round(ms, 3), "iters": its, "fp64_ms": round(ms64, 3),
+                 "speedup_vs_fp64": round(ms64 / ms, 3)}
+    log("C5")
+    # C5: n = 8192, A = U diag(sigma) V^T, U, V from QR of Gaussian matrices (generated on the GPU here)
+    n5 = 8192
+    g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED + 2)
+    U, _ = torch.linalg.qr(torch.randn((n5, n5), dtype=torch.float64, device=dev, generator=g))
+    V, _ = torch.linalg.qr(torch.randn((n5, n5), dtype=torch.float64, device=dev, generator=g))
+    xt = (torch.rand((1, n5), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+    c5 = []
+    for kappa in (1e2, 1e4, 1e6, 1e8, 1e10):
+        sig = kappa ** (-torch.arange(n5, dtype=torch.float64, device=dev) / (n5 - 1))
+        Ak = ((U * sig[None, :]) @ V.t()).t().contiguous().t()       # column-major
+        Bk = (Ak @ xt).t().contiguous().t()
+        ms, its = time_solves(mp, Ak, Bk, mp.make_opts(), 2)
+        c5.append({"kappa": kappa, "iters": its[0], "ms": round(ms, 3)})
+        del Ak, Bk
+    res["C5"] = {"n": n5, "sweep": c5, "note": "iters -31 = no convergence in 30 corrections, binary64 fallback "
+                                                "(time includes the wasted refinement)"}
+    del U, V
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    log("C4")
+    # C4: n = 49152, nrhs = 16 (A = 19.3 GB fp64), device-generated with a seeded torch generator
+    if not args.no_c4:
+        n4, r4 = 49152, 16
+        g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED)
+        dA = torch.randn((n4, n4), dtype=torch.float64, device=dev, generator=g).t()
+        Xt = (torch.rand((r4, n4), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+        dB = (dA @ Xt).t().contiguous().t()
+        torch.cuda.synchronize()
+        ms, its = time_solves(mp, dA, dB, mp.make_opts(), 1)
+        _, _, _, rep = mp.mp_dsgesv_ex(dA, dB, None, mp.make_opts())
+        torch.cuda.synchronize()
+        ms64, _ = time_solves(mp, dA, dB, mp.make_opts(), 1, fp64=True)
+        res["C4"] = {"n": n4, "nrhs": r4, "ms": round(ms, 1), "gflops": round(flops(n4) / ms / 1e6, 1), "iters": its,
+                     "factor_ms": round(rep.t_factor_ms, 1), "refine_ms": round(rep.t_refine_ms, 1),
+                     "fp64_ms": round(ms64, 1), "speedup_vs_fp64": round(ms64 / ms, 3)}
+        del dA, dB, Xt
+        torch.cuda.empty_cache()
+    return res
+
+
+def log(msg: str):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
+    import faulthandler
+    faulthandler.enable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -307,6 +456,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-n", type=int, default=8192)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C4/C5/FFMA lines beside the headline")
+    ap.add_argument("--no-c4", action="store_true", help="skip C4 (n = 49152) among the other configs")
     ap.add_argument("--quiet", action="store_true")
     ap.add_argument("--dist", action="store_true",
                     help="use the 1D block-cyclic multi-GPU solver even at N = 1 (it is always used at N > 1)")
@@ -353,6 +504,7 @@ def main():
         _, it, info, rep = mp.mp_dsgesv_ex(dA, dB, dX, opts)
         return it, info, rep
 
+    log("warm-up")
     clk = ClockSampler(dev.index).start()                         # running before the warm-up
     for _ in range(args.warmup):
         it, info, rep = solve()
@@ -437,6 +589,7 @@ def main():
                          if v["ms"] > 0 else None}
                  for k, v in sorted(kern.items(), key=lambda kv: -kv[1]["ms"])}
 
+    log("fp64 path")
     # FP64 path on the same inputs (speedup denominator, B:5)
     fp64_ms = None
     if args.fp64_steps > 0:
@@ -450,7 +603,12 @@ def main():
         f1.record(stream)
         torch.cuda.synchronize()
         fp64_ms = f0.elapsed_time(f1) / args.fp64_steps
+    log("fp64 roofline")
+    roof64 = fp64_roofline(mp, dA, dB, args.nb) if args.fp64_steps > 0 else None
+    log("cusolver context")
+    cusolver_ms = cusolver_context(dA, dB) if args.fp64_steps > 0 else None
 
+    log("e2e")
     # end-to-end through the C-ABI with pinned HOST buffers (copies inside the timed region)
     e2e = None
     if args.e2e_steps > 0:
@@ -480,13 +638,23 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         dt, r, threads = cpu_oracle_sample(args.cpu_n, inputs.BASE_SEED)
         cpu = {"value": round(flops(args.cpu_n) / dt / 1e9, 3), "unit": "GFLOP/s", "cores": threads,
-               "kind": "oracle", "sample": f"one full oracle_dsgesv solve at n={args.cpu_n} (same generator, "
-                                           f"{dt:.1f} s, iters={r.iters}); the n=16384 solve is 8x that work"}
+               "kind": "oracle", "sample": f"one full oracle_dsgesv solve at n={args.cpu_n} (C3's generator at a "
+                                           f"bounded size; GFLOP/s = 2n^3/3 of that n / its time: {dt:.1f} s, "
+                                           f"iters={r.iters})"}
+        import oracle
+        nt = oracle.num_threads()
+        oracle.set_num_threads(1)
+        dt1, r1, _ = cpu_oracle_sample(512, inputs.BASE_SEED)
+        oracle.set_num_threads(nt)
+        cpu["c1_one_thread"] = {"n": 512, "s": round(dt1, 3), "gflops": round(flops(512) / dt1 / 1e9, 3),
+                                "iters": r1.iters}
+    log("other configs")
+    extra = other_configs(mp, args, dev) if (rank == 0 and world == 1 and not args.no_configs) else None
 
     if rank == 0:
         out = {"metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic",
+               "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(args.variant), "data": "synthetic",
                "config": {"workload": WORKLOAD, "n": n, "nrhs": nrhs, "nb": reps[-1][2].nb,
                           "variant": args.variant, "iters": iters,
                           "l2": "inputs larger than L2 (A fp64 = %.2f GB)" % (8 * n * n / 1e9),
@@ -495,9 +663,15 @@ def main():
                           if mp.mp_exec_info()[0] else "off"},
                "speedup_vs_fp64": round(fp64_ms / ms_step, 3) if fp64_ms else None,
                "fp64_ms_per_step": round(fp64_ms, 3) if fp64_ms else None,
+               "roofline_fp64_path": roof64,
+               "fp64_context": {"cusolver_dgetrf_dgetrs_ms": round(cusolver_ms, 3),
+                                "speedup_vs_cusolver": round(cusolver_ms / ms_step, 3),
+                                "fp64_path_vs_cusolver": round(fp64_ms / cusolver_ms, 3) if fp64_ms else None,
+                                "note": "vendor FP64 LU solve via torch.linalg (context only, not on the path)"}
+               if cusolver_ms else None,
                "e2e": e2e, "roofline": roof, "roofline_residual": roof_res,
                "panel_us_per_column": panel_us_col, "kernels": breakdown, "cpu_baseline": cpu,
-               "clocks": clk.summary(), "gpu_launches": launches,
+               "clocks": clk.summary(), "gpu_launches": launches, "other_configs": extra,
                "phases_ms": {"wall": round(1e3 * sum(walls) / len(walls), 3),
                              "call_device": round(sum(r[2].t_total_ms for r in reps) / len(reps), 3),
                              "demote": round(sum(r[2].t_demote_ms for r in reps) / len(reps), 3),

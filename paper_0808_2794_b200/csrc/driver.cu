@@ -485,6 +485,10 @@ struct Factor {
         if (w <= wl) { leaf(q, c0, w, klo, khi); return; }
         int w1 = (int)round_up(w / 2, 8);
         if (w1 > wl && w1 % wl) w1 = (int)round_up(w1, wl);
+        // leaves narrower than 8 columns (binary64 leaves of m > 32768 rows are 4 wide): split on
+        // the leaf width instead, so the recursion always shrinks
+        if (w1 >= w) w1 = (int)round_up(w / 2, wl);
+        if (w1 >= w) w1 = w - wl;
         panel(q, c0, w1, klo, khi);
         prof_begin(KC_GEMM, q);
         const bool fused = fuse_trsm &&

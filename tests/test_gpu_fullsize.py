@@ -202,28 +202,28 @@ def test_kappa1_8192_budget_edge(mp, orc, uv8192):
 
 
 # --------------------------------------------------------------------------- EXACT (P2) at size
-def _exact_case(mp, n, nb, variant, solve):
+def _exact_case(mp, n, nb, variant, solve, fp64=False):
     import ctypes
     import torch
     A, B, X, perm, L, U = inputs.exact_lu_device(n, nrhs=2, seed=n + variant)
     torch.cuda.synchronize()
-    LU = torch.empty((n, n), dtype=torch.float32, device="cuda")      # column-major: LU[:, j] contiguous
+    LU = torch.empty((n, n), dtype=torch.float64 if fp64 else torch.float32, device="cuda")   # column-major
     ipiv = torch.empty(n, dtype=torch.int32, device="cuda")
     info = ctypes.c_int(7)
     opts = mp.make_opts(nb=nb, variant=variant)
     mp.lib.mp_set_stream(torch.cuda.current_stream().cuda_stream)
     t0 = time.perf_counter()
-    mp._check(mp.lib.mp_sgetrf(n, A.data_ptr(), n, LU.data_ptr(), ipiv.data_ptr(), ctypes.byref(info),
-                               ctypes.byref(opts)))
+    getrf = mp.lib.mp_dgetrf if fp64 else mp.lib.mp_sgetrf
+    mp._check(getrf(n, A.data_ptr(), n, LU.data_ptr(), ipiv.data_ptr(), ctypes.byref(info), ctypes.byref(opts)))
     torch.cuda.synchronize()
     tf = time.perf_counter() - t0
     assert info.value == 0
     LUr = LU.view(n, n)                     # LUr[j, i] = LU(i, j)  (column-major buffer read row-major)
     # L strictly below the diagonal, U on and above, bitwise
     Lg = torch.tril(LUr.t(), -1)
-    ok_l = torch.equal(Lg, torch.tril(L, -1))
+    ok_l = torch.equal(Lg, torch.tril(L, -1).to(LUr.dtype))
     del Lg
-    ok_u = torch.equal(torch.triu(LUr.t()), U)
+    ok_u = torch.equal(torch.triu(LUr.t()), U.to(LUr.dtype))
     del LU, LUr
     # pivots: replay the sequential interchanges into a permutation
     ip = ipiv.cpu().numpy()
@@ -231,9 +231,14 @@ def _exact_case(mp, n, nb, variant, solve):
     for k, q in enumerate(ip):
         p[k], p[q] = p[q], p[k]
     ok_p = np.array_equal(p, perm.cpu().numpy())
-    rec = {"cfg": "EXACT", "n": n, "nb": nb, "variant": variant, "P": ok_p, "L": ok_l, "U": ok_u,
-           "t_getrf_s": tf}
-    if solve:
+    rec = {"cfg": "EXACT", "n": n, "nb": nb, "variant": "fp64" if fp64 else variant, "P": ok_p, "L": ok_l,
+           "U": ok_u, "t_getrf_s": tf}
+    if solve and fp64:
+        Xg, info2, rep = mp.mp_dgesv_ex(A, B, opts=opts)
+        torch.cuda.synchronize()
+        it = 0
+        rec.update(info=info2, X=bool(torch.equal(Xg, X)))
+    elif solve:
         Xg, it, info2, rep = mp.mp_dsgesv_ex(A, B, opts=opts)
         torch.cuda.synchronize()
         rec.update(iters=it, info=info2, X=bool(torch.equal(Xg, X)))
@@ -255,3 +260,9 @@ def test_exact_lu_16384(mp):
 def test_exact_lu_49152(mp):
     """C4's size: the m > 16384 leaf instantiations and the largest clusters."""
     _exact_case(mp, 49152, 256, 1, True)
+
+
+def test_exact_lu_fp64_36864(mp):
+    """The binary64 path (mp_dgetrf / mp_dgesv, the fallback) above 32768 rows, where its leaves are
+    4 columns wide (512 x 8 rows per CTA, 16-CTA cluster): P, L, U and X bitwise."""
+    _exact_case(mp, 36864, 256, 1, True, fp64=True)
