@@ -21,6 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O3", "-march=x86-64-v2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
            "-fPIC", "-shared", "-std=c11"]
@@ -32,9 +33,9 @@ ITERMAX = 30
 
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc).  Building the checker is not using it."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *_CFLAGS, "-o", tmp, *_SRCS, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -56,6 +57,16 @@ def _load():
             lib.oracle_fro_norm.restype = ctypes.c_double
             lib.oracle_dgesv.argtypes = [i64, i64, p, i64, p, p, pint]
             lib.oracle_dsgesv_ex.argtypes = [i64, i64, p, i64, p, p, pint, pint, ctypes.c_int,
+                                             p, pint, ctypes.POINTER(ctypes.c_double)]
+            lib.oracle_spotf2.argtypes = [i64, p, i64]
+            lib.oracle_dpotf2.argtypes = [i64, p, i64]
+            lib.oracle_spotrs.argtypes = [i64, i64, p, i64, p]
+            lib.oracle_dpotrs.argtypes = [i64, i64, p, i64, p]
+            lib.oracle_symv_residual.argtypes = [i64, i64, p, i64, p, p, p]
+            lib.oracle_sym_fro_norm.argtypes = [i64, p, i64]
+            lib.oracle_sym_fro_norm.restype = ctypes.c_double
+            lib.oracle_dposv.argtypes = [i64, i64, p, i64, p, p, pint]
+            lib.oracle_dsposv_ex.argtypes = [i64, i64, p, i64, p, p, pint, pint, ctypes.c_int,
                                              p, pint, ctypes.POINTER(ctypes.c_double)]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
@@ -162,4 +173,78 @@ def dsgesv(A, B, itermax: int = ITERMAX, lda: int | None = None) -> Result:
     _load().oracle_dsgesv_ex(n, Bm.shape[1], _ptr(A), lda if lda is not None else max(1, n), _ptr(Bm), _ptr(X),
                              ctypes.byref(iters), ctypes.byref(info), int(itermax), _ptr(hist),
                              ctypes.byref(nh), ctypes.byref(anrm))
+    return Result(X.reshape(np.shape(B), order="F"), iters.value, info.value, hist[: nh.value].copy(), anrm.value)
+
+
+# ---------------------------------------------------------------------------- SPD variant (oracle_chol.c)
+# SPOTRF / SPOTRS / DSYMM in place of SGETRF / SGETRS / DGEMM.  Only the LOWER
+# triangle of A is read (LAPACK UPLO = 'L').
+def spotf2(A):
+    """Step 1, SPD case, binary32: returns (L lower (upper part of the input copy untouched), info)."""
+    L = _fortran(A, np.float32).copy(order="F")
+    info = _load().oracle_spotf2(L.shape[0], _ptr(L), max(1, L.shape[0]))
+    return L, int(info)
+
+
+def dpotf2(A):
+    L = _fortran(A, np.float64).copy(order="F")
+    info = _load().oracle_dpotf2(L.shape[0], _ptr(L), max(1, L.shape[0]))
+    return L, int(info)
+
+
+def spotrs(L, B):
+    L = _fortran(L, np.float32)
+    n = L.shape[0]
+    Bm = _fortran(B, np.float32).reshape(n, -1, order="F").copy(order="F")
+    _load().oracle_spotrs(n, Bm.shape[1], _ptr(L), max(1, n), _ptr(Bm))
+    return Bm.reshape(np.shape(B), order="F")
+
+
+def dpotrs(L, B):
+    L = _fortran(L, np.float64)
+    n = L.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F").copy(order="F")
+    _load().oracle_dpotrs(n, Bm.shape[1], _ptr(L), max(1, n), _ptr(Bm))
+    return Bm.reshape(np.shape(B), order="F")
+
+
+def symv_residual(A, X, B):
+    """Step 4, SPD case: R = B - A_sym X in binary64 from the lower triangle of A."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Xm = _fortran(X, np.float64).reshape(n, -1, order="F")
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    R = np.empty_like(Bm, order="F")
+    _load().oracle_symv_residual(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(Xm), _ptr(R))
+    return R.reshape(np.shape(B), order="F")
+
+
+def sym_fro_norm(A) -> float:
+    A = _fortran(A, np.float64)
+    return float(_load().oracle_sym_fro_norm(A.shape[0], _ptr(A), max(1, A.shape[0])))
+
+
+def dposv(A, B):
+    """Binary64 SPD solver (Cholesky + the two solves): (X, info)."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    X = np.zeros_like(Bm, order="F")
+    info = ctypes.c_int(0)
+    _load().oracle_dposv(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), ctypes.byref(info))
+    return X.reshape(np.shape(B), order="F"), info.value
+
+
+def dsposv(A, B, itermax: int = ITERMAX) -> Result:
+    """Algorithm 1, SPD form, with B:5's stop test, cap and fallback."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64)
+    Bm = Bm.reshape(n, Bm.size // n if n else (Bm.shape[1] if Bm.ndim > 1 else 1), order="F")
+    X = np.zeros_like(Bm, order="F")
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(itermax + 1, dtype=np.float64)
+    anrm = ctypes.c_double(0.0)
+    _load().oracle_dsposv_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), ctypes.byref(iters),
+                             ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh), ctypes.byref(anrm))
     return Result(X.reshape(np.shape(B), order="F"), iters.value, info.value, hist[: nh.value].copy(), anrm.value)

@@ -140,3 +140,43 @@ def exact_lu_device(n: int, nrhs: int = 1, seed: int = BASE_SEED, density: float
     Bt = (Xt @ At)                           # B^T = X^T A^T, exact (dyadic, < 2^53)
     B = Bt.t()
     return A, B, X, perm, L, U
+
+
+# --------------------------------------------------------------------------- SPD variant (NEXT-1)
+def spd_wishart(n: int, nrhs: int = 1, seed: int = BASE_SEED):
+    """Dense SPD stand-in (the paper's SPD runs state no matrices): A = G G^T / (2n) with G an
+    n x 2n N(0,1) matrix — Marchenko-Pastur spectrum in [(1 - 1/sqrt 2)^2, (1 + 1/sqrt 2)^2], kappa ~ 34.
+    Full symmetric A (both triangles), x_true U[-1,1], b = A x_true."""
+    G = _rng(seed).standard_normal(size=(n, 2 * n))
+    A = np.asfortranarray((G @ G.T) / (2.0 * n))
+    A = np.asfortranarray(0.5 * (A + A.T))         # exactly symmetric bytes
+    X = _xtrue(n, nrhs, seed)
+    B = np.asfortranarray(A @ X)
+    return A, B, X
+
+
+def spd_conditioned(n: int, kappa: float, nrhs: int = 1, seed: int = BASE_SEED, U=None):
+    """SPD analog of C5: A = U diag(sigma) U^T, U Haar-orthogonal, sigma_i = kappa^(-i/(n-1))."""
+    if U is None:
+        U = haar_orthogonal(n, seed + 2)
+    s = singular_values(n, kappa)
+    A = (U * s[None, :]) @ U.T
+    A = np.asfortranarray(0.5 * (A + A.T))
+    X = _xtrue(n, nrhs, seed)
+    B = np.asfortranarray(A @ X)
+    return A, B, X
+
+
+def exact_chol(n: int, nrhs: int = 1, seed: int = BASE_SEED, density: float = 0.5):
+    """Pin family for the SPD path: A = L L^T with L lower, diagonal in {1, 2, 4} and off-diagonal entries
+    in {0, +-1/4, +-1/2}.  Every step of a Cholesky factorisation (the square roots of l_jj^2, the
+    divisions by powers of two, the updates) is exact, so L is reproduced bitwise; x_true is a multiple of
+    1/4 in [-1, 1], so the two triangular solves are exact too.  Returns (A full symmetric, B, X, L)."""
+    r = _rng(seed)
+    choices = np.array([0.25, -0.25, 0.5, -0.5])
+    L = np.tril(r.choice(choices, size=(n, n)) * (r.random((n, n)) < density), -1)
+    L += np.diag(r.choice(np.array([1.0, 2.0, 4.0]), size=n))
+    A = np.asfortranarray(L @ L.T)
+    X = np.asfortranarray(r.integers(-4, 5, size=(n, nrhs)).astype(np.float64) / 4.0)
+    B = np.asfortranarray(A @ X)
+    return A, B, X, L
