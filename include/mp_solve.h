@@ -163,6 +163,46 @@ int mp_sgetrf(int64_t n, const double *A, int64_t lda, float *LU, int32_t *ipiv,
 int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv,
               int *info, const mp_opts *opts);
 
+/* ------------------------------------------------------------------------------------------
+ * SPD variant.  PAPER.md P:369-371: "For the symmetric case the SGETRF,
+ * SGETRS and DGEMM subroutines were replaced by the SPOTRF, SPOTRS and DSYMM subroutines":
+ * Algorithm 1 with step 1 a binary32 Cholesky A = L L^T, steps 2-3 / 5-6 the two binary32
+ * triangular solves with L and L^T, step 4 r = b - A x in binary64 with the symmetric A; the
+ * stop test, the 30-correction cap and the binary64 fallback are those of mp_dsgesv.
+ *
+ * A: n x n symmetric positive definite, column-major, leading dimension lda; ONLY its LOWER
+ * triangle (i >= j) is read (LAPACK UPLO = 'L'); the strict upper triangle is never touched and
+ * may hold anything.  B, X, pointers, ownership, synchronisation, return value: as mp_dsgesv.
+ * ||A||_F in the stop test is the norm of the full symmetric matrix (reading C-3).
+ *
+ * *info: 0; -i argument errors as mp_dsgesv (-3 also: a NaN/Inf in the lower triangle);
+ *   +k: the binary64 Cholesky broke down at column k (the leading minor of order k is not
+ *   positive definite, reading C-2); X is unspecified.
+ * *iters: >= 0 corrections; -2 demotion overflow; -3 the binary32 Cholesky broke down (a pivot
+ *   not > 0, reading C-1); -31 no convergence within 30 corrections.  iters < 0: X came from
+ *   the binary64 Cholesky solver.
+ * opts.variant selects the trailing (SYRK) update: MP_VARIANT_3XTF32 (default, lower tiles only)
+ * or MP_VARIANT_FFMA; opts.nb <= 256 (binary32) / 128 (binary64). */
+int mp_dsposv(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+              const double *B, double *X, int *iters, int *info);
+int mp_dsposv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+                 const double *B, double *X, int *iters, int *info,
+                 const mp_opts *opts, mp_report *rep);
+
+/* The binary64 SPD solver (Cholesky + the two solves, no refinement): the T3 "reference time"
+ * of the symmetric column and mp_dsposv's fallback.  info as above. */
+int mp_dposv(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+             const double *B, double *X, int *info);
+int mp_dposv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda,
+                const double *B, double *X, int *info, const mp_opts *opts, mp_report *rep);
+
+/* Step 1 of the SPD variant alone: the Cholesky factor of fl32(A) (mp_spotrf) or A (mp_dpotrf)
+ * from A's lower triangle.  L: n x n column-major output, leading dimension n (device or host):
+ * L in the lower triangle, its strict upper triangle holds L^T.  info: argument errors as
+ * mp_sgetrf (-5: L NULL); +k breakdown at column k (1-based); -2 demotion overflow. */
+int mp_spotrf(int64_t n, const double *A, int64_t lda, float *L, int *info, const mp_opts *opts);
+int mp_dpotrf(int64_t n, const double *A, int64_t lda, double *L, int *info, const mp_opts *opts);
+
 /* Resolve the per-launch events recorded by calls made with opts.flags = 2|4 since the
  * last collection: fills rep->k_ms / k_work / k_launches (summed over those calls, all
  * other fields untouched) and clears the records.  Synchronises the device. */

@@ -66,6 +66,12 @@ lib.mp_dgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi]
 lib.mp_dgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
 lib.mp_sgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_dgetrf.argtypes = [_i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_dsposv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, _pi]
+lib.mp_dsposv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+lib.mp_dposv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi]
+lib.mp_dposv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+lib.mp_spotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_dpotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_kernel_schur_update.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_kernel_schur_update_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_set_stream.argtypes = [_p]
@@ -86,7 +92,8 @@ lib.mp_dgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi]
 
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
-            "mp_kernel_schur_update_f64",
+            "mp_kernel_schur_update_f64", "mp_dsposv", "mp_dsposv_ex", "mp_dposv", "mp_dposv_ex", "mp_spotrf",
+            "mp_dpotrf",
             "mp_profile_collect", "mp_exec_info", "mp_get_unique_id", "mp_comm_init", "mp_comm_init_loopback",
             "mp_comm_destroy", "mp_1dbc_local_cols", "mp_dsgesv_1dbc", "mp_dsgesv_1dbc_ex", "mp_dgesv_1dbc")
 
@@ -213,6 +220,60 @@ def mp_dgesv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
 def mp_dgesv(A, B, X=None, opts: Opts | None = None):
     X, info, _ = mp_dgesv_ex(A, B, X, opts, report=False)
     return X, info
+
+
+def mp_dsposv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
+    """Mixed-precision SPD solve (lower triangle of A read); returns (X, iters, info, Report|None)."""
+    n = A.shape[0]
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
+    lib.mp_set_stream(_stream_of(A, B, X))
+    it, info = ctypes.c_int(0), ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_dsposv_ex(n, nrhs, pa, lda, pb, px, ctypes.byref(it), ctypes.byref(info),
+                            ctypes.byref(opts) if opts is not None else None,
+                            ctypes.byref(rep) if rep is not None else None))
+    return X, it.value, info.value, rep
+
+
+def mp_dposv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
+    n = A.shape[0]
+    nrhs = _nrhs(B, n)
+    if X is None:
+        X = _alloc_like_X(B, n, nrhs)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    px, _ = _ptr_ld(X, "X", False, n)
+    lib.mp_set_stream(_stream_of(A, B, X))
+    info = ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_dposv_ex(n, nrhs, pa, lda, pb, px, ctypes.byref(info),
+                           ctypes.byref(opts) if opts is not None else None,
+                           ctypes.byref(rep) if rep is not None else None))
+    return X, info.value, rep
+
+
+def _potrf(fn, dtype, A, opts):
+    n = A.shape[0]
+    pa, lda = _ptr_ld(A, "A", True)
+    L = np.zeros((n, n), dtype=dtype, order="F")
+    info = ctypes.c_int(0)
+    lib.mp_set_stream(_stream_of(A))
+    _check(fn(n, pa, lda, L.ctypes.data, ctypes.byref(info), ctypes.byref(opts) if opts is not None else None))
+    return L, info.value
+
+
+def mp_spotrf(A, opts: Opts | None = None):
+    """SPD step 1 alone (binary32 Cholesky of fl32(A)'s lower triangle): host (L Fortran, info)."""
+    return _potrf(lib.mp_spotrf, np.float32, A, opts)
+
+
+def mp_dpotrf(A, opts: Opts | None = None):
+    return _potrf(lib.mp_dpotrf, np.float64, A, opts)
 
 
 def _getrf(fn, dtype, A, opts):

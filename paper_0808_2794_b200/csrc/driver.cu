@@ -1003,6 +1003,289 @@ int getrf_impl(int64_t n, const double *A, int64_t lda, T *LU, int32_t *ipiv_out
     return MP_OK;
 }
 
+// ------------------------------------------------------------------ SPD variant
+// Algorithm 1 with SPOTRF / SPOTRS / DSYMM.  Step 1 is a blocked right-looking
+// Cholesky of the binary32 working copy: per panel the diagonal block (C2), the panel below it
+// (C3, which also writes L21^T into the upper block), and the trailing update A22 -= L21 L21^T on
+// the tiles that touch the lower triangle (3xTF32 tcgen05 / DMMA; the FFMA variant updates the
+// whole square: the upper part is overwritten by later panels).  The factors are then put in the
+// unit-lower / upper form of the LU path (C4, reading C-4), so the triangular-solve kernels,
+// the refinement loop and the fallback logic are the nonsymmetric path's, with P = I.
+int chol_nb(size_t elem, int64_t n, int requested)
+{
+    const int mx = elem == 4 ? chol_block_max<float>() : chol_block_max<double>();
+    const int nb = requested > 0 ? requested : (n <= 1024 ? 64 : (n <= 4096 ? 128 : 256));
+    return std::max(1, std::min(nb, mx));
+}
+
+template <typename T>
+void run_chol(T *W, int64_t n, int64_t ldw, int nb, DevStatus *st, Pool &pool, cudaStream_t s, int variant)
+{
+    float *scratch = nullptr;
+    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32 && n > nb)
+        scratch = pool.get<float>(tf32_scratch_floats(n, nb));
+    const int sms = num_sms();
+    for (int64_t k = 0; k < n; k += nb) {
+        const int w = (int)std::min<int64_t>(nb, n - k);
+        prof_begin(KC_PANEL, s);
+        launch_potrf_diag<T>(W, ldw, k, w, st, s);
+        prof_end(KC_PANEL, (double)w * w * w / 3.0, s);
+        const int64_t m = n - k - w;
+        if (m <= 0) break;
+        prof_begin(KC_TRSM, s);
+        launch_trsm_chol<T>(W, ldw, k, w, n, s);
+        prof_end(KC_TRSM, (double)w * w * m, s);
+        prof_begin(KC_TRAIL, s);
+        T *A21 = W + (k + w) * ldw + k, *A22 = W + (k + w) * ldw + k + w;
+        if constexpr (sizeof(T) == 4) {
+            if (scratch && m >= 256)
+                launch_syrk_lower_3xtf32(A21, ldw, A22, ldw, m, w, scratch, sms, s);
+            else
+                launch_gemm_update<T>(W, ldw, k + w, k + w, k, m, m, w, s);
+        } else {
+            if (!launch_dgemm_dmma(A21, ldw, W + k * ldw + k + w, ldw, A22, ldw, m, m, w, s, true))
+                launch_gemm_update<T>(W, ldw, k + w, k + w, k, m, m, w, s);
+        }
+        prof_end(KC_TRAIL, (double)m * (m + 1) * w, s);        // SYRK: lower triangle incl. diagonal
+    }
+}
+
+// binary64 SPD solve on a fresh working copy (the fallback, and mp_dposv).  Returns info:
+// 0, or k + 1 when the binary64 Cholesky breaks down at column k (reading C-2).
+int fp64_chol_solve(const Views &v, int64_t n, int64_t nrhs, int nb, Pool &pool, StatusIO &sio, cudaStream_t s)
+{
+    const int64_t ldw = round_up(n, 64);
+    double *W = pool.get<double>((size_t)n * ldw);
+    int32_t *ident = pool.get<int32_t>(n);
+    double *Y = pool.get<double>((size_t)n * nrhs), *d = pool.get<double>(n);
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<double>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    const int sms = num_sms();
+    double *dpart = pool.get<double>(demote_sym_partials(sms));
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    sio.reset();
+    launch_demote_sym<double>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, sms, s);
+    run_chol<double>(W, n, ldw, chol_nb(8, n, nb), sio.d, pool, s, MP_VARIANT_FFMA);
+    const DevStatus &st = sio.read();
+    if (st.flags & ST_A_NONFINITE) return -3;
+    if (st.flags & ST_ZERO_PIVOT) return st.zero_col;
+    launch_chol_to_lu<double>(W, ldw, n, d, s);
+    launch_init_perm(ident, n, s);
+    launch_permute_demote_rhs<double>(v.B, n, nrhs, ident, Y, sio.d, s);
+    launch_lu_solve<double>(W, ldw, n, nrhs, Y, v.X, 0, ss, s);
+    return 0;
+}
+
+int dsposv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0; *iters = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    if (check_args(a, info)) { if (rep) rep->info = *info; return MP_OK; }
+    if (a.n == 0 || a.nrhs == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int64_t n = a.n, nrhs = a.nrhs;
+    const int nb = chol_nb(4, n, o.nb);
+    const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    if (o.variant != MP_VARIANT_FFMA && o.variant != MP_VARIANT_3XTF32) throw std::runtime_error("unknown variant");
+    check_size_limits(n);
+    cudaStream_t s = g_stream;
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    Views v = stage_in(a, pool, s, true);
+    const int t_staged = tm.mark();
+    StatusIO sio(pool, s);
+    const int sms = num_sms();
+    const int64_t ldw = round_up(n, 64);
+    float *W = pool.get<float>((size_t)n * ldw);
+    int32_t *ident = pool.get<int32_t>(n);
+    float *Y = pool.get<float>((size_t)n * nrhs), *dsc = pool.get<float>(n);
+    double *R = pool.get<double>((size_t)n * nrhs), *AX = pool.get<double>((size_t)n * nrhs);
+    double *spart = pool.get<double>(symv_partial_elems(n));
+    ResidualScratch rs;
+    rs.partial = nullptr;
+    rs.blocksums = pool.get<double>((size_t)ceil_div(n, 256) * 2 * nrhs);
+    rs.counter = pool.get<unsigned>(1);
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<float>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    ss.tags = pool.get<uint64_t>(solve_tag_words(n, nrhs));
+    ss.tag_cols = (int)std::min<int64_t>(nrhs, 16);
+    MP_CUDA(cudaMemsetAsync(ss.tags, 0, solve_tag_words(n, nrhs) * sizeof(uint64_t), s));
+    double *dpart = pool.get<double>(demote_sym_partials(sms));
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(rs.counter, 0, sizeof(unsigned), s));
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+
+    // ---- C1: lower triangle -> symmetric binary32 working copy + ||A||_F; B finiteness
+    prof_begin(KC_DEMOTE, s);
+    launch_demote_sym<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, sms, s);
+    prof_end(KC_DEMOTE, 8.0 * n * n, s);
+    launch_init_perm(ident, n, s);
+    launch_permute_demote_rhs<float>(v.B, n, nrhs, ident, Y, sio.d, s);
+    const int t_dem = tm.mark();
+    DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) { *info = -3; if (rep) rep->info = -3; return MP_OK; }
+    if (st0.flags & ST_B_NONFINITE) { *info = -5; if (rep) rep->info = -5; return MP_OK; }
+    const double anrm = std::sqrt(st0.anrm2);
+    const double cte = anrm * std::ldexp(1.0, -53) * std::sqrt((double)n);
+    int code = (st0.flags & ST_OVERFLOW) ? -2 : 0;
+    int t_fac = t_dem, t_ref = t_dem, nhist = 0;
+    double hist[MP_HIST_MAX] = {0};
+    bool used_inv = false;
+    if (!code) {
+        run_chol<float>(W, n, ldw, nb, sio.d, pool, s, o.variant);             // step 1 (SPOTRF)
+        t_fac = tm.mark();
+        const DevStatus &st1 = sio.read();
+        if (st1.flags & ST_ZERO_PIVOT) code = -3;                              // reading C-1
+    }
+    if (!code && (o.flags & 1)) code = -31;
+    if (!code) {
+        launch_chol_to_lu<float>(W, ldw, n, dsc, s);                            // reading C-4
+        float *inv = nullptr;
+        if (!(o.flags & 32)) {
+            inv = pool.get<float>(solve_inv_floats(n));
+            launch_solve_inverses(W, ldw, n, inv, s);
+            if (!(solve_inverses_cond(inv, n, s) <= kInvCondMax)) inv = nullptr;
+        }
+        used_inv = inv != nullptr;
+        prof_begin(KC_SOLVE, s);
+        launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 0, ss, s, inv);        // steps 2-3 (SPOTRS)
+        prof_end(KC_SOLVE, 4.0 * n * n, s);
+        code = -31;
+        for (int it = 0; it <= itermax; ++it) {
+            prof_begin(KC_RESIDUAL, s);                                         // step 4 (DSYMM)
+            launch_symv_products(v.A, v.lda, n, nrhs, v.X, AX, spart, s);
+            launch_residual_finalize<float>(AX, n, nrhs, v.B, v.X, R, ident, Y, cte, rs, sio.d, s);
+            prof_end(KC_RESIDUAL, 4.0 * n * n * nrhs + 8.0 * 4 * n * nrhs, s);
+            const DevStatus &st = sio.read();
+            if (st.flags & ST_NORM_NONFINITE) break;
+            hist[nhist++] = st.ratio;
+            if (st.converged) { *iters = it; code = 0; break; }
+            if (it == itermax) break;
+            prof_begin(KC_SOLVE, s);
+            launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 1, ss, s, inv);    // steps 5-7
+            prof_end(KC_SOLVE, 4.0 * n * n, s);
+        }
+        t_ref = tm.mark();
+    }
+    int t_fb = tm.mark();
+    if (code) {
+        *iters = code;
+        *info = fp64_chol_solve(v, n, nrhs, o.nb, pool, sio, s);
+        t_fb = tm.mark();
+    }
+    finish_copy_out(a, v, s);
+    const int t_end = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = nb; rep->variant = o.variant;
+        rep->solve_inv = used_inv ? 1 : 0;
+        rep->anrm = anrm;
+        for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
+        rep->t_total_ms = tm.ms(t0, t_end);
+        rep->t_copy_ms = tm.ms(t0, t_staged);
+        rep->t_demote_ms = tm.ms(t_staged, t_dem);
+        rep->t_factor_ms = (t_fac != t_dem) ? tm.ms(t_dem, t_fac) : 0.0;
+        rep->t_refine_ms = (t_ref != t_dem) ? tm.ms(t_fac, t_ref) : 0.0;
+        rep->t_fallback_ms = code ? tm.ms(t_ref, t_fb) : 0.0;
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        if (!g_prof.deferred) prof_collect(rep);
+    }
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
+    return MP_OK;
+}
+
+int dposv_impl(const Args &a, int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    if (check_args(a, info)) { if (rep) rep->info = *info; return MP_OK; }
+    if (a.n == 0 || a.nrhs == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    check_size_limits(a.n);
+    cudaStream_t s = g_stream;
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    Views v = stage_in(a, pool, s, true);
+    const int t1 = tm.mark();
+    StatusIO sio(pool, s);
+    *info = fp64_chol_solve(v, a.n, a.nrhs, o.nb, pool, sio, s);
+    const DevStatus &st = sio.read();
+    if (*info != -3 && (st.flags & ST_B_NONFINITE)) *info = -5;
+    finish_copy_out(a, v, s);
+    const int t2 = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->info = *info; rep->nb = chol_nb(8, a.n, o.nb);
+        rep->t_total_ms = tm.ms(t0, t2);
+        rep->t_copy_ms = tm.ms(t0, t1);
+        rep->t_factor_ms = tm.ms(t1, t2);
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        if (!g_prof.deferred) prof_collect(rep);
+    }
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
+    return MP_OK;
+}
+
+// Cholesky factor alone (SPOTRF / DPOTRF of the lower triangle): L in the lower triangle of the
+// column-major output (leading dimension n); its strict upper triangle holds L^T.
+template <typename T>
+int potrf_impl(int64_t n, const double *A, int64_t lda, T *L, int *info, const mp_opts *opts)
+{
+    *info = 0;
+    if (n < 0) return *info = -1, MP_OK;
+    if (n > 0 && !A) return *info = -3, MP_OK;
+    if (lda < std::max<int64_t>(1, n)) return *info = -4, MP_OK;
+    if (n > 0 && !L) return *info = -5, MP_OK;
+    if (n == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    check_size_limits(n);
+    cudaStream_t s = g_stream;
+    g_launches = 0;
+    Pool pool(s);
+    Args a{n, 0, lda, A, nullptr, nullptr};
+    Views v = stage_in(a, pool, s, false);
+    StatusIO sio(pool, s);
+    const int64_t ldw = round_up(n, 64);
+    T *W = pool.get<T>((size_t)n * ldw);
+    const int sms = num_sms();
+    double *dpart = pool.get<double>(demote_sym_partials(sms));
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    launch_demote_sym<T>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, sms, s);
+    const DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) return *info = -3, MP_OK;
+    if (st0.flags & ST_OVERFLOW) return *info = -2, MP_OK;
+    run_chol<T>(W, n, ldw, chol_nb(sizeof(T), n, o.nb), sio.d, pool, s,
+                sizeof(T) == 4 ? o.variant : MP_VARIANT_FFMA);
+    const DevStatus &st = sio.read();
+    if (st.flags & ST_ZERO_PIVOT) *info = st.zero_col;
+    const bool l_dev = is_device_ptr(L);
+    T *dL = l_dev ? L : pool.get<T>((size_t)n * n);
+    launch_transpose_out<T>(W, ldw, n, dL, s);
+    if (!l_dev) MP_CUDA(cudaMemcpyAsync(L, dL, (size_t)n * n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    return MP_OK;
+}
+
 // ------------------------------------------------------------------ 1D block-cyclic multi-GPU path
 // SURVEY 8(e) / B:5: global column block j (nb columns) lives on rank j mod P at local slot
 // j / P; A (binary64, caller's) and the working copy use the same distribution; B, X, r, z,
@@ -1548,6 +1831,38 @@ int mp_dgetrf(int64_t n, const double *A, int64_t lda, double *LU, int32_t *ipiv
 {
     if (!info) { g_err = "info must not be NULL"; return MP_ERR_INTERNAL; }
     return guarded([&] { return getrf_impl<double>(n, A, lda, LU, ipiv, info, opts); });
+}
+
+int mp_dsposv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *iters, int *info)
+{
+    return guarded([&] { return dsposv_impl(Args{n, nrhs, lda, A, B, X}, iters, info, nullptr, nullptr); });
+}
+
+int mp_dsposv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *iters,
+                 int *info, const mp_opts *opts, mp_report *rep)
+{
+    return guarded([&] { return dsposv_impl(Args{n, nrhs, lda, A, B, X}, iters, info, opts, rep); });
+}
+
+int mp_dposv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *info)
+{
+    return guarded([&] { return dposv_impl(Args{n, nrhs, lda, A, B, X}, info, nullptr, nullptr); });
+}
+
+int mp_dposv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *X, int *info,
+                const mp_opts *opts, mp_report *rep)
+{
+    return guarded([&] { return dposv_impl(Args{n, nrhs, lda, A, B, X}, info, opts, rep); });
+}
+
+int mp_spotrf(int64_t n, const double *A, int64_t lda, float *L, int *info, const mp_opts *opts)
+{
+    return guarded([&] { return potrf_impl<float>(n, A, lda, L, info, opts); });
+}
+
+int mp_dpotrf(int64_t n, const double *A, int64_t lda, double *L, int *info, const mp_opts *opts)
+{
+    return guarded([&] { return potrf_impl<double>(n, A, lda, L, info, opts); });
 }
 
 int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,

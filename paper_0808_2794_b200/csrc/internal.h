@@ -199,7 +199,7 @@ void launch_gemm_update(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, i
 void launch_dgemm_dfma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
                        int64_t M, int64_t N, int64_t K, cudaStream_t s);
 bool launch_dgemm_dmma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, cudaStream_t s);
+                       int64_t M, int64_t N, int64_t K, cudaStream_t s, bool lower = false);
 template <typename T>
 void launch_gemm_ops(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
                      int64_t K, cudaStream_t s);
@@ -292,4 +292,29 @@ void launch_residual_finalize(const double *AX, int64_t n, int64_t nrhs, const d
                               const int32_t *pinv, T *Y, double cte, ResidualScratch &rs, DevStatus *st,
                               cudaStream_t s);
 
+}  // namespace mp
+
+namespace mp {
+// ---------------------------------------------------------------- SPD variant (k_chol.cu, NEXT-1)
+// Lower triangle of the column-major A -> full symmetric row-major W (fl32 RN for T = float),
+// ||A||_F^2 of the symmetric matrix into st->anrm2, flags.  partials: demote_sym_partials() doubles.
+template <typename T>
+void launch_demote_sym(const double *A, int64_t lda, int64_t n, T *W, int64_t ldw, double *partials,
+                       unsigned *counter, DevStatus *st, int num_sms, cudaStream_t s);
+size_t demote_sym_partials(int num_sms);
+template <typename T>
+int chol_block_max();                     // widest diagonal block of potrf / trsm_chol (256 / 128)
+template <typename T>
+void launch_potrf_diag(T *W, int64_t ldw, int64_t k, int w, DevStatus *st, cudaStream_t s);
+template <typename T>
+void launch_trsm_chol(T *W, int64_t ldw, int64_t k, int w, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_chol_to_lu(T *W, int64_t ldw, int64_t n, T *dscratch, cudaStream_t s);
+size_t symv_partial_elems(int64_t n);
+// AX = A_sym X from the lower triangle of the column-major A (n x nrhs, ld n)
+void launch_symv_products(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *X, double *AX,
+                          double *partials, cudaStream_t s);
+// C[M x M] lower tiles -= L21 L21^T, L21 = A[M x K] row-major (3xTF32 tcgen05)
+void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc, int64_t M, int64_t K, float *scratch,
+                              int num_sms, cudaStream_t s);
 }  // namespace mp

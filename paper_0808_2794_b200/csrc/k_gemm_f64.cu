@@ -57,7 +57,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b)
 template <int BN, int MINB>
 __global__ void __launch_bounds__(TileCfg<BN>::NT, MINB)
 dgemm_dmma_kernel(const double *__restrict__ A, int64_t lda, const double *__restrict__ B, int64_t ldb,
-                  double *__restrict__ C, int64_t ldc, int M, int N, int K)
+                  double *__restrict__ C, int64_t ldc, int M, int N, int K, int lower)
 {
     constexpr int NT = TileCfg<BN>::NT, BPAD = TileCfg<BN>::BPAD, B_ELEMS = TileCfg<BN>::B_ELEMS;
     constexpr int WN = BN / 32;                          // warps along N
@@ -68,6 +68,7 @@ dgemm_dmma_kernel(const double *__restrict__ A, int64_t lda, const double *__res
     pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    if (lower && m0 + BM - 1 < n0) return;               // SPD SYRK: tile entirely above the diagonal
     const int wm = (warp / WN) * 64, wn = (warp % WN) * 32;
     const int nk = (K + BK - 1) / BK;
     // pull this tile of C into L2 now, so the epilogue's read-modify-write does not wait on HBM
@@ -156,7 +157,7 @@ dgemm_dmma_kernel(const double *__restrict__ A, int64_t lda, const double *__res
 }  // namespace
 
 bool launch_dgemm_dmma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
-                       int64_t M, int64_t N, int64_t K, cudaStream_t s)
+                       int64_t M, int64_t N, int64_t K, cudaStream_t s, bool lower)
 {
     auto al = [](const void *p, int64_t ld) { return ((uintptr_t)p % 16 == 0) && (ld % 2 == 0); };
     if (M <= 0 || N <= 0 || K <= 0) return true;
@@ -169,12 +170,12 @@ bool launch_dgemm_dmma(const double *A, int64_t lda, const double *B, int64_t ld
         auto kern = dgemm_dmma_kernel<128, 1>;
         func_smem_once((const void *)kern, TileCfg<128>::SMEM);
         launch_ex(kern, dim3((unsigned)ceil_div(N, 128), (unsigned)ceil_div(M, BM)), dim3(TileCfg<128>::NT),
-                  TileCfg<128>::SMEM, s, nullptr, A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K);
+                  TileCfg<128>::SMEM, s, nullptr, A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, (int)lower);
     } else {
         auto kern = dgemm_dmma_kernel<64, 2>;
         func_smem_once((const void *)kern, TileCfg<64>::SMEM);
         launch_ex(kern, dim3((unsigned)ceil_div(N, 64), (unsigned)ceil_div(M, BM)), dim3(TileCfg<64>::NT),
-                  TileCfg<64>::SMEM, s, nullptr, A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K);
+                  TileCfg<64>::SMEM, s, nullptr, A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, (int)lower);
     }
     return true;
 }

@@ -153,7 +153,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
 __global__ void __launch_bounds__(GT, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_constant__ CUtensorMap tmUl,
                    const __grid_constant__ CUtensorMap tmLh, const __grid_constant__ CUtensorMap tmLl,
-                   float *__restrict__ C, int64_t ldc, int M, int N, int K, int terms)
+                   float *__restrict__ C, int64_t ldc, int M, int N, int K, int terms, int lower)
 {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned ring (SWIZZLE_128B atoms)
@@ -165,6 +165,12 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
     const int tiles_n = (N + TM_COLS - 1) / TM_COLS, tiles_m = (M + TM_ROWS - 1) / TM_ROWS;
     const int ntiles = tiles_n * tiles_m;
     const int nk = (K + KC - 1) / KC;
+    // lower != 0 (the SPD path's SYRK, C square with its diagonal at i == j): tiles entirely above
+    // the diagonal (every row index below every column index) are skipped by all three roles
+    auto skip = [&](int t) {
+        const int tn = t % tiles_n, tm = t / tiles_n;
+        return lower && tm * TM_ROWS + TM_ROWS - 1 < tn * TM_COLS;
+    };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
@@ -191,6 +197,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
             int stage = 0;
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                if (skip(t)) continue;
                 const int tn = t % tiles_n, tm = t / tiles_n;
                 for (int kc = 0; kc < nk; ++kc) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
@@ -212,6 +219,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
             uint32_t acc_phase[2] = {0, 0};
             int a = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                if (skip(t)) continue;
                 mbar_wait(&acc_empty[a], acc_phase[a] ^ 1);           // epilogue drained this accumulator
                 tc_fence_after();
                 const uint32_t tacc = tmem_base + (uint32_t)(a * TM_ROWS);
@@ -251,6 +259,7 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
         uint32_t acc_phase[2] = {0, 0};
         int a = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            if (skip(t)) continue;
             const int tn = t % tiles_n, tm = t / tiles_n;
             const int j = tn * TM_COLS + q * 32 + lane;
             const int i0 = tm * TM_ROWS + h * (TM_ROWS / 2);
@@ -396,7 +405,31 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
     func_smem_once((const void *)gemm_3xtf32_kernel, smem);
     launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N,
-              (int)K, terms);
+              (int)K, terms, 0);
+}
+
+// SPD path: C[M x M] (lower tiles) -= L21 L21^T with L21 = A[M x K] (row-major, lda).  The B operand of
+// the 3xTF32 kernel is K-major U^T = L21 itself, so one hi/lo split of L21 serves as both operands.
+void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc, int64_t M, int64_t K, float *scratch,
+                              int num_sms, cudaStream_t s)
+{
+    if (M <= 0 || K <= 0) return;
+    const int kp = (int)round_up(K, 4);
+    float *Lh = scratch, *Ll = Lh + (size_t)M * kp;
+    const int64_t tot = M * kp;
+    launch_ex(split_rows_kernel, dim3((unsigned)std::min<int64_t>(ceil_div(tot, 256), 4096)), dim3(256), 0, s, nullptr,
+              A, lda, (int)M, (int)K, Lh, Ll, kp);
+    CUtensorMap mUh, mUl, mLh, mLl;
+    encode_kmajor(&mUh, Lh, (int)M, (int)K, kp, TM_COLS);
+    encode_kmajor(&mUl, Ll, (int)M, (int)K, kp, TM_COLS);
+    encode_kmajor(&mLh, Lh, (int)M, (int)K, kp, TM_ROWS);
+    encode_kmajor(&mLl, Ll, (int)M, (int)K, kp, TM_ROWS);
+    const int ntiles = (int)(ceil_div(M, TM_COLS) * ceil_div(M, TM_ROWS));
+    const int grid = std::min(ntiles, num_sms);
+    const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
+    func_smem_once((const void *)gemm_3xtf32_kernel, smem);
+    launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)M,
+              (int)K, 3, 1);
 }
 
 // The hi/lo split of the A operand alone (M x K rows at A, lda) into scratch, in the layout
