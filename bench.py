@@ -415,6 +415,61 @@ def other_configs(mp, args, dev):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     log("C4")
+    # SPD variant (NEXT-1) at C3's size: A = G G^T / (2n), G n x 2n N(0,1), generated on the GPU
+    log("SPD")
+    ns = args.n
+    g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED + 7)
+    G = torch.randn((ns, 2 * ns), dtype=torch.float64, device=dev, generator=g)
+    As = (G @ G.t()) / (2.0 * ns)
+    del G
+    As = 0.5 * (As + As.t())                                       # symmetric bytes; column-major = row-major
+    xs = (torch.rand((1, ns), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+    Bs = (As @ xs).t().contiguous().t()
+    Asc = As.t()                                                    # (n, n) stride (1, n) view
+    mp.mp_dsposv_ex(Asc, Bs, None, mp.make_opts(), report=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    its = []
+    for _ in range(3):
+        _, it, _, _ = mp.mp_dsposv_ex(Asc, Bs, None, mp.make_opts(), report=False)
+        its.append(it)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_s = e0.elapsed_time(e1) / 3
+    _, it, _, rep = mp.mp_dsposv_ex(Asc, Bs, None, mp.make_opts(flags=2))
+    torch.cuda.synchronize()
+    kk = rep.kernels()
+    mp.mp_dposv_ex(Asc, Bs, None, mp.make_opts(), report=False)
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    mp.mp_dposv_ex(Asc, Bs, None, mp.make_opts(), report=False)
+    f1.record()
+    torch.cuda.synchronize()
+    ms64 = f0.elapsed_time(f1)
+    Ac = As.contiguous()
+    torch.linalg.cholesky(Ac)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    Lc = torch.linalg.cholesky(Ac)
+    torch.cholesky_solve(Bs.contiguous(), Lc)
+    c1.record()
+    torch.cuda.synchronize()
+    tr = kk.get("trail", {"ms": 0, "work": 0})
+    rr = kk.get("residual", {"ms": 0, "work": 0})
+    spd_flops = ns ** 3 / 3.0
+    res["SPD_C3"] = {"n": ns, "matrix": "Wishart G G^T/(2n), G n x 2n N(0,1) (kappa ~ 34)", "ms": round(ms_s, 3),
+                     "gflops_n3_over_3": round(spd_flops / ms_s / 1e6, 1), "iters": its,
+                     "factor_ms": round(rep.t_factor_ms, 3), "refine_ms": round(rep.t_refine_ms, 3),
+                     "fp64_ms": round(ms64, 3), "speedup_vs_fp64": round(ms64 / ms_s, 3),
+                     "cusolver_dpotrf_dpotrs_ms": round(c0.elapsed_time(c1), 3),
+                     "syrk_tensor_tflops": round(3 * tr["work"] / tr["ms"] / 1e9, 1) if tr["ms"] else None,
+                     "symv_residual_gbs": round(rr["work"] / rr["ms"] / 1e6, 1) if rr["ms"] else None,
+                     "kernels_ms": {k: [round(v["ms"], 3), v["launches"]] for k, v in kk.items()}}
+    del As, Ac, Lc, Bs, Asc
+    torch.cuda.empty_cache()
     # C4: n = 49152, nrhs = 16 (A = 19.3 GB fp64), device-generated with a seeded torch generator
     if not args.no_c4:
         n4, r4 = 49152, 16

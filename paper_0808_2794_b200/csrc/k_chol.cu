@@ -144,12 +144,23 @@ demote_sym_kernel(const double *__restrict__ A, int64_t lda, int64_t n, T *__res
 }
 
 // ---------------------------------------------------------------- C2 diagonal-block Cholesky
+// The w x w diagonal block lives in shared memory as a packed lower triangle (row r contiguous:
+// element (r, k) at r (r + 1) / 2 + k).  Left-looking by 32-column chunks c, three barriers each:
+//   (1) columns of chunk c, rows [32c, w): a_rj -= sum_{k < 32c} l_rk l_jk   (dot products)
+//   (2) one warp factors the 32 x 32 diagonal sub-block: lane i holds row i in registers; per
+//       column j every lane forms l_jj = sqrt(a_jj) itself (IEEE), divides (IEEE), and applies
+//       the column to its row with the other lanes' l_kj obtained by shuffles
+//   (3) rows below the sub-block (within the block): thread-per-row forward substitution with
+//       the 32 x 32 factor: l_rj = (a_rj - sum_{i < j} l_ri l_ji) / l_jj.
+// The operations per entry are the oracle's (square root, division, products and differences;
+// FMA-contracted: reading A-8), only grouped by chunk, so the exact family stays bitwise.
 __host__ __device__ constexpr int pk(int i, int j) { return i * (i + 1) / 2 + j; }   // packed lower, j <= i
+
+constexpr int PTHREADS = 512;
+constexpr int CW = 32;           // chunk width
 
 template <typename T>
 __device__ __forceinline__ T sqrt_rn(T x) { return sqrt(x); }
-
-constexpr int PTHREADS = 1024;
 
 template <typename T>
 __global__ void __launch_bounds__(PTHREADS)
@@ -157,46 +168,115 @@ potrf_diag_kernel(T *__restrict__ W, int64_t ldw, int64_t k, int w, DevStatus *s
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *P = reinterpret_cast<T *>(smem_raw);                       // packed lower, w (w + 1) / 2
-    T *D = P + pk(w, 0);                                          // the computed l_jj
+    T *LT = P + pk(w, 0);                                         // [w][CW] chunk rows, transposed
     pdl_wait();
     pdl_trigger();
-    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = PTHREADS / 32;
     T *Wd = W + k * ldw + k;
-    for (int i = ty; i < w; i += PTHREADS / 32)
-        for (int j = tx; j <= i; j += 32) P[pk(i, j)] = Wd[(int64_t)i * ldw + j];
+    for (int i = warp; i < w; i += NW)
+        for (int j = lane; j <= i; j += 32) P[pk(i, j)] = Wd[(int64_t)i * ldw + j];
     __syncthreads();
-    for (int j = 0; j < w; ++j) {
-        // every thread forms l_jj itself (IEEE sqrt: identical everywhere); a non-positive pivot
-        // is recorded (reading C-1) and replaced by 1 so the rest stays finite (the driver falls back)
-        const T d = P[pk(j, j)];
-        const bool ok = d > T(0);
-        const T l = ok ? sqrt_rn(d) : T(1);
-        if (tid == 0) {
-            D[j] = l;
-            if (!ok) {
-                atomicOr(&st->flags, (int)ST_ZERO_PIVOT);
-                atomicMin(&st->zero_col, (int)(k + j + 1));
+    for (int c0 = 0; c0 < w; c0 += CW) {
+        const int cw = min(CW, w - c0);
+        // (1) left-looking update of the chunk's columns, rows [c0, w): the chunk's L rows are first
+        //     copied transposed (LT[kk][j], lanes read consecutive j: no bank conflicts); a thread
+        //     owns 4 rows of one column (4 independent chains, the row operands broadcast)
+        if (c0 > 0) {
+            for (int idx = tid; idx < c0 * CW; idx += PTHREADS) {
+                const int kk = idx / CW, j = idx % CW;
+                LT[idx] = j < cw ? P[pk(c0 + j, kk)] : T(0);
             }
+            __syncthreads();
+            const int rows = w - c0, ngr = (rows + 3) / 4;
+            for (int o = tid; o < ngr * CW; o += PTHREADS) {
+                const int j = o % CW, rb = c0 + 4 * (o / CW);
+                if (j >= cw) continue;
+                const int jr = c0 + j;
+                T acc[4];
+                const T *lr[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = min(rb + q, w - 1);
+                    lr[q] = P + pk(r, 0);
+                    acc[q] = (rb + q < w && jr <= rb + q) ? P[pk(rb + q, jr)] : T(0);
+                }
+#pragma unroll 4
+                for (int kk = 0; kk < c0; ++kk) {
+                    const T l = LT[kk * CW + j];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[q] = fma(-lr[q][kk], l, acc[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (rb + q < w && jr <= rb + q) P[pk(rb + q, jr)] = acc[q];
+            }
+            __syncthreads();
         }
-        for (int i = j + 1 + tid; i < w; i += PTHREADS) P[pk(i, j)] = P[pk(i, j)] / l;   // IEEE division
+        // (2) the cw x cw diagonal sub-block, one warp
+        if (warp == 0) {
+            T row[CW];
+#pragma unroll
+            for (int j = 0; j < CW; ++j) row[j] = (lane < cw && j <= lane) ? P[pk(c0 + lane, c0 + j)] : T(0);
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                if (j < cw) {
+                    const T d = __shfl_sync(0xffffffffu, row[j], j);
+                    const bool ok = d > T(0);
+                    const T l = ok ? sqrt_rn(d) : T(1);
+                    if (lane == 0 && !ok) {
+                        atomicOr(&st->flags, (int)ST_ZERO_PIVOT);
+                        atomicMin(&st->zero_col, (int)(k + c0 + j + 1));
+                    }
+                    if (lane == j) row[j] = l;
+                    else if (lane > j) row[j] = row[j] / l;               // IEEE division
+                    const T lij = row[j];
+#pragma unroll
+                    for (int kk = j + 1; kk < CW; ++kk) {
+                        const T lkj = __shfl_sync(0xffffffffu, row[j], kk);
+                        if (lane >= kk && kk < cw) row[kk] = fma(-lij, lkj, row[kk]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CW; ++j)
+                if (lane < cw && j <= lane) P[pk(c0 + lane, c0 + j)] = row[j];
+        }
         __syncthreads();
-        // a_ic -= l_ij l_cj for j < c <= i (lower part of the trailing block)
-        for (int i = j + 1 + ty; i < w; i += PTHREADS / 32) {
-            const T lij = P[pk(i, j)];
-            for (int c = j + 1 + tx; c <= i; c += 32) P[pk(i, c)] = fma(-lij, P[pk(c, j)], P[pk(i, c)]);
+        // (3) rows below the sub-block: forward substitution with the cw x cw factor
+        for (int r = c0 + cw + tid; r < w; r += PTHREADS) {
+            // substitution in place in the row's packed storage (no unrolled register array:
+            // the kernel stays small enough for the instruction cache)
+            T *xr = P + pk(r, c0);
+#pragma unroll 1
+            for (int j = 0; j < cw; ++j) {
+                const T *lj = P + pk(c0 + j, c0);
+                T a = xr[j], b = T(0);                 // two interleaved partial sums (even / odd i)
+                int i = 0;
+#pragma unroll 2
+                for (; i + 1 < j; i += 2) {
+                    a = fma(-xr[i], lj[i], a);
+                    b = fma(-xr[i + 1], lj[i + 1], b);
+                }
+                if (i < j) a = fma(-xr[i], lj[i], a);
+                xr[j] = (a + b) / lj[j];                   // IEEE division
+            }
         }
         __syncthreads();
     }
-    // L11 into the lower block (diagonal: l_jj), L11^T into the upper block
-    for (int i = ty; i < w; i += PTHREADS / 32)
-        for (int j = tx; j <= i; j += 32) {
-            const T v = (i == j) ? D[j] : P[pk(i, j)];
+    // L11 into the lower block, L11^T into the upper block
+    for (int i = warp; i < w; i += NW)
+        for (int j = lane; j <= i; j += 32) {
+            const T v = P[pk(i, j)];
             Wd[(int64_t)i * ldw + j] = v;
             Wd[(int64_t)j * ldw + i] = v;
         }
 }
 
 // ---------------------------------------------------------------- C3 L21 = A21 L11^-T
+// One CTA per 64 rows of L21, the rows in shared memory.  Left-looking by 32-column chunks:
+//   (1) X[:, chunk] -= X[:, 0:32c] L11[chunk, 0:32c]^T   (dot products; L11's chunk rows staged)
+//   (2) thread-per-row substitution with the 32 x 32 diagonal factor of the chunk.
 constexpr int TRB = 64;          // rows per CTA
 constexpr int TTHREADS = 256;
 
@@ -205,29 +285,73 @@ __global__ void __launch_bounds__(TTHREADS)
 trsm_chol_kernel(T *__restrict__ W, int64_t ldw, int64_t k, int w, int64_t n)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    T *Ls = reinterpret_cast<T *>(smem_raw);                      // packed lower L11
-    T *X = Ls + pk(w, 0);                                         // [TRB][w + 1]
     const int ldx = w + 1;
+    T *X = reinterpret_cast<T *>(smem_raw);                       // [TRB][w + 1]
+    T *LcT = X + round_up((int64_t)TRB * ldx, 4);                 // [w][CW]: L11 rows of the chunk, transposed
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x;
     const int64_t r0 = k + w + (int64_t)blockIdx.x * TRB;
     const int nr = (int)std::min<int64_t>(TRB, n - r0);
     const T *Wd = W + k * ldw + k;
-    for (int i = tid / 32; i < w; i += TTHREADS / 32)
-        for (int j = tid % 32; j <= i; j += 32) Ls[pk(i, j)] = Wd[(int64_t)i * ldw + j];
     for (int idx = tid; idx < TRB * w; idx += TTHREADS) {
         const int r = idx / w, c = idx - r * w;
         X[r * ldx + c] = r < nr ? W[(r0 + r) * ldw + k + c] : T(0);
     }
-    __syncthreads();
-    for (int j = 0; j < w; ++j) {
-        if (tid < TRB) X[tid * ldx + j] = X[tid * ldx + j] / Ls[pk(j, j)];     // IEEE division
+    for (int c0 = 0; c0 < w; c0 += CW) {
+        const int cw = min(CW, w - c0);
+        for (int idx = tid; idx < (c0 + cw) * CW; idx += TTHREADS) {           // the chunk's rows of L11,
+            const int kk = idx / CW, j = idx % CW;                              // transposed: LcT[kk][j]
+            LcT[idx] = j < cw ? Wd[(int64_t)(c0 + j) * ldw + kk] : T(0);
+        }
         __syncthreads();
-        const int nc = w - j - 1;
-        for (int idx = tid; idx < TRB * nc; idx += TTHREADS) {
-            const int r = idx / nc, c = j + 1 + (idx - r * nc);
-            X[r * ldx + c] = fma(-Ls[pk(c, j)], X[r * ldx + j], X[r * ldx + c]);
+        if (c0 > 0) {
+            // thread -> 2 rows x 4 chunk columns (8 independent chains; 16-byte loads of LcT)
+            const int r = 2 * (tid >> 3), jg = (tid & 7) * 4;
+            T acc[2][4];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[a][q] = X[(r + a) * ldx + c0 + jg + q];
+#pragma unroll 4
+            for (int kk = 0; kk < c0; ++kk) {
+                const T x0 = X[r * ldx + kk], x1 = X[(r + 1) * ldx + kk];
+                T l[4];
+                if constexpr (sizeof(T) == 4) {
+                    const float4 v = *reinterpret_cast<const float4 *>(LcT + kk * CW + jg);
+                    l[0] = v.x; l[1] = v.y; l[2] = v.z; l[3] = v.w;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) l[q] = LcT[kk * CW + jg + q];
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[0][q] = fma(-x0, l[q], acc[0][q]);
+                    acc[1][q] = fma(-x1, l[q], acc[1][q]);
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (jg + q < cw) X[(r + a) * ldx + c0 + jg + q] = acc[a][q];
+            __syncthreads();
+        }
+        if (tid < TRB) {
+            T *xr = X + tid * ldx + c0;
+#pragma unroll 1
+            for (int j = 0; j < cw; ++j) {
+                const T *lj = LcT + c0 * CW + j;           // lj[i * CW] = L11(c0 + j, c0 + i)
+                T a = xr[j], b = T(0);
+                int i = 0;
+#pragma unroll 2
+                for (; i + 1 < j; i += 2) {
+                    a = fma(-xr[i], lj[i * CW], a);
+                    b = fma(-xr[i + 1], lj[(i + 1) * CW], b);
+                }
+                if (i < j) a = fma(-xr[i], lj[i * CW], a);
+                xr[j] = (a + b) / lj[j * CW];              // IEEE division
+            }
         }
         __syncthreads();
     }
@@ -379,8 +503,9 @@ int chol_block_max() { return sizeof(T) == 4 ? 256 : 128; }
 template <typename T>
 void launch_potrf_diag(T *W, int64_t ldw, int64_t k, int w, DevStatus *st, cudaStream_t s)
 {
-    const size_t smem = ((size_t)pk(w, 0) + (size_t)w) * sizeof(T);
-    func_smem_once((const void *)potrf_diag_kernel<T>, (size_t)(pk(chol_block_max<T>(), 0) + chol_block_max<T>()) * sizeof(T));
+    const int wm = chol_block_max<T>();
+    const size_t smem = ((size_t)pk(w, 0) + (size_t)w * CW) * sizeof(T);
+    func_smem_once((const void *)potrf_diag_kernel<T>, ((size_t)pk(wm, 0) + (size_t)wm * CW) * sizeof(T));
     launch_ex(potrf_diag_kernel<T>, dim3(1), dim3(PTHREADS), smem, s, nullptr, W, ldw, k, w, st);
 }
 
@@ -390,9 +515,9 @@ void launch_trsm_chol(T *W, int64_t ldw, int64_t k, int w, int64_t n, cudaStream
     const int64_t m = n - k - w;
     if (m <= 0) return;
     const int wm = chol_block_max<T>();
-    const size_t smem_max = ((size_t)pk(wm, 0) + (size_t)TRB * (wm + 1)) * sizeof(T);
-    func_smem_once((const void *)trsm_chol_kernel<T>, smem_max);
-    const size_t smem = ((size_t)pk(w, 0) + (size_t)TRB * (w + 1)) * sizeof(T);
+    auto bytes = [](int ww) { return (round_up((int64_t)TRB * (ww + 1), 4) + (size_t)ww * CW) * sizeof(T); };
+    func_smem_once((const void *)trsm_chol_kernel<T>, bytes(wm));
+    const size_t smem = bytes(w);
     launch_ex(trsm_chol_kernel<T>, dim3((unsigned)ceil_div(m, TRB)), dim3(TTHREADS), smem, s, nullptr, W, ldw, k, w, n);
 }
 

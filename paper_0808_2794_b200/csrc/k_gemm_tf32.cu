@@ -150,10 +150,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16])
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+template <bool LOWER>
 __global__ void __launch_bounds__(GT, 1)
 gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_constant__ CUtensorMap tmUl,
                    const __grid_constant__ CUtensorMap tmLh, const __grid_constant__ CUtensorMap tmLl,
-                   float *__restrict__ C, int64_t ldc, int M, int N, int K, int terms, int lower)
+                   float *__restrict__ C, int64_t ldc, int M, int N, int K, int terms)
 {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     // 1024-byte aligned ring (SWIZZLE_128B atoms)
@@ -165,11 +166,12 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
     const int tiles_n = (N + TM_COLS - 1) / TM_COLS, tiles_m = (M + TM_ROWS - 1) / TM_ROWS;
     const int ntiles = tiles_n * tiles_m;
     const int nk = (K + KC - 1) / KC;
-    // lower != 0 (the SPD path's SYRK, C square with its diagonal at i == j): tiles entirely above
+    // LOWER (the SPD path's SYRK, C square with its diagonal at i == j): tiles entirely above
     // the diagonal (every row index below every column index) are skipped by all three roles
     auto skip = [&](int t) {
+        if constexpr (!LOWER) return false;
         const int tn = t % tiles_n, tm = t / tiles_n;
-        return lower && tm * TM_ROWS + TM_ROWS - 1 < tn * TM_COLS;
+        return tm * TM_ROWS + TM_ROWS - 1 < tn * TM_COLS;
     };
 
     if (threadIdx.x == 0) {
@@ -403,9 +405,9 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
     const int ntiles = (int)(ceil_div(N, TM_COLS) * ceil_div(M, TM_ROWS));
     const int grid = std::min(ntiles, num_sms);
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
-    func_smem_once((const void *)gemm_3xtf32_kernel, smem);
-    launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)N,
-              (int)K, terms, 0);
+    func_smem_once((const void *)gemm_3xtf32_kernel<false>, smem);
+    launch_ex(gemm_3xtf32_kernel<false>, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M,
+              (int)N, (int)K, terms);
 }
 
 // SPD path: C[M x M] (lower tiles) -= L21 L21^T with L21 = A[M x K] (row-major, lda).  The B operand of
@@ -427,9 +429,9 @@ void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc
     const int ntiles = (int)(ceil_div(M, TM_COLS) * ceil_div(M, TM_ROWS));
     const int grid = std::min(ntiles, num_sms);
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
-    func_smem_once((const void *)gemm_3xtf32_kernel, smem);
-    launch_ex(gemm_3xtf32_kernel, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M, (int)M,
-              (int)K, 3, 1);
+    func_smem_once((const void *)gemm_3xtf32_kernel<true>, smem);
+    launch_ex(gemm_3xtf32_kernel<true>, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M,
+              (int)M, (int)K, 3);
 }
 
 // The hi/lo split of the A operand alone (M x K rows at A, lda) into scratch, in the layout
