@@ -169,9 +169,11 @@ struct LoopbackComm final : Comm {
         MP_CUDA(cudaStreamSynchronize(s));
         sh->send[rank] = send;
         sh->barrier();
-        for (int r = 0; r < size; ++r)
-            MP_CUDA(cudaMemcpyAsync(static_cast<char *>(recv) + (size_t)r * bytes, sh->send[r], bytes,
-                                    cudaMemcpyDeviceToDevice, s));
+        for (int r = 0; r < size; ++r) {
+            char *dst = static_cast<char *>(recv) + (size_t)r * bytes;
+            if (dst != sh->send[r])                  // in place (NCCL's convention): own chunk already there
+                MP_CUDA(cudaMemcpyAsync(dst, sh->send[r], bytes, cudaMemcpyDeviceToDevice, s));
+        }
         MP_CUDA(cudaStreamSynchronize(s));
         sh->barrier();
     }

@@ -1695,9 +1695,29 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
             if (!(solve_inverses_cond(inv, n, s) <= kInvCondMax)) inv = nullptr;
         }
         used_inv = inv != nullptr;
-        prof_begin(KC_SOLVE, s);
-        launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 0, ss, s, inv);
-        prof_end(KC_SOLVE, 4.0 * n * n, s);
+        // With nrhs >= P the triangular solves are split by right-hand-side column: rank r solves
+        // (and updates x for) columns [r cpr, (r + 1) cpr) only, then the solution columns are
+        // all-gathered, so the refinement's O(n^2 nrhs) solve work scales with P (C4: nrhs = 16).
+        // MP_DIST_REPLICATED_SOLVES=1: every rank solves every column (the round-1 scheme).
+        static const bool replicated = std::getenv("MP_DIST_REPLICATED_SOLVES") != nullptr;
+        const bool split = d.P > 1 && nrhs >= d.P && !replicated;
+        const int64_t cpr = split ? ceil_div(nrhs, (int64_t)d.P) : nrhs;
+        const int64_t c_lo = split ? std::min<int64_t>(nrhs, (int64_t)d.r * cpr) : 0;
+        const int64_t nc = split ? std::max<int64_t>(0, std::min<int64_t>(nrhs, c_lo + cpr) - c_lo) : nrhs;
+        double *Zg = split ? pool.get<double>((size_t)n * cpr * d.P) : nullptr;
+        auto solve = [&](int accumulate) {
+            prof_begin(KC_SOLVE, s);
+            if (nc > 0) launch_lu_solve<float>(Wf, ldf, n, nc, Y + c_lo * n, X + c_lo * n, accumulate, ss, s, inv);
+            prof_end(KC_SOLVE, 4.0 * n * n, s);
+            if (split) {
+                if (nc > 0)
+                    MP_CUDA(cudaMemcpyAsync(Zg + (size_t)d.r * cpr * n, X + c_lo * n, (size_t)n * nc * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, s));
+                cm.allgather(Zg + (size_t)d.r * cpr * n, Zg, (size_t)n * cpr * sizeof(double), s);
+                MP_CUDA(cudaMemcpyAsync(X, Zg, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            }
+        };
+        solve(0);
         code = -31;
         const int gblk = (int)std::min<int64_t>(ceil_div(d.nloc * nrhs, 256), 4096);
         for (int it = 0; it <= itermax; ++it) {
@@ -1720,9 +1740,7 @@ int dsgesv_1dbc_impl(Comm &cm, int64_t n, int64_t nrhs, int64_t nb, const double
             hist[nhist++] = st.ratio;
             if (st.converged) { *iters = it; code = 0; break; }
             if (it == itermax) break;
-            prof_begin(KC_SOLVE, s);
-            launch_lu_solve<float>(Wf, ldf, n, nrhs, Y, X, 1, ss, s, inv);
-            prof_end(KC_SOLVE, 4.0 * n * n, s);
+            solve(1);
         }
         t_ref = tm.mark();
     }

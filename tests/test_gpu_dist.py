@@ -151,3 +151,18 @@ def test_nccl_p1_communicator(mp):
     kappa = np.linalg.cond(A)
     assert info64 == infoo == 0
     assert np.abs(X64 - Xo).max() / np.abs(Xo).max() <= 8 * n * kappa * 2.0 ** -53
+
+
+@pytest.mark.parametrize("nranks,n,nrhs,nb", [(2, 900, 2, 128), (3, 1100, 7, 128), (4, 1000, 16, 256)])
+def test_dist_split_rhs_solves(mp, nranks, n, nrhs, nb):
+    """nrhs >= P: each rank solves its own right-hand-side columns and the solution is all-gathered
+    (the refinement's solve work scales with P).  Same verdicts as the oracle, every rank holds the
+    same X."""
+    A, B, Xt = inputs.gaussian(n, nrhs=nrhs, seed=n + nranks)
+    ro = orc_mod.dsgesv(A, B)
+    res = run_dist(mp, A, B, nranks, nb)
+    X0 = res[0][0]
+    for Xg, it, info in res:
+        assert info == 0 and ro.info == 0 and abs(it - ro.iters) <= 1, (it, ro.iters)
+        assert np.array_equal(Xg, X0)
+    assert certificate_ok(A, X0, B)
