@@ -21,7 +21,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c"), os.path.join(_HERE, "oracle_dd.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O3", "-march=x86-64-v2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
            "-fPIC", "-shared", "-std=c11"]
@@ -68,6 +68,13 @@ def _load():
             lib.oracle_dposv.argtypes = [i64, i64, p, i64, p, p, pint]
             lib.oracle_dsposv_ex.argtypes = [i64, i64, p, i64, p, p, pint, pint, ctypes.c_int,
                                              p, pint, ctypes.POINTER(ctypes.c_double)]
+            pd = ctypes.POINTER(ctypes.c_double)
+            d = ctypes.c_double
+            lib.oracle_dd_two_sum.argtypes = [d, d, pd, pd]
+            lib.oracle_dd_two_prod.argtypes = [d, d, pd, pd]
+            lib.oracle_dd_add.argtypes = [d, d, d, d, pd, pd]
+            lib.oracle_dd_residual.argtypes = [i64, i64, p, i64, p, p, p, p, p]
+            lib.oracle_qdgesv_ex.argtypes = [i64, i64, p, i64, p, p, p, pint, pint, ctypes.c_int, p, pint]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -248,3 +255,55 @@ def dsposv(A, B, itermax: int = ITERMAX) -> Result:
     _load().oracle_dsposv_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), ctypes.byref(iters),
                              ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh), ctypes.byref(anrm))
     return Result(X.reshape(np.shape(B), order="F"), iters.value, info.value, hist[: nh.value].copy(), anrm.value)
+
+
+# ---------------------------------------------------------------------------- NEXT-4 (oracle_dd.c)
+# P:638-697 "Extension to Quadruple Precision" (QDGESV): binary64 LU + double-double residual / update.
+def dd_two_sum(a: float, b: float):
+    s, e = ctypes.c_double(), ctypes.c_double()
+    _load().oracle_dd_two_sum(a, b, ctypes.byref(s), ctypes.byref(e))
+    return s.value, e.value
+
+
+def dd_two_prod(a: float, b: float):
+    s, e = ctypes.c_double(), ctypes.c_double()
+    _load().oracle_dd_two_prod(a, b, ctypes.byref(s), ctypes.byref(e))
+    return s.value, e.value
+
+
+def dd_add(a, b):
+    s, e = ctypes.c_double(), ctypes.c_double()
+    _load().oracle_dd_add(a[0], a[1], b[0], b[1], ctypes.byref(s), ctypes.byref(e))
+    return s.value, e.value
+
+
+def dd_residual(A, Xh, Xl, B):
+    """R = B - A (Xh + Xl) in double-double: returns (Rh, Rl)."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    Xh = _fortran(Xh, np.float64).reshape(n, -1, order="F")
+    Xl = _fortran(Xl, np.float64).reshape(n, -1, order="F")
+    Rh, Rl = np.empty_like(Bm, order="F"), np.empty_like(Bm, order="F")
+    _load().oracle_dd_residual(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(Xh), _ptr(Xl), _ptr(Rh), _ptr(Rl))
+    return Rh, Rl
+
+
+class DDResult:
+    __slots__ = ("Xh", "Xl", "iters", "info", "hist")
+
+    def __init__(self, Xh, Xl, iters, info, hist):
+        self.Xh, self.Xl, self.iters, self.info, self.hist = Xh, Xl, iters, info, hist
+
+
+def qdgesv(A, B, itermax: int = ITERMAX) -> DDResult:
+    """QDGESV analog: binary64 GEPP, double-double residual and update, stop test Q-1."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F")
+    Xh, Xl = np.zeros_like(Bm, order="F"), np.zeros_like(Bm, order="F")
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(itermax + 1)
+    _load().oracle_qdgesv_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(Xh), _ptr(Xl), ctypes.byref(iters),
+                             ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh))
+    return DDResult(Xh, Xl, iters.value, info.value, hist[: nh.value].copy())
