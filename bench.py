@@ -415,6 +415,27 @@ def other_configs(mp, args, dev):
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     log("C4")
+    # NEXT-4: extended-precision refinement (QDGESV analog) on the C3 inputs
+    log("QD")
+    A, B, _ = inputs.gaussian(args.n, nrhs=1, seed=inputs.BASE_SEED)
+    dA, dB = mp.colmajor_cuda(A), mp.colmajor_cuda(B)
+    del A
+    mp.mp_qdgesv_ex(dA, dB, report=False)
+    torch.cuda.synchronize()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record()
+    _, _, itq, infoq, _ = mp.mp_qdgesv_ex(dA, dB, report=False)
+    q1.record()
+    torch.cuda.synchronize()
+    _, _, _, _, repq = mp.mp_qdgesv_ex(dA, dB, opts=mp.make_opts(flags=2))
+    torch.cuda.synchronize()
+    kq = repq.kernels()
+    rq = kq.get("residual", {"ms": 0, "work": 0})
+    res["QD_C3"] = {"n": args.n, "what": "binary64 LU + double-double residual/update (stop at 2^-104)",
+                    "ms": round(q0.elapsed_time(q1), 3), "iters": itq, "info": infoq,
+                    "factor_ms": round(repq.t_factor_ms, 3), "refine_ms": round(repq.t_refine_ms, 3),
+                    "dd_residual_gbs": round(rq["work"] / rq["ms"] / 1e6, 1) if rq["ms"] else None}
+    del dA, dB
     # SPD variant (NEXT-1) at C3's size: A = G G^T / (2n), G n x 2n N(0,1), generated on the GPU
     log("SPD")
     ns = args.n

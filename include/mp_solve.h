@@ -203,6 +203,23 @@ int mp_dposv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda,
 int mp_spotrf(int64_t n, const double *A, int64_t lda, float *L, int *info, const mp_opts *opts);
 int mp_dpotrf(int64_t n, const double *A, int64_t lda, double *L, int *info, const mp_opts *opts);
 
+/* ------------------------------------------------------------------------------------------
+ * Extended-precision refinement: "Extension to Quadruple
+ * Precision" — QDGESV factors A in binary64 (DGETRF), solves with DGETRS, and carries the residual
+ * r = b - A x (QGEMV) and the update x += z in quadruple precision, here double-double (reading
+ * Q-0: X = Xhi + Xlo, |Xlo| <= ulp(Xhi)/2, 106 significand bits).  Stop test (Q-1):
+ *     ||fl64(r_c)||_2 < ||Xhi_c||_2 * ||A||_F * 2^-104 * sqrt(n)  or  r_c == 0, for every column;
+ * at most 30 corrections; no fallback (Q-2): iters = -31 returns the last iterate.
+ * A (n x n, lda), B (n x nrhs, ld n): binary64, used exactly.  Xhi, Xlo: n x nrhs outputs, ld n,
+ * device or host (as mp_dsgesv), must not overlap A, B or each other (info -6 / -7).
+ * *info: 0; -i argument errors (-3 A NaN/Inf, -5 B NaN/Inf, -7 Xlo NULL/overlapping);
+ *   +k exact zero pivot at column k in the binary64 LU (X unspecified).
+ * *iters: >= 0 corrections applied; -31 no convergence (rows of X = the last iterate). */
+int mp_qdgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B,
+              double *Xhi, double *Xlo, int *iters, int *info);
+int mp_qdgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B,
+                 double *Xhi, double *Xlo, int *iters, int *info, const mp_opts *opts, mp_report *rep);
+
 /* Resolve the per-launch events recorded by calls made with opts.flags = 2|4 since the
  * last collection: fills rep->k_ms / k_work / k_launches (summed over those calls, all
  * other fields untouched) and clears the records.  Synchronises the device. */

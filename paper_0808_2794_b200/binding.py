@@ -72,6 +72,8 @@ lib.mp_dposv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi]
 lib.mp_dposv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
 lib.mp_spotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_dpotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
+lib.mp_qdgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _p, _pi, _pi]
+lib.mp_qdgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _p, _pi, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
 lib.mp_kernel_schur_update.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_kernel_schur_update_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_set_stream.argtypes = [_p]
@@ -93,7 +95,7 @@ lib.mp_dgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi]
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
             "mp_kernel_schur_update_f64", "mp_dsposv", "mp_dsposv_ex", "mp_dposv", "mp_dposv_ex", "mp_spotrf",
-            "mp_dpotrf",
+            "mp_dpotrf", "mp_qdgesv", "mp_qdgesv_ex",
             "mp_profile_collect", "mp_exec_info", "mp_get_unique_id", "mp_comm_init", "mp_comm_init_loopback",
             "mp_comm_destroy", "mp_1dbc_local_cols", "mp_dsgesv_1dbc", "mp_dsgesv_1dbc_ex", "mp_dgesv_1dbc")
 
@@ -255,6 +257,28 @@ def mp_dposv_ex(A, B, X=None, opts: Opts | None = None, report: bool = True):
                            ctypes.byref(opts) if opts is not None else None,
                            ctypes.byref(rep) if rep is not None else None))
     return X, info.value, rep
+
+
+def mp_qdgesv_ex(A, B, Xhi=None, Xlo=None, opts: Opts | None = None, report: bool = True):
+    """Extended-precision refinement (QDGESV analog): X = Xhi + Xlo (double-double);
+    returns (Xhi, Xlo, iters, info, Report|None)."""
+    n = A.shape[0]
+    nrhs = _nrhs(B, n)
+    if Xhi is None:
+        Xhi = _alloc_like_X(B, n, nrhs)
+    if Xlo is None:
+        Xlo = _alloc_like_X(B, n, nrhs)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(B, "B", False, n)
+    ph, _ = _ptr_ld(Xhi, "Xhi", False, n)
+    pl, _ = _ptr_ld(Xlo, "Xlo", False, n)
+    lib.mp_set_stream(_stream_of(A, B, Xhi))
+    it, info = ctypes.c_int(0), ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_qdgesv_ex(n, nrhs, pa, lda, pb, ph, pl, ctypes.byref(it), ctypes.byref(info),
+                            ctypes.byref(opts) if opts is not None else None,
+                            ctypes.byref(rep) if rep is not None else None))
+    return Xhi, Xlo, it.value, info.value, rep
 
 
 def _potrf(fn, dtype, A, opts):

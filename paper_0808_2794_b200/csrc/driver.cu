@@ -1286,6 +1286,127 @@ int potrf_impl(int64_t n, const double *A, int64_t lda, T *L, int *info, const m
     return MP_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-4: extended-precision refinement
+// PAPER.md P:638-697 ("Extension to Quadruple Precision", QDGESV): the binary64 LU (DGETRF) and
+// solves (DGETRS) of mp_dgesv, the residual r = b - A x and the update x += z in double-double
+// (reading Q-0), B:5's stop test with the double-double unit roundoff 2^-104 (Q-1), at most 30
+// corrections and no fallback (Q-2).  X = Xhi + Xlo.
+int qdgesv_impl(const Args &a, double *Xlo, int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0; *iters = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    if (check_args(a, info)) { if (rep) rep->info = *info; return MP_OK; }
+    if (a.n > 0 && a.nrhs > 0) {
+        const size_t xb = (size_t)a.n * a.nrhs * sizeof(double);
+        const size_t ab = (size_t)((a.n - 1) * a.lda + a.n) * sizeof(double);
+        if (!Xlo || overlaps(Xlo, xb, a.A, ab) || overlaps(Xlo, xb, a.B, xb) || overlaps(Xlo, xb, a.X, xb)) {
+            *info = -7;
+            if (rep) rep->info = -7;
+            return MP_OK;
+        }
+    }
+    if (a.n == 0 || a.nrhs == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int64_t n = a.n, nrhs = a.nrhs;
+    const int nb = o.nb > 0 ? o.nb : default_nb(n);
+    const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    check_size_limits(n);
+    cudaStream_t s = g_stream;
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = (o.flags & 8) ? ((1u << KC_TRAIL) | (1u << KC_RESIDUAL)) : ~0u;
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    Views v = stage_in(a, pool, s, true);
+    const bool lo_host = !is_device_ptr(Xlo);
+    double *XL = lo_host ? pool.get<double>((size_t)n * nrhs) : Xlo;
+    const int t_staged = tm.mark();
+    StatusIO sio(pool, s);
+    const int sms = num_sms();
+    const int64_t ldw = round_up(n, 64);
+    double *W = pool.get<double>((size_t)n * ldw);
+    int32_t *ipiv = pool.get<int32_t>(n), *perm = pool.get<int32_t>(n), *pinv = pool.get<int32_t>(n);
+    double *Y = pool.get<double>((size_t)n * nrhs), *Z = pool.get<double>((size_t)n * nrhs);
+    double *Rh = pool.get<double>((size_t)n * nrhs), *Rl = pool.get<double>((size_t)n * nrhs);
+    double *dds = pool.get<double>(dd_scratch_doubles(n, sms));
+    unsigned *cnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s));
+    SolveScratch ss{pool.get<unsigned>(solve_flag_words(n)), pool.get<double>((size_t)n * std::min<int64_t>(nrhs, 16)), 0u};
+    MP_CUDA(cudaMemsetAsync(ss.flags, 0, solve_flag_words(n) * sizeof(unsigned), s));
+    double *dpart = pool.get<double>((size_t)sms * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    {   // B finiteness
+        launch_init_perm(perm, n, s);
+        launch_permute_demote_rhs<double>(v.B, n, nrhs, perm, Y, sio.d, s);
+    }
+    // ||A||_F in binary64 (the demote kernel's sum of squares runs for the binary32 copy only:
+    // take it from a throw-away binary32 demotion into W's storage, then overwrite W)
+    launch_demote_transpose<float>(v.A, v.lda, n, reinterpret_cast<float *>(W), ldw, dpart, dcnt, sio.d, s);
+    DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) { *info = -3; if (rep) rep->info = -3; return MP_OK; }
+    if (st0.flags & ST_B_NONFINITE) { *info = -5; if (rep) rep->info = -5; return MP_OK; }
+    const double anrm = std::sqrt(st0.anrm2);
+    const double cte = anrm * std::ldexp(1.0, -104) * std::sqrt((double)n);     // reading Q-1
+    sio.reset();
+    launch_demote_transpose<double>(v.A, v.lda, n, W, ldw, nullptr, nullptr, sio.d, s);
+    const int t_dem = tm.mark();
+    run_factor<double>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s);                 // DGETRF
+    const int t_fac = tm.mark();
+    const DevStatus &st1 = sio.read();
+    int nhist = 0;
+    double hist[MP_HIST_MAX] = {0};
+    if (st1.flags & ST_ZERO_PIVOT) {
+        *info = st1.zero_col;
+    } else {
+        launch_invert_perm(perm, pinv, n, s);
+        launch_permute_demote_rhs<double>(v.B, n, nrhs, pinv, Y, sio.d, s);
+        prof_begin(KC_SOLVE, s);
+        launch_lu_solve<double>(W, ldw, n, nrhs, Y, v.X, 0, ss, s);                // x0 = DGETRS(b)
+        prof_end(KC_SOLVE, 8.0 * n * n, s);
+        MP_CUDA(cudaMemsetAsync(XL, 0, (size_t)n * nrhs * sizeof(double), s));
+        *iters = -31;
+        for (int it = 0; it <= itermax; ++it) {
+            prof_begin(KC_RESIDUAL, s);                                             // QGEMV (double-double)
+            launch_dd_residual(v.A, v.lda, n, nrhs, v.B, v.X, XL, Rh, Rl, pinv, Y, cte, dds, cnt, sio.d, sms, s);
+            prof_end(KC_RESIDUAL, 8.0 * n * n * nrhs, s);
+            const DevStatus &st = sio.read();
+            if (st.flags & ST_NORM_NONFINITE) break;
+            hist[nhist++] = st.ratio;
+            if (st.converged) { *iters = it; break; }
+            if (it == itermax) break;
+            prof_begin(KC_SOLVE, s);
+            launch_lu_solve<double>(W, ldw, n, nrhs, Y, Z, 0, ss, s);               // DGETRS(fl64(P r))
+            launch_dd_update(v.X, XL, Z, n * nrhs, s);                              // x += z (double-double)
+            prof_end(KC_SOLVE, 8.0 * n * n, s);
+        }
+    }
+    const int t_ref = tm.mark();
+    if (lo_host) MP_CUDA(cudaMemcpyAsync(Xlo, XL, (size_t)n * nrhs * sizeof(double), cudaMemcpyDeviceToHost, s));
+    finish_copy_out(a, v, s);
+    const int t_end = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->nb = nb; rep->variant = -1;
+        rep->anrm = anrm;
+        for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
+        rep->t_total_ms = tm.ms(t0, t_end);
+        rep->t_copy_ms = tm.ms(t0, t_staged);
+        rep->t_demote_ms = tm.ms(t_staged, t_dem);
+        rep->t_factor_ms = tm.ms(t_dem, t_fac);
+        rep->t_refine_ms = tm.ms(t_fac, t_ref);
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        if (!g_prof.deferred) prof_collect(rep);
+    }
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
+    return MP_OK;
+}
+
 // ------------------------------------------------------------------ 1D block-cyclic multi-GPU path
 // SURVEY 8(e) / B:5: global column block j (nb columns) lives on rank j mod P at local slot
 // j / P; A (binary64, caller's) and the working copy use the same distribution; B, X, r, z,
@@ -1881,6 +2002,20 @@ int mp_spotrf(int64_t n, const double *A, int64_t lda, float *L, int *info, cons
 int mp_dpotrf(int64_t n, const double *A, int64_t lda, double *L, int *info, const mp_opts *opts)
 {
     return guarded([&] { return potrf_impl<double>(n, A, lda, L, info, opts); });
+}
+
+int mp_qdgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *Xhi, double *Xlo,
+              int *iters, int *info)
+{
+    if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return qdgesv_impl(Args{n, nrhs, lda, A, B, Xhi}, Xlo, iters, info, nullptr, nullptr); });
+}
+
+int mp_qdgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B, double *Xhi, double *Xlo,
+                 int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return qdgesv_impl(Args{n, nrhs, lda, A, B, Xhi}, Xlo, iters, info, opts, rep); });
 }
 
 int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,

@@ -318,3 +318,12 @@ void launch_symv_products(const double *A, int64_t lda, int64_t n, int64_t nrhs,
 void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc, int64_t M, int64_t K, float *scratch,
                               int num_sms, cudaStream_t s);
 }  // namespace mp
+
+namespace mp {
+// ---------------------------------------------------------------- NEXT-4 double-double refinement (k_dd.cu)
+size_t dd_scratch_doubles(int64_t n, int num_sms);
+void launch_dd_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, const double *B, const double *Xh,
+                        const double *Xl, double *Rh, double *Rl, const int32_t *pinv, double *Y, double cte,
+                        double *scratch, unsigned *counter, DevStatus *st, int num_sms, cudaStream_t s);
+void launch_dd_update(double *Xh, double *Xl, const double *Z, int64_t count, cudaStream_t s);
+}  // namespace mp
