@@ -509,10 +509,31 @@ struct Factor {
         panel(q, c0 + w1, w - w1, klo, khi);
     }
     // panel [k, k+w) on stream q, its panel-level pairs into buffer b
+    // Left-looking panel (binary32, w <= 256, MP_PANEL_LL=1 enables; off by default): the leaves run back to back,
+    // each bringing its own columns up to date (k_panel.cu ll_catch_up) on rows that stay at their
+    // panel-start positions; one interchange launch at the end moves the panel's rows to their
+    // final positions.  Replaces the recursive panel's in-panel interchanges, TRSMs and updates.
+    int32_t *lpos = nullptr;
+    bool ll_panel = false;
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
         cur_np = nppairs[b];                 // the first leaf zeroes it and starts orig[] as the identity
         emit_job = EmitJob{ps.orig, k, n, ppairs[b], nppairs[b]};
         emitted = false;
+        if (ll_panel && lpos && sizeof(T) == 4 && w <= 256) {
+            const int wl = panel_leaf_width<T>(n - k);
+            if (wl <= 0) throw std::runtime_error("matrix too tall for one panel cluster");
+            for (int64_t c0 = k; c0 < k + w; c0 += wl) {
+                const int ww = (int)std::min<int64_t>(wl, k + w - c0);
+                prof_begin(KC_PANEL, q);
+                launch_panel_leaf<T>(W, ldw, n, c0, ww, ipiv, ps, st, q, c0 == k ? cur_np : nullptr, k, lpos, k + w);
+                prof_end(KC_PANEL, (double)(n - c0) * ww * ww + 2.0 * (double)(n - k) * (c0 - k) * ww, q);
+            }
+            launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
+            prof_begin(KC_LASWP, q);
+            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, k, k + w, 0, 0, nullptr, q);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)w * sizeof(T), q);
+            return;
+        }
         panel(q, k, w, k, k + w);
         if (!emitted) launch_emit_pairs(ps.orig, k, n, ppairs[b], nppairs[b], q);
     }
@@ -649,6 +670,13 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
         f.tfU[1] = pool.get<float>(tf32_scratch_floats(n, nb));
     }
     f.ps.orig = pool.get<int32_t>(n);
+    // left-looking leaves (MP_PANEL_LL=1, experimental: bitwise-correct but slower than the recursive
+    // panel on B200)
+    static const bool ll_env = [] { const char *e = std::getenv("MP_PANEL_LL"); return e && e[0] == '1'; }();
+    if (sizeof(T) == 4 && ll_env && nb <= 256 && nb % 8 == 0) {   // (16-byte loads of the multipliers)
+        f.lpos = pool.get<int32_t>(n);
+        f.ll_panel = true;
+    }
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
     f.ps.ticket = pool.get<int32_t>(1);
@@ -1513,6 +1541,13 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     f.sms = num_sms();
     f.variant = variant;
     f.ps.orig = pool.get<int32_t>(n);
+    // left-looking leaves (MP_PANEL_LL=1, experimental: bitwise-correct but slower than the recursive
+    // panel on B200)
+    static const bool ll_env = [] { const char *e = std::getenv("MP_PANEL_LL"); return e && e[0] == '1'; }();
+    if (sizeof(T) == 4 && ll_env && nb <= 256 && nb % 8 == 0) {   // (16-byte loads of the multipliers)
+        f.lpos = pool.get<int32_t>(n);
+        f.ll_panel = true;
+    }
     f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
     f.ps.npairs = pool.get<int32_t>(1);
     f.ps.ticket = pool.get<int32_t>(1);

@@ -153,8 +153,10 @@ bool solve_fits(int64_t n);
 // and emits the leaf's (position <- position-at-leaf-start) pairs.
 template <typename T>
 // first_np != nullptr: the panel's first leaf (orig[] taken as the identity, *first_np zeroed)
+// ll_k / lpos (lpos != nullptr): left-looking leaf of the binary32 panel starting at ll_k (k_panel.cu)
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
-                       DevStatus *st, cudaStream_t s, int32_t *first_np = nullptr);
+                       DevStatus *st, cudaStream_t s, int32_t *first_np = nullptr, int64_t ll_k = 0,
+                       int32_t *lpos = nullptr, int64_t ll_kend = 0);
 void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs, int32_t *npairs, cudaStream_t s);
 
 // ---------------------------------------------------------------- K3 laswp (k_laswp.cu)

@@ -191,7 +191,194 @@ struct LeafArgs {
     DevStatus *st;
     int32_t *first_np;     // first leaf of a panel: orig[] is the identity (not read) and this
                            // panel-level pair counter is zeroed here
+    // Left-looking mode (ll != 0, see ll_catch_up): the panel [k, k + nb) keeps its rows at their
+    // panel-start (physical) positions while its leaves are factored; the leaf covers every row
+    // [k, n), brings its own columns up to date itself and records positions instead of moving rows
+    int ll;
+    long long k;           // panel start
+    long long kend;        // panel end (columns [k, kend))
+    int32_t *lpos;         // [n] logical position of the row physically at r (rows [k, n))
 };
+
+// NPMAX: previous pivots of the panel a left-looking leaf can catch up on (panels <= 256 wide)
+constexpr int LL_NPMAX = 256;
+constexpr int LL_LDL = LL_NPMAX + 4;
+template <typename T, int W>
+constexpr size_t ll_smem_bytes()
+{
+    const size_t pro = (size_t)LL_NPMAX * W, epi = (size_t)32 * LL_LDL + (size_t)LL_NPMAX * 16 + 32 * 16;
+    return sizeof(T) * (pro > epi ? pro : epi);
+}
+
+// Left-looking leaves (LeafArgs::ll).  The panel [k, kend) keeps its rows at their panel-start
+// (physical) positions while its leaves are factored (one interchange launch moves them at the end).
+// Invariants after leaf b (columns [c0, c0 + w)): the pivot rows orig[k .. c0 + w) hold their
+// multipliers in the columns left of their pivot and their U row in every column to the right,
+// including the panel's later columns; every other row holds its multipliers in [k, c0 + w) and its
+// panel-start values right of that.  Then SGETRF's in-panel update of a later leaf's columns
+// (step 1), reordered left-looking, is for an active row:
+//     x = A(row, leaf) - L(row, k : c0) U(k : c0, leaf)          (ll_catch_up, before the leaf)
+// and the U rows of the new pivots in the later columns are, per column c (ll_pivot_rows, after it):
+//     u(j, c) = A(piv_j, c) - sum_{i < c0 - k + j} L(piv_j, i) u(i, c)
+// (the earlier pivots' u(i, c) are in their rows), split over the cluster's CTAs by column.
+template <typename T, int NT, int RPT, int W>
+__device__ __forceinline__ void ll_catch_up(const LeafArgs<T> &a, long long base, int nn, T (&x)[RPT][W],
+                                            int (&org)[RPT], int (&cs)[RPT])
+{
+    // dynamic shared memory (ll_smem_bytes): U [LL_NPMAX][W]
+    extern __shared__ __align__(16) unsigned char ll_raw[];
+    T (*U)[W] = reinterpret_cast<T (*)[W]>(ll_raw);
+    __shared__ int prow[LL_NPMAX];
+    const int tid = threadIdx.x;
+    const long long k = a.k, c0 = a.c0, ldw = a.ldw;
+    const int np = (int)(c0 - k), w = a.w;
+    const T *W0 = a.W;
+    if (np > 0) {
+        // U(k : c0, leaf) from the earlier pivots' rows (all loads in flight, 16 bytes each)
+        for (int i = tid; i < np; i += NT) prow[i] = a.orig[k + i];
+        __syncthreads();
+        constexpr int QW = W / 4;
+        for (int o = tid; o < np * QW; o += NT) {
+            const int i = o / QW, s4 = (o - i * QW) * 4;
+            float4 v = *reinterpret_cast<const float4 *>(W0 + (long long)prow[i] * ldw + c0 + s4);
+            if (s4 + 3 >= w) {                      // partial leaf: zero the columns beyond w
+                if (s4 >= w) v.x = 0.f;
+                if (s4 + 1 >= w) v.y = 0.f;
+                if (s4 + 2 >= w) v.z = 0.f;
+                v.w = 0.f;
+            }
+            *reinterpret_cast<float4 *>(&U[i][s4]) = v;
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int li = tid + NT * q;
+        const bool valid = li < nn;
+        const long long r = base + li;
+        const int pos = valid ? (np == 0 ? (int)r : a.lpos[r]) : (int)r;
+        const bool active = valid && pos >= c0;
+        cs[q] = active ? pos : ~pos;
+        org[q] = (int)r;
+        const T *rowp = W0 + r * ldw + c0;
+        // active rows: panel-start values; pivot rows: their U row (written by earlier leaves)
+        if (valid && w == W) {
+#pragma unroll
+            for (int s4 = 0; s4 < W; s4 += 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(rowp + s4);
+                x[q][s4] = v.x; x[q][s4 + 1] = v.y; x[q][s4 + 2] = v.z; x[q][s4 + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int s = 0; s < W; ++s) x[q][s] = valid && s < w ? rowp[s] : T(0);
+        }
+    }
+    if (np > 0) {
+        // x -= L(row, k : c0) U for the active rows, 8 pivots at a time; the next 8 multipliers of every
+        // row are loaded (two 16-byte loads) while the current 8 are applied (U rows broadcast from
+        // shared memory); np is a multiple of 8
+        float4 nxt[RPT][2];
+        auto load8 = [&](int j) {
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                const int li = tid + NT * q;
+                const bool act = li < nn && cs[q] >= 0;
+                const float4 *src = reinterpret_cast<const float4 *>(W0 + (base + li) * ldw + k + j);
+                nxt[q][0] = act ? src[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+                nxt[q][1] = act ? src[1] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        };
+        load8(0);
+        for (int j = 0; j < np; j += 8) {
+            float lv[RPT][8];
+#pragma unroll
+            for (int q = 0; q < RPT; ++q) {
+                lv[q][0] = nxt[q][0].x; lv[q][1] = nxt[q][0].y; lv[q][2] = nxt[q][0].z; lv[q][3] = nxt[q][0].w;
+                lv[q][4] = nxt[q][1].x; lv[q][5] = nxt[q][1].y; lv[q][6] = nxt[q][1].z; lv[q][7] = nxt[q][1].w;
+            }
+            if (j + 8 < np) load8(j + 8);
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+#pragma unroll
+                for (int s4 = 0; s4 < W; s4 += 4) {
+                    const float4 u4 = *reinterpret_cast<const float4 *>(&U[j + jj][s4]);
+#pragma unroll
+                    for (int q = 0; q < RPT; ++q) {
+                        x[q][s4] = fma(-lv[q][jj], u4.x, x[q][s4]);
+                        x[q][s4 + 1] = fma(-lv[q][jj], u4.y, x[q][s4 + 1]);
+                        x[q][s4 + 2] = fma(-lv[q][jj], u4.z, x[q][s4 + 2]);
+                        x[q][s4 + 3] = fma(-lv[q][jj], u4.w, x[q][s4 + 3]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// After the leaf's rows are stored (and a cluster barrier): the U rows of the leaf's w new pivots
+// in the panel's later columns [c0 + w, kend), CTA g of CL taking a contiguous slice of them,
+// 16 columns per batch.  Shared memory (the same dynamic block): Lp [32][LL_LDL] the new pivots'
+// multipliers L(piv_j, k : c0 + w); Uo [LL_NPMAX][16] the earlier pivots' u(i, c); Tt [32][16].
+template <typename T, int NT, int W>
+__device__ __forceinline__ void ll_pivot_rows(const LeafArgs<T> &a, int g, int CL)
+{
+    extern __shared__ __align__(16) unsigned char ll_raw[];
+    T (*Lp)[LL_LDL] = reinterpret_cast<T (*)[LL_LDL]>(ll_raw);
+    T (*Uo)[16] = reinterpret_cast<T (*)[16]>(ll_raw + sizeof(T) * 32 * LL_LDL);
+    T (*Tt)[16] = reinterpret_cast<T (*)[16]>(ll_raw + sizeof(T) * (32 * LL_LDL + LL_NPMAX * 16));
+    __shared__ int prw[LL_NPMAX];
+    const int tid = threadIdx.x;
+    const long long k = a.k, c0 = a.c0, ldw = a.ldw;
+    const int np = (int)(c0 - k), w = a.w, nt = np + w;
+    const long long cs0 = c0 + w, ncols = a.kend - cs0;
+    if (ncols <= 0) return;
+    const long long per = (ncols + CL - 1) / CL;
+    const long long cb0 = cs0 + g * per, cb1 = min(a.kend, cb0 + per);
+    if (cb0 >= cb1) return;
+    T *W0 = a.W;
+    for (int i = tid; i < nt; i += NT) prw[i] = a.orig[k + i];
+    __syncthreads();
+    for (int o = tid; o < w * (nt / 4); o += NT) {           // multipliers of the new pivots (nt % 4 == 0)
+        const int j = o / (nt / 4), i4 = (o - j * (nt / 4)) * 4;
+        *reinterpret_cast<float4 *>(&Lp[j][i4]) =
+            *reinterpret_cast<const float4 *>(W0 + (long long)prw[np + j] * ldw + k + i4);
+    }
+    for (long long cb = cb0; cb < cb1; cb += 16) {
+        const int nc = (int)min(16LL, cb1 - cb);
+        for (int o = tid; o < np * 16; o += NT) {
+            const int i = o >> 4, cc = o & 15;
+            Uo[i][cc] = cc < nc ? W0[(long long)prw[i] * ldw + cb + cc] : T(0);
+        }
+        __syncthreads();
+        // the GEMM part: T(j, cc) = A(piv_j, c) - sum_{i < np} L(piv_j, i) u(i, c)
+        for (int o = tid; o < w * 16; o += NT) {
+            const int j = o >> 4, cc = o & 15;
+            T acc = cc < nc ? W0[(long long)prw[np + j] * ldw + cb + cc] : T(0);
+            for (int i = 0; i < np; ++i) acc = fma(-Lp[j][i], Uo[i][cc], acc);
+            Tt[j][cc] = acc;
+        }
+        __syncthreads();
+        // the triangle of the new pivots: warp 0, lane j holds row j of the 16-column batch; for each
+        // pivot jj (in order) the final row jj is broadcast by shuffles and applied to the rows below
+        if (tid < 32) {
+            const int j = tid;
+            T u[16];
+#pragma unroll
+            for (int cc = 0; cc < 16; ++cc) u[cc] = j < w ? Tt[j][cc] : T(0);
+#pragma unroll
+            for (int jj = 0; jj < W; ++jj) {
+                if (jj < w) {
+                    const T l = (j > jj && j < w) ? Lp[j][np + jj] : T(0);
+#pragma unroll
+                    for (int cc = 0; cc < 16; ++cc) u[cc] = fma(-l, __shfl_sync(0xffffffffu, u[cc], jj), u[cc]);
+                }
+            }
+            if (j < w)
+                for (int cc = 0; cc < nc; ++cc) W0[(long long)prw[np + j] * ldw + cb + cc] = u[cc];
+        }
+        __syncthreads();
+    }
+}
 
 // RPT rows per thread, leaf width W, column loop unrolled in groups of UG columns.
 //
@@ -204,7 +391,7 @@ struct LeafArgs {
 // the frame is rotated by UG after every group (W/UG rotations = identity at the end).
 // Slots s >= W - o*UG hold multipliers of earlier columns ("dead"); the staged pivot
 // row has them zeroed so the rank-1 update leaves them unchanged.
-template <typename T, int NT, int RPT, int W, int UG, bool MULTI, bool HW = true>
+template <typename T, int NT, int RPT, int W, int UG, bool MULTI, bool HW = true, bool LLK = false>
 __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 {
     constexpr int NWP = NT / 32;
@@ -229,7 +416,9 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     const long long n = a.n, c0 = a.c0, ldw = a.ldw;
     const int w = a.w;
     constexpr int R = NT * RPT;                  // rows per CTA
-    const long long base = c0 + (long long)g * R;
+    constexpr bool ll = LLK && sizeof(T) == 4;   // left-looking instantiation (LeafArgs::ll)
+    const long long rows0 = ll ? a.k : c0;       // left-looking: every row of the panel [k, n)
+    const long long base = rows0 + (long long)g * R;
     const int nn = (int)(n - base);              // rows of this CTA that exist: local index < nn
     const unsigned bytes_per_col = (unsigned)(CL * sizeof(SlotT));
 
@@ -247,6 +436,10 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     // cs[q]: the row's current logical position; bitwise-complemented (negative) once the row is
     // no longer active (it became a pivot row, or does not exist)
     int org[RPT], cs[RPT];
+    if constexpr (ll) {                         // (binary32 only: the binary64 leaves keep the recursive panel)
+        ll_catch_up<T, NT, RPT, W>(a, base, nn, x, org, cs);
+    }
+    if (!ll)
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
@@ -454,6 +647,16 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int li = tid + NT * q;
+        if (ll && li < nn) {               // left-looking: the row stays where it is; record its position
+            const long long pos = cs[q] >= 0 ? cs[q] : ~cs[q];
+            T *row = a.W + (base + li) * ldw + c0;
+#pragma unroll
+            for (int s = 0; s < W; ++s)
+                if (s < w) row[s] = x[q][s];
+            a.orig[pos] = (int32_t)(base + li);
+            a.lpos[base + li] = (int32_t)pos;
+            continue;
+        }
         if (li < nn) {
             const long long pos = cs[q] >= 0 ? cs[q] : ~cs[q];
             T *row = a.W + pos * ldw + c0;
@@ -478,6 +681,12 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                 a.pairs[2 * si] = (int32_t)pos;
                 a.pairs[2 * si + 1] = lorg;
             }
+        }
+    }
+    if constexpr (ll) {
+        if (a.kend > c0 + w) {
+            cluster.sync();                       // every CTA's multipliers and U rows are stored
+            ll_pivot_rows<T, NT, W>(a, g, CL);
         }
     }
 }
@@ -528,13 +737,18 @@ void launch_cfg(const LeafArgs<T> &a, int cl, cudaStream_t s)
     static const bool fullw = [] { const char *e = std::getenv("MP_LEAF_FULLW"); return e && e[0] == '1'; }();
     auto kern = cl > 1 ? (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, true, false> : panel_leaf_kernel<T, NT, RPT, W, UG, true>)
                        : (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, false, false> : panel_leaf_kernel<T, NT, RPT, W, UG, false>);
+    if constexpr (sizeof(T) == 4)
+        if (a.ll) kern = cl > 1 ? panel_leaf_kernel<T, NT, RPT, W, UG, true, true, true>
+                                : panel_leaf_kernel<T, NT, RPT, W, UG, false, true, true>;
     if (cl > 8) func_cluster16_once((const void *)kern);
+    const size_t dsm = a.ll ? ll_smem_bytes<T, W>() : 0;
+    if (a.ll) func_smem_once((const void *)kern, dsm);
     cudaLaunchAttribute at;
     at.id = cudaLaunchAttributeClusterDimension;
     at.val.clusterDim.x = cl;
     at.val.clusterDim.y = 1;
     at.val.clusterDim.z = 1;
-    launch_ex(kern, dim3(cl), dim3(NT), 0, s, &at, a);
+    launch_ex(kern, dim3(cl), dim3(NT), dsm, s, &at, a);
 }
 
 int cluster_size()
@@ -583,10 +797,12 @@ int panel_leaf_width(int64_t m)
 
 template <typename T>
 void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t *ipiv, PanelScratch &ps,
-                       DevStatus *st, cudaStream_t s, int32_t *first_np)
+                       DevStatus *st, cudaStream_t s, int32_t *first_np, int64_t ll_k, int32_t *lpos,
+                       int64_t ll_kend)
 {
     const int clmax = cluster_size();
-    const int64_t m = n - c0;
+    const bool ll = lpos != nullptr;
+    const int64_t m = n - (ll ? ll_k : c0);
     const int sel = select_cfg(sizeof(T), m, clmax);
     const LeafCfg *cfgs = sizeof(T) == 4 ? kCfgF : kCfgD;
     if (sel < 0 || w > cfgs[sel].w)
@@ -595,6 +811,9 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
     LeafArgs<T> a;
     a.W = W; a.ldw = ldw; a.n = n; a.c0 = c0; a.w = w; a.ipiv = ipiv;
     a.orig = ps.orig; a.pairs = ps.pairs; a.npairs = ps.npairs; a.st = st; a.first_np = first_np;
+    a.ll = ll ? 1 : 0; a.k = ll ? ll_k : c0; a.lpos = lpos; a.kend = ll ? ll_kend : c0 + w;
+    if (ll && (sizeof(T) != 4 || c0 - ll_k > LL_NPMAX - w))
+        throw CudaError{cudaErrorInvalidValue, "left-looking leaf: binary32 panels of at most 256 columns", __LINE__};
     if constexpr (sizeof(T) == 4) {
         switch (sel) {
         case 0: launch_cfg<T, MP_LEAF_C0>(a, cl, s); break;
@@ -621,8 +840,8 @@ void launch_emit_pairs(const int32_t *orig, int64_t k, int64_t n, int32_t *pairs
 template int panel_leaf_width<float>(int64_t);
 template int panel_leaf_width<double>(int64_t);
 template void launch_panel_leaf<float>(float *, int64_t, int64_t, int64_t, int, int32_t *, PanelScratch &,
-                                       DevStatus *, cudaStream_t, int32_t *);
+                                       DevStatus *, cudaStream_t, int32_t *, int64_t, int32_t *, int64_t);
 template void launch_panel_leaf<double>(double *, int64_t, int64_t, int64_t, int, int32_t *, PanelScratch &,
-                                        DevStatus *, cudaStream_t, int32_t *);
+                                        DevStatus *, cudaStream_t, int32_t *, int64_t, int32_t *, int64_t);
 
 }  // namespace mp

@@ -430,3 +430,39 @@ def test_solve_exchange_modes_bitwise(mp, tmp_path, n, nrhs, seed):
     it_f, info_f = map(int, r.stdout.split()[-2:])
     assert info == info_f == 0 and it == it_f
     assert np.array_equal(Xt.view(np.uint64), np.load(out).view(np.uint64))
+
+
+_LL_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_0808_2794_b200 import binding as mp, inputs
+import oracle
+n = int(sys.argv[2])
+A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n)
+LU, ipiv, info = mp.mp_sgetrf(A, mp.make_opts(nb=256))
+p = np.arange(n)
+for k, q in enumerate(ipiv):
+    p[k], p[q] = p[q], p[k]
+ok = info == 0 and np.array_equal(p, perm) and np.array_equal(np.tril(LU, -1).astype(float), np.tril(L, -1)) \
+     and np.array_equal(np.triu(LU).astype(float), U)
+A2, B2, _ = inputs.gaussian(n, nrhs=2, seed=n + 1)
+ro = oracle.dsgesv(A2, B2)
+Xg, it, info2, _ = mp.mp_dsgesv_ex(mp.colmajor_cuda(A2), mp.colmajor_cuda(B2))
+torch.cuda.synchronize()
+print(int(ok), it, ro.iters, info2)
+"""
+
+
+@pytest.mark.parametrize("n", [700, 2100])
+def test_left_looking_panel_option(mp, n):
+    """The experimental left-looking leaves (MP_PANEL_LL=1, read once per process: run in a child)
+    reproduce the exact-LU factors bitwise and refine Gaussian systems within one iteration of the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _LL_CHILD, root, str(n)], env=dict(os.environ, MP_PANEL_LL="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ok, it, it_or, info = map(int, r.stdout.split()[-4:])
+    assert ok == 1 and info == 0 and abs(it - it_or) <= 1
