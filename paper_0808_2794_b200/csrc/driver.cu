@@ -414,6 +414,22 @@ cudaEvent_t la_event(int i)
     return evs[i];
 }
 
+// one non-blocking host-to-device copy stream per device (the streamed e2e path)
+cudaStream_t copy_stream()
+{
+    static std::mutex mu;
+    static std::map<int, cudaStream_t> per_dev;
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = per_dev.find(dev);
+    if (it != per_dev.end()) return it->second;
+    cudaStream_t cs;
+    MP_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    per_dev.emplace(dev, cs);
+    return cs;
+}
+
 // ------------------------------------------------------------------ blocked GEPP
 // Right-looking blocked LU (SGETRF's structure): for every panel of nb
 // columns — recursive panel factorisation (cluster leaves K2 + in-panel K3/K4/K5),
@@ -515,6 +531,9 @@ struct Factor {
     // final positions.  Replaces the recursive panel's in-panel interchanges, TRSMs and updates.
     int32_t *lpos = nullptr;
     bool ll_panel = false;
+    // step range and column limit (the streamed e2e path factors column blocks as they arrive):
+    // panels k in [kb, ke), interchanges / U12 / Schur updates on columns [0, nc); rows always [0, n)
+    int64_t kb = 0, ke = -1, nc = -1;
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
         cur_np = nppairs[b];                 // the first leaf zeroes it and starts orig[] as the identity
         emit_job = EmitJob{ps.orig, k, n, ppairs[b], nppairs[b]};
@@ -539,18 +558,29 @@ struct Factor {
     }
     void run_sequential() {
         psms = sms;
-        launch_init_perm(perm, n, s);
-        for (int64_t k = 0; k < n; k += nb) {
-            const int w = (int)std::min<int64_t>(nb, n - k);
+        if (kb == 0) launch_init_perm(perm, n, s);
+        for (int64_t k = kb; k < ke; k += nb) {
+            const int w = (int)std::min<int64_t>(nb, ke - k);
             factor_panel(s, k, w, 0);
             // the panel's interchanges on every other column (left factors + trailing matrix)
             prof_begin(KC_LASWP, s);
-            launch_laswp_pairs<T>(W, ldw, ppairs[0], nppairs[0], 2 * w, 0, n, k, k + w, perm, s);
-            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w) * sizeof(T), s);
-            if (k + w < n) {
-                trsm(s, k, w, k + w, n);                                                   // U12 <- L11^-1 A12
-                gemm(s, k + w, k + w, k, n - k - w, n - k - w, w, true, KC_TRAIL, tf32[0], sms);   // A22 -= L21 U12
+            launch_laswp_pairs<T>(W, ldw, ppairs[0], nppairs[0], 2 * w, 0, nc, k, k + w, perm, s);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(nc - w) * sizeof(T), s);
+            if (k + w < nc) {
+                trsm(s, k, w, k + w, nc);                                                  // U12 <- L11^-1 A12
+                gemm(s, k + w, k + w, k, n - k - w, nc - k - w, w, true, KC_TRAIL, tf32[0], sms);   // A22 -= L21 U12
             }
+        }
+    }
+    // Bring the column block [c_lo, c_hi) (its rows already permuted by perm) up to date with the
+    // panels [0, c_lo): U12 and the Schur update of every earlier step, in order (the right-looking
+    // updates it missed while it was in flight; the later interchanges commute).
+    float *tfC = nullptr;                  // the catch-up's own 3xTF32 scratch (it may run beside the look-ahead)
+    void catch_up(int64_t c_lo, int64_t c_hi, cudaStream_t q, int nsm) {
+        for (int64_t k = 0; k < c_lo; k += nb) {
+            const int w = (int)std::min<int64_t>(nb, c_lo - k);
+            trsm(q, k, w, c_lo, c_hi);
+            gemm(q, k + w, c_lo, k, n - k - w, c_hi - c_lo, w, true, KC_TRAIL, tfC ? tfC : tf32[0], nsm);
         }
     }
     // Look-ahead (depth 1).  Step k:
@@ -581,15 +611,15 @@ struct Factor {
         MP_CUDA(cudaEventRecord(e0, s));
         MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
         MP_CUDA(cudaStreamWaitEvent(cur, e0, 0));
-        launch_init_perm(perm, n, cur);
-        factor_panel(sP, 0, (int)std::min<int64_t>(nb, n), 0);
+        if (kb == 0) launch_init_perm(perm, n, cur);
+        factor_panel(sP, kb, (int)std::min<int64_t>(nb, ke - kb), 0);
         MP_CUDA(cudaEventRecord(eP[0], sP));
-        split_ok[0] = split_l21(0, (int)std::min<int64_t>(nb, n), 0);
+        split_ok[0] = split_l21(kb, (int)std::min<int64_t>(nb, ke - kb), 0);
         int idx = 0;
-        for (int64_t k = 0; k < n; k += nb, ++idx) {
-            const int w = (int)std::min<int64_t>(nb, n - k);
+        for (int64_t k = kb; k < ke; k += nb, ++idx) {
+            const int w = (int)std::min<int64_t>(nb, ke - k);
             const int64_t kn = k + w;
-            const int wn = kn < n ? (int)std::min<int64_t>(nb, n - kn) : 0;
+            const int wn = kn < ke ? (int)std::min<int64_t>(nb, ke - kn) : 0;
             const int b = idx & 1;
             // early steps (large trailing matrix): the larger update partition
             const bool early = ex.sU2 && (double)(n - kn) > ex.big_frac * (double)n;
@@ -602,7 +632,7 @@ struct Factor {
                 cur = sU;
             }
             MP_CUDA(cudaStreamWaitEvent(sU, eP[b], 0));
-            if (kn < n) {
+            if (kn < ke) {
                 // the next panel's columns first (on the panel's critical path) ...
                 prof_begin(KC_LASWP, sU);
                 launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sU);
@@ -626,18 +656,18 @@ struct Factor {
             }
             // ... then every other column (left factors, rest of the trailing matrix), off it
             prof_begin(KC_LASWP, sU);
-            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, n, k, kn + wn, perm, sU);
-            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(n - w - wn) * sizeof(T), sU);
-            if (kn < n && kn + wn < n) {
+            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, nc, k, kn + wn, perm, sU);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(nc - w - wn) * sizeof(T), sU);
+            if (kn < nc && kn + wn < nc) {
                 const int kp = (int)round_up(w, 4);
-                const int64_t nr = n - kn - wn;
+                const int64_t nr = nc - kn - wn;
                 const bool bsplit = split_ok[b] && nr >= 128 && w <= 256;
                 float *bh = bsplit ? tfU[b] + 2 * (size_t)(n - kn) * kp : nullptr;
-                trsm(sU, k, w, kn + wn, n, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
+                trsm(sU, k, w, kn + wn, nc, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
                 const bool reuse = split_ok[b] || (kn < n && n - kn >= 256 && wn >= 128);
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
-                gemm(sU, kn, kn + wn, k, n - kn, n - kn - wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
+                gemm(sU, kn, kn + wn, k, n - kn, nc - kn - wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
                      reuse, terms, bsplit);
             }
         }
@@ -647,7 +677,9 @@ struct Factor {
         MP_CUDA(cudaStreamWaitEvent(s, eEndU, 0));
     }
     void run(bool lookahead) {
-        if (lookahead && n > 2 * (int64_t)nb) {
+        if (ke < 0) ke = n;
+        if (nc < 0) nc = n;
+        if (lookahead && ke - kb > 2 * (int64_t)nb) {
             const ExecRes &ex = exec_res();
             if (ex.ok) { run_lookahead(ex); return; }
         }
@@ -656,10 +688,9 @@ struct Factor {
 };
 
 template <typename T>
-void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
-                cudaStream_t s, int variant = MP_VARIANT_FFMA, bool lookahead = true)
+void make_factor(Factor<T> &f, T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st,
+                 Pool &pool, cudaStream_t s, int variant)
 {
-    Factor<T> f;
     f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
     f.sms = num_sms();
     f.variant = variant;
@@ -690,7 +721,68 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
     }
     f.ps.ppairs = f.ppairs[0];
     f.ps.nppairs = f.nppairs[0];
+}
+
+template <typename T>
+void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
+                cudaStream_t s, int variant = MP_VARIANT_FFMA, bool lookahead = true)
+{
+    Factor<T> f;
+    make_factor<T>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant);
     f.run(lookahead);
+}
+
+// e2e path with a host A: the 8 n^2 bytes of A cross PCIe in q column blocks on a copy
+// stream while the factorisation runs.  Block j (columns [c_lo, c_hi), multiples of nb) is demoted
+// when it lands (its ||A||_F^2 share saved to anrm_parts[j]), its rows put in the current row order
+// (perm) and brought up to date with the panels [0, c_lo) (catch_up), then its own panels are
+// factored with every update restricted to the columns that have arrived.  Same operations per
+// entry as the one-shot factorisation, reordered (the exact-LU family stays bitwise).
+void run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n, float *W, int64_t ldw, int nb,
+                         int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool, cudaStream_t s, int variant,
+                         bool lookahead, int nblocks, double *anrm_parts, cudaStream_t cs)
+{
+    Factor<float> f;
+    make_factor<float>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant);
+    if (variant == MP_VARIANT_3XTF32) f.tfC = pool.get<float>(tf32_scratch_floats(n, nb));
+    const int64_t nbk = ceil_div(n, (int64_t)nb);
+    const int64_t per = ceil_div(nbk, (int64_t)nblocks) * nb;                 // block width (multiple of nb)
+    float *S = pool.get<float>((size_t)n * round_up(per, 64));
+    double *dpart = pool.get<double>((size_t)num_sms() * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    std::vector<cudaEvent_t> ev;
+    {   // dA was allocated stream-ordered on s: the copy stream starts after that point of s
+        cudaEvent_t e0 = la_event(19);
+        MP_CUDA(cudaEventRecord(e0, s));
+        MP_CUDA(cudaStreamWaitEvent(cs, e0, 0));
+    }
+    for (int64_t c_lo = 0, j = 0; c_lo < n; c_lo += per, ++j) {
+        const int64_t c_hi = std::min(n, c_lo + per);
+        cudaEvent_t e = la_event(20 + (int)j);
+        MP_CUDA(cudaMemcpy2DAsync(dA + c_lo * n, n * sizeof(double), hA + c_lo * lda_h, lda_h * sizeof(double),
+                                  n * sizeof(double), c_hi - c_lo, cudaMemcpyHostToDevice, cs));
+        MP_CUDA(cudaEventRecord(e, cs));
+        ev.push_back(e);
+    }
+    const int sms = num_sms();
+    for (int64_t c_lo = 0, j = 0; c_lo < n; c_lo += per, ++j) {
+        const int64_t c_hi = std::min(n, c_lo + per), wcols = c_hi - c_lo;
+        MP_CUDA(cudaStreamWaitEvent(s, ev[j], 0));
+        prof_begin(KC_DEMOTE, s);
+        if (c_lo == 0) {
+            launch_demote_rect<float>(dA, n, n, wcols, W, ldw, dpart, dcnt, st, s);
+        } else {
+            const int64_t lds = round_up(wcols, 64);
+            launch_demote_rect<float>(dA + c_lo * n, n, n, wcols, S, lds, dpart, dcnt, st, s);
+            launch_gather_rows(S, lds, round_up(wcols, 4), perm, n, W + c_lo, ldw, s);
+        }
+        prof_end(KC_DEMOTE, 12.0 * n * wcols, s);
+        MP_CUDA(cudaMemcpyAsync(anrm_parts + j, &st->anrm2, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (c_lo > 0) f.catch_up(c_lo, c_hi, s, sms);
+        f.kb = c_lo; f.ke = c_hi; f.nc = c_hi;
+        f.run(lookahead);
+    }
 }
 
 struct Args {
@@ -707,13 +799,14 @@ struct Views {
     bool x_host;
 };
 
-Views stage_in(const Args &a, Pool &pool, cudaStream_t s, bool need_b)
+Views stage_in(const Args &a, Pool &pool, cudaStream_t s, bool need_b, bool defer_a = false)
 {
     Views v{a.A, a.B, a.X, a.lda, false};
     if (!is_device_ptr(a.A)) {
         double *d = pool.get<double>((size_t)a.n * a.n);
-        MP_CUDA(cudaMemcpy2DAsync(d, a.n * sizeof(double), a.A, a.lda * sizeof(double), a.n * sizeof(double),
-                                  a.n, cudaMemcpyHostToDevice, s));
+        if (!defer_a)                        // defer_a: the caller streams A in itself (run_factor_streamed)
+            MP_CUDA(cudaMemcpy2DAsync(d, a.n * sizeof(double), a.A, a.lda * sizeof(double), a.n * sizeof(double),
+                                      a.n, cudaMemcpyHostToDevice, s));
         v.A = d;
         v.lda = a.n;
     }
@@ -824,7 +917,12 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     const int t0 = tm.mark();
 
     Pool pool(s);
-    Views v = stage_in(a, pool, s, true);
+    // host A (the end-to-end path): stream it in by column blocks, overlapped with the factorisation
+    // (flags bit 6 or MP_NO_STREAM_H2D=1: one copy, then the factorisation)
+    static const bool no_stream = std::getenv("MP_NO_STREAM_H2D") != nullptr;
+    const bool stream_a = !is_device_ptr(a.A) && n >= 4096 && nb % 4 == 0 && !(o.flags & 64) && !no_stream &&
+                          !(o.flags & 1);
+    Views v = stage_in(a, pool, s, true, stream_a);
     const int t_staged = tm.mark();
     StatusIO sio(pool, s);
     const int sms = num_sms();
@@ -848,16 +946,34 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
 
     // ---- K1: demote + ||A||_F; B finiteness (identity scatter into Y, discarded)
-    prof_begin(KC_DEMOTE, s);
-    launch_demote_transpose<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);
-    prof_end(KC_DEMOTE, 12.0 * n * n, s);
-    launch_init_perm(perm, n, s);
-    launch_permute_demote_rhs<float>(v.B, n, nrhs, perm, Y, sio.d, s);
+    double anrm2_streamed = -1.0;
+    if (stream_a) {
+        // demote + step 1 as the column blocks of A land (the status is checked right after)
+        int32_t *ident = pool.get<int32_t>(n);
+        launch_init_perm(ident, n, s);
+        launch_permute_demote_rhs<float>(v.B, n, nrhs, ident, Y, sio.d, s);
+        static const int kBlocks = [] { const char *e = std::getenv("MP_STREAM_BLOCKS"); return e ? std::max(1, std::min(16, std::atoi(e))) : 4; }();
+        double *parts = pool.get<double>(17);
+        run_factor_streamed(a.A, a.lda, const_cast<double *>(v.A), n, W, ldw, nb, ipiv, perm, sio.d, pool, s,
+                            o.variant, (o.flags & 16) == 0, kBlocks, parts, copy_stream());
+        double hp[17] = {0};
+        MP_CUDA(cudaMemcpyAsync(hp, parts, sizeof(hp), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        anrm2_streamed = 0.0;
+        for (int j = 0; j < (int)ceil_div(ceil_div(n, (int64_t)nb), (int64_t)ceil_div(ceil_div(n, (int64_t)nb), kBlocks)); ++j)
+            anrm2_streamed += hp[j];
+    } else {
+        prof_begin(KC_DEMOTE, s);
+        launch_demote_transpose<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);
+        prof_end(KC_DEMOTE, 12.0 * n * n, s);
+        launch_init_perm(perm, n, s);
+        launch_permute_demote_rhs<float>(v.B, n, nrhs, perm, Y, sio.d, s);
+    }
     const int t_dem = tm.mark();
     DevStatus st0 = sio.read();
     if (st0.flags & ST_A_NONFINITE) { *info = -3; if (rep) rep->info = -3; return MP_OK; }
     if (st0.flags & ST_B_NONFINITE) { *info = -5; if (rep) rep->info = -5; return MP_OK; }
-    const double anrm = std::sqrt(st0.anrm2);
+    const double anrm = std::sqrt(stream_a ? anrm2_streamed : st0.anrm2);
     const double cte = anrm * std::ldexp(1.0, -53) * std::sqrt((double)n);   // A-1, A-2
     int code = 0;
     int t_fac = t_dem, t_ref = t_dem;
@@ -866,7 +982,9 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     bool used_inv = false;
 
     if (st0.flags & ST_OVERFLOW) code = -2;
-    if (!code) {
+    if (!code && stream_a) {
+        if (st0.flags & ST_ZERO_PIVOT) code = -3;                   // (step 1 already ran)
+    } else if (!code) {
         // ---- step 1: binary32 blocked GEPP
         run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant, (o.flags & 16) == 0);
         t_fac = tm.mark();

@@ -124,6 +124,10 @@ template <typename T>
 void launch_demote_rect(const double *A, int64_t lda, int64_t n, int64_t ncols, T *W, int64_t ldw,
                         double *partials, unsigned *counter, DevStatus *st, cudaStream_t s);
 
+// W[i][c] = S[perm[i]][c] (i < n, c < ncols; S row-major with ld lds; 16-byte aligned rows)
+void launch_gather_rows(const float *S, int64_t lds, int64_t ncols, const int32_t *perm, int64_t n, float *W,
+                        int64_t ldw, cudaStream_t s);
+
 // LU[i + j*n] = W[i*ldw + j]: packed factors back to the column-major ABI layout.
 template <typename T>
 void launch_transpose_out(const T *W, int64_t ldw, int64_t n, T *LU, cudaStream_t s);

@@ -211,6 +211,30 @@ void launch_permute_demote_rhs(const double *B, int64_t n, int64_t nrhs, const i
     ++g_launches;
 }
 
+// W[i][c0 + c] = S[perm[i]][c] for i < n, c < ncols (S row-major, lds): a demoted column block, received in
+// the original row order, brought to the current row order of the factorisation (streamed e2e path).
+__global__ void gather_rows_kernel(const float *__restrict__ S, int64_t lds, int64_t ncols, const int32_t *__restrict__ perm,
+                                   int64_t n, float *__restrict__ W, int64_t ldw)
+{
+    const int64_t q4 = ncols / 4;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const float4 *src = reinterpret_cast<const float4 *>(S + (int64_t)perm[i] * lds);
+        float4 *dst = reinterpret_cast<float4 *>(W + i * ldw);
+        for (int64_t c = threadIdx.x; c < q4; c += blockDim.x) dst[c] = src[c];
+    }
+}
+
+void launch_gather_rows(const float *S, int64_t lds, int64_t ncols, const int32_t *perm, int64_t n, float *W,
+                        int64_t ldw, cudaStream_t s)
+{
+    if (n <= 0 || ncols <= 0) return;
+    if ((ncols % 4) || (lds % 4) || (ldw % 4) || (reinterpret_cast<uintptr_t>(W) & 15) || (reinterpret_cast<uintptr_t>(S) & 15))
+        throw CudaError{cudaErrorInvalidValue, "gather_rows: 16-byte aligned rows required", __LINE__};
+    gather_rows_kernel<<<(unsigned)std::min<int64_t>(n, 8192), 256, 0, s>>>(S, lds, ncols, perm, n, W, ldw);
+    MP_LAUNCH_CHECK();
+    ++g_launches;
+}
+
 template void launch_demote_rect<float>(const double *, int64_t, int64_t, int64_t, float *, int64_t, double *,
                                         unsigned *, DevStatus *, cudaStream_t);
 template void launch_demote_rect<double>(const double *, int64_t, int64_t, int64_t, double *, int64_t, double *,

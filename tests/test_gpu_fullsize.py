@@ -266,3 +266,25 @@ def test_exact_lu_fp64_36864(mp):
     """The binary64 path (mp_dgetrf / mp_dgesv, the fallback) above 32768 rows, where its leaves are
     4 columns wide (512 x 8 rows per CTA, 16-CTA cluster): P, L, U and X bitwise."""
     _exact_case(mp, 36864, 256, 1, True, fp64=True)
+
+
+def test_streamed_host_path_exact_and_criterion(mp, orc):
+    """Host buffers (the end-to-end path) with n >= 4096: A crosses PCIe in column blocks while the
+    factorisation runs.  The exact-LU family stays bitwise (iters 0, X = x_true) and a
+    Gaussian system gives the device path's result bitwise (same operations, reordered only across
+    independent column blocks)."""
+    import torch
+    n = 4608
+    A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n)
+    Xh, it, info, rep = mp.mp_dsgesv_ex(A, B)
+    assert (it, info) == (0, 0) and np.array_equal(Xh, X)
+    A2, B2, _ = inputs.gaussian(n, nrhs=2, seed=77)
+    Xh2, ith, infoh, reph = mp.mp_dsgesv_ex(A2, B2)
+    Xd2, itd, infod, repd, _ = gpu_solve(mp, A2, B2)
+    ro = orc.dsgesv(A2, B2)
+    log({"cfg": "streamed-host", "n": n, "iters_host": ith, "iters_dev": itd, "iters_oracle": ro.iters,
+         "x_gap_host_dev": float(np.abs(Xh2 - Xd2).max() / np.abs(Xd2).max()),
+         "anrm_rel": abs(reph.anrm - ro.anrm) / ro.anrm})
+    assert infoh == infod == 0 and abs(ith - ro.iters) <= 1
+    assert certificate(A2, Xh2, B2) < 1.05
+    assert abs(reph.anrm - ro.anrm) <= 1e-12 * ro.anrm
