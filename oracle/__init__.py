@@ -21,7 +21,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
-_SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c"), os.path.join(_HERE, "oracle_dd.c")]
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c"), os.path.join(_HERE, "oracle_dd.c"),
+         os.path.join(_HERE, "oracle_gmres.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O3", "-march=x86-64-v2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
            "-fPIC", "-shared", "-std=c11"]
@@ -75,6 +76,10 @@ def _load():
             lib.oracle_dd_add.argtypes = [d, d, d, d, pd, pd]
             lib.oracle_dd_residual.argtypes = [i64, i64, p, i64, p, p, p, p, p]
             lib.oracle_qdgesv_ex.argtypes = [i64, i64, p, i64, p, p, p, pint, pint, ctypes.c_int, p, pint]
+            lib.oracle_gmres_sp_cycle.argtypes = [i64, p, i64, p, ctypes.c_int, p]
+            lib.oracle_gmres_sp_cycle.restype = ctypes.c_int
+            lib.oracle_fgmres_ex.argtypes = [i64, p, i64, p, p, ctypes.c_int, ctypes.c_int, pint, pint, ctypes.c_int,
+                                             p, pint]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -307,3 +312,28 @@ def qdgesv(A, B, itermax: int = ITERMAX) -> DDResult:
     _load().oracle_qdgesv_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(Xh), _ptr(Xl), ctypes.byref(iters),
                              ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh))
     return DDResult(Xh, Xl, iters.value, info.value, hist[: nh.value].copy())
+
+
+# ---------------------------------------------------------------------------- NEXT-3 (oracle_gmres.c)
+# Algorithm 2: FGMRES(m_out) in binary64 with one GMRES_SP(m_in) cycle (binary32) per step.
+def gmres_sp_cycle(A32, v, m_in: int):
+    """One GMRES_SP(m_in) cycle for A32 z = v from z = 0, binary32: returns (z, steps)."""
+    A32 = _fortran(A32, np.float32)
+    n = A32.shape[0]
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    z = np.zeros(n, dtype=np.float32)
+    steps = _load().oracle_gmres_sp_cycle(n, _ptr(A32), max(1, n), _ptr(v), int(m_in), _ptr(z))
+    return z, int(steps)
+
+
+def fgmres(A, b, m_out: int = 10, m_in: int = 20, itermax: int = ITERMAX) -> Result:
+    """Algorithm 2 from x0 = 0; Result.iters = outer cycles (-31: none converged in itermax)."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    bb = np.ascontiguousarray(np.asarray(b, dtype=np.float64).reshape(n))
+    x = np.zeros(n, dtype=np.float64)
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(itermax + 1)
+    _load().oracle_fgmres_ex(n, _ptr(A), max(1, n), _ptr(bb), _ptr(x), int(m_out), int(m_in), ctypes.byref(iters),
+                             ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh))
+    return Result(x.reshape(n, 1), iters.value, info.value, hist[: nh.value].copy(), fro_norm(A))

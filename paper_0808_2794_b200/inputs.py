@@ -180,3 +180,17 @@ def exact_chol(n: int, nrhs: int = 1, seed: int = BASE_SEED, density: float = 0.
     X = np.asfortranarray(r.integers(-4, 5, size=(n, nrhs)).astype(np.float64) / 4.0)
     B = np.asfortranarray(A @ X)
     return A, B, X, L
+
+
+# --------------------------------------------------------------------------- NEXT-3 (Alg. 2) operators
+def shifted_gaussian(n: int, shift: float = 2.5, nrhs: int = 1, seed: int = BASE_SEED):
+    """Stand-in for the paper's sparse application matrices (T2, not in the container):
+    A = shift I + G / sqrt(n), G i.i.d. N(0,1) — by the circular law its spectrum fills the disk of radius 1
+    around `shift`, so restarted GMRES converges geometrically (~1/shift per step) on a dense nonsymmetric
+    operator.  x_true U[-1,1], b = A x_true."""
+    G = _rng(seed).standard_normal(size=(n, n))
+    A = np.asfortranarray(G.T / np.sqrt(n))
+    A[np.diag_indices(n)] += shift
+    X = _xtrue(n, nrhs, seed)
+    B = np.asfortranarray(A @ X)
+    return A, B, X
