@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -490,6 +491,35 @@ def other_configs(mp, args, dev):
                      "symv_residual_gbs": round(rr["work"] / rr["ms"] / 1e6, 1) if rr["ms"] else None,
                      "kernels_ms": {k: [round(v["ms"], 3), v["launches"]] for k, v in kk.items()}}
     del As, Ac, Lc, Bs, Asc
+    torch.cuda.empty_cache()
+    # Algorithm 2 (NEXT-3): FGMRES(10)-GMRES_SP(20) at C3's size on A = 2.5 I + G / sqrt(n)
+    # (the stand-in for the paper's application matrices, inputs.shifted_gaussian), generated on the GPU
+    log("FGMRES")
+    g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED + 11)
+    Ag = (torch.randn((ns, ns), dtype=torch.float64, device=dev, generator=g) / math.sqrt(ns)).t()
+    Ag.diagonal().add_(2.5)
+    xg = (torch.rand((1, ns), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+    bg = (Ag @ xg).t().contiguous().t()
+    mp.mp_fgmres_ex(Ag, bg, m_out=10, m_in=20, report=False)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _, itg, infog, _ = mp.mp_fgmres_ex(Ag, bg, m_out=10, m_in=20, report=False)
+    e1.record()
+    torch.cuda.synchronize()
+    _, _, _, repg = mp.mp_fgmres_ex(Ag, bg, m_out=10, m_in=20, opts=mp.make_opts(flags=2))
+    torch.cuda.synchronize()
+    kg = repg.kernels()
+    sg, rg = kg.get("solve", {"ms": 0, "work": 0}), kg.get("residual", {"ms": 0, "work": 0})
+    ms_d, _ = time_solves(mp, Ag, bg, mp.make_opts(), 1)
+    res["FGMRES_C3"] = {"n": ns, "m_out": 10, "m_in": 20, "matrix": "2.5 I + G/sqrt(n), G N(0,1)",
+                        "ms": round(e0.elapsed_time(e1), 3), "outer_cycles": itg, "info": infog,
+                        "launches": repg.kernel_launches,
+                        "inner_cycle_gbs": round(sg["work"] / sg["ms"] / 1e6, 1) if sg["ms"] else None,
+                        "outer_products_gbs": round(rg["work"] / rg["ms"] / 1e6, 1) if rg["ms"] else None,
+                        "dsgesv_same_matrix_ms": round(ms_d, 3),
+                        "kernels_ms": {k: [round(v["ms"], 3), v["launches"]] for k, v in kg.items()}}
+    del Ag, bg, xg
     torch.cuda.empty_cache()
     # C4: n = 49152, nrhs = 16 (A = 19.3 GB fp64), device-generated with a seeded torch generator
     if not args.no_c4:

@@ -220,6 +220,26 @@ int mp_qdgesv(int64_t n, int64_t nrhs, const double *A, int64_t lda, const doubl
 int mp_qdgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const double *B,
                  double *Xhi, double *Xlo, int *iters, int *info, const mp_opts *opts, mp_report *rep);
 
+/* ---------------------------------------------------------------- NEXT-3: Algorithm 2
+ * Mixed precision inner-outer FGMRES(m_out)-GMRES_SP(m_in) (Algorithm 2,
+ * P:240-279).  Outer: flexible GMRES in binary64 with the caller's A (products r = A z_k, modified
+ * Gram-Schmidt, Givens least squares, x += Z y); preconditioner: one cycle of GMRES_SP(m_in) in
+ * binary32 with fl32(A), started from z = 0.  x0 = 0.  One right-hand side.
+ * Readings (G-1..G-6): the stop test is B:5's ||b - A x||_2 < ||x||_2 ||A||_F 2^-53 sqrt(n)
+ * (or r == 0), checked at the top of every outer cycle (G-1); at most opts.itermax (default 30)
+ * outer cycles, then *iters = -31 and x is the last iterate (G-2, no fallback); an exact breakdown
+ * ends the basis (G-4); the binary32 Arnoldi orthogonalises by classical Gram-Schmidt applied twice
+ * (G-6; the oracle follows the printed MGS).
+ * A: n x n binary64, column-major, lda >= max(1, n); b: n; x: n output.  Device or host pointers (host
+ * buffers are staged).  1 <= m_out, m_in <= 31.
+ * *info: 0; -1 n < 0; -2 A NULL or NaN/Inf; -3 lda; -4 b NULL or NaN/Inf; -5 x NULL; -6 m_out / m_in.
+ * *iters: outer cycles applied before convergence (>= 0); -31 no convergence.
+ * Workspace: 4 n^2 + O(n (m_out + m_in)) bytes (the binary32 copy of A dominates). */
+int mp_fgmres(int64_t n, const double *A, int64_t lda, const double *b, double *x, int m_out, int m_in,
+              int *iters, int *info);
+int mp_fgmres_ex(int64_t n, const double *A, int64_t lda, const double *b, double *x, int m_out, int m_in,
+                 int *iters, int *info, const mp_opts *opts, mp_report *rep);
+
 /* Resolve the per-launch events recorded by calls made with opts.flags = 2|4 since the
  * last collection: fills rep->k_ms / k_work / k_launches (summed over those calls, all
  * other fields untouched) and clears the records.  Synchronises the device. */

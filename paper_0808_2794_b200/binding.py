@@ -74,6 +74,9 @@ lib.mp_spotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_dpotrf.argtypes = [_i64, _p, _i64, _p, _pi, ctypes.POINTER(Opts)]
 lib.mp_qdgesv.argtypes = [_i64, _i64, _p, _i64, _p, _p, _p, _pi, _pi]
 lib.mp_qdgesv_ex.argtypes = [_i64, _i64, _p, _i64, _p, _p, _p, _pi, _pi, ctypes.POINTER(Opts), ctypes.POINTER(Report)]
+lib.mp_fgmres.argtypes = [_i64, _p, _i64, _p, _p, ctypes.c_int, ctypes.c_int, _pi, _pi]
+lib.mp_fgmres_ex.argtypes = [_i64, _p, _i64, _p, _p, ctypes.c_int, ctypes.c_int, _pi, _pi, ctypes.POINTER(Opts),
+                             ctypes.POINTER(Report)]
 lib.mp_kernel_schur_update.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_kernel_schur_update_f64.argtypes = [_p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, ctypes.c_int]
 lib.mp_set_stream.argtypes = [_p]
@@ -95,7 +98,7 @@ lib.mp_dgesv_1dbc.argtypes = [_p, _i64, _i64, _i64, _p, _i64, _p, _p, _pi]
 EXPORTED = ("mp_default_opts", "mp_dsgesv", "mp_dsgesv_ex", "mp_dgesv", "mp_dgesv_ex", "mp_sgetrf",
             "mp_dgetrf", "mp_set_stream", "mp_last_error", "mp_version", "mp_kernel_schur_update",
             "mp_kernel_schur_update_f64", "mp_dsposv", "mp_dsposv_ex", "mp_dposv", "mp_dposv_ex", "mp_spotrf",
-            "mp_dpotrf", "mp_qdgesv", "mp_qdgesv_ex",
+            "mp_dpotrf", "mp_qdgesv", "mp_qdgesv_ex", "mp_fgmres", "mp_fgmres_ex",
             "mp_profile_collect", "mp_exec_info", "mp_get_unique_id", "mp_comm_init", "mp_comm_init_loopback",
             "mp_comm_destroy", "mp_1dbc_local_cols", "mp_dsgesv_1dbc", "mp_dsgesv_1dbc_ex", "mp_dgesv_1dbc")
 
@@ -279,6 +282,25 @@ def mp_qdgesv_ex(A, B, Xhi=None, Xlo=None, opts: Opts | None = None, report: boo
                             ctypes.byref(opts) if opts is not None else None,
                             ctypes.byref(rep) if rep is not None else None))
     return Xhi, Xlo, it.value, info.value, rep
+
+
+def mp_fgmres_ex(A, b, x=None, m_out: int = 10, m_in: int = 20, opts: Opts | None = None, report: bool = True):
+    """Algorithm 2, FGMRES(m_out)-GMRES_SP(m_in) (include/mp_solve.h): returns (x, iters, info, Report|None)."""
+    n = A.shape[0]
+    if _nrhs(b, n) != 1:
+        raise ValueError("mp_fgmres: one right-hand side")
+    if x is None:
+        x = _alloc_like_X(b, n, 1)
+    pa, lda = _ptr_ld(A, "A", True)
+    pb, _ = _ptr_ld(b, "b", False, n)
+    px, _ = _ptr_ld(x, "x", False, n)
+    lib.mp_set_stream(_stream_of(A, b, x))
+    it, info = ctypes.c_int(0), ctypes.c_int(0)
+    rep = Report() if report else None
+    _check(lib.mp_fgmres_ex(n, pa, lda, pb, px, int(m_out), int(m_in), ctypes.byref(it), ctypes.byref(info),
+                            ctypes.byref(opts) if opts is not None else None,
+                            ctypes.byref(rep) if rep is not None else None))
+    return x, it.value, info.value, rep
 
 
 def _potrf(fn, dtype, A, opts):

@@ -1553,6 +1553,162 @@ int qdgesv_impl(const Args &a, double *Xlo, int *iters, int *info, const mp_opts
     return MP_OK;
 }
 
+// ------------------------------------------------------------------ NEXT-3: Algorithm 2 (FGMRES-GMRES_SP)
+// PAPER.md P:240-279.  Outer FGMRES(m_out) in binary64 with the caller's A (its products through the
+// residual kernel K8, modified Gram-Schmidt as printed), one GMRES_SP(m_in) cycle per outer step in
+// binary32 with the row-major binary32 copy W (products: gemv_rows_f32; Arnoldi by classical
+// Gram-Schmidt applied twice, reading G-6), Givens least squares on the device, B:5's test at the top of
+// every outer cycle (G-1), at most itermax cycles (G-2).  x0 = 0.  One right-hand side.
+int fgmres_impl(int64_t n, const double *A, int64_t lda, const double *b, double *x, int m_out, int m_in, int *iters,
+                int *info, const mp_opts *opts, mp_report *rep)
+{
+    *info = 0; *iters = 0;
+    if (rep) std::memset(rep, 0, sizeof(*rep));
+    if (n < 0) return *info = -1, MP_OK;
+    if (n > 0 && !A) return *info = -2, MP_OK;
+    if (lda < std::max<int64_t>(1, n)) return *info = -3, MP_OK;
+    if (n > 0 && !b) return *info = -4, MP_OK;
+    if (n > 0 && !x) return *info = -5, MP_OK;
+    if (m_out < 1 || m_in < 1 || m_out > 31 || m_in > 31) return *info = -6, MP_OK;
+    if (n == 0) return MP_OK;
+    mp_opts o;
+    mp_default_opts(&o);
+    if (opts) o = *opts;
+    const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
+    cudaStream_t s = g_stream;
+    g_launches = 0;
+    g_prof.reset((o.flags & 2) != 0, (o.flags & 4) != 0);
+    g_prof.mask = ~0u;
+    Timer tm(s);
+    const int t0 = tm.mark();
+    Pool pool(s);
+    Args a{n, 1, lda, A, b, x};
+    Views v = stage_in(a, pool, s, true);
+    StatusIO sio(pool, s);
+    const int sms = num_sms();
+    const int64_t ldw = round_up(n, 64);
+    float *W = pool.get<float>((size_t)n * ldw);
+    double *dpart = pool.get<double>((size_t)sms * 8);
+    unsigned *dcnt = pool.get<unsigned>(1);
+    MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
+    int32_t *ident = pool.get<int32_t>(n);
+    float *ychk = pool.get<float>(n);
+    launch_demote_transpose<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);      // binary32 copy + ||A||_F
+    launch_init_perm(ident, n, s);
+    launch_permute_demote_rhs<float>(v.B, n, 1, ident, ychk, sio.d, s);
+    const DevStatus st0 = sio.read();
+    if (st0.flags & ST_A_NONFINITE) { *info = -2; if (rep) rep->info = -2; return MP_OK; }
+    if (st0.flags & ST_B_NONFINITE) { *info = -4; if (rep) rep->info = -4; return MP_OK; }
+    const double anrm = std::sqrt(st0.anrm2);
+    const double cte = anrm * std::ldexp(1.0, -53) * std::sqrt((double)n);
+    // binary64 outer workspace
+    const int64_t ldv = round_up(n, 32);                     // 16-byte aligned columns for the vector kernels
+    double *V = pool.get<double>((size_t)ldv * (m_out + 1)), *Z = pool.get<double>((size_t)ldv * m_out);
+    double *r = pool.get<double>(n), *ax = pool.get<double>(n);
+    double *R = pool.get<double>((size_t)(m_out + 1) * m_out), *cs = pool.get<double>(32), *sn = pool.get<double>(32);
+    double *g = pool.get<double>(33), *y = pool.get<double>(32), *hcol = pool.get<double>(32), *hn = pool.get<double>(32);
+    double *sc = pool.get<double>(8), *ones = pool.get<double>(32), *pd = pool.get<double>(gmres_partial_elems(n));
+    // binary32 inner workspace
+    float *Vs = pool.get<float>((size_t)ldv * (m_in + 1)), *vs = pool.get<float>(n), *zs = pool.get<float>(n);
+    float *Rs = pool.get<float>((size_t)(m_in + 1) * m_in), *css = pool.get<float>(32), *sns = pool.get<float>(32);
+    float *gs = pool.get<float>(33), *ys = pool.get<float>(32), *hs = pool.get<float>(32), *hs2 = pool.get<float>(32);
+    float *hns = pool.get<float>(32), *scs = pool.get<float>(8), *oness = pool.get<float>(32);
+    float *ps = pool.get<float>(gmres_partial_elems(n));
+    ResidualScratch rs;
+    rs.partial = pool.get<double>(residual_partial_elems(n, 1, sms));
+    rs.blocksums = nullptr;
+    rs.counter = nullptr;
+    {
+        std::vector<double> h1(32, 1.0);
+        std::vector<float> h1s(32, 1.0f);
+        MP_CUDA(cudaMemcpyAsync(ones, h1.data(), 32 * sizeof(double), cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemcpyAsync(oness, h1s.data(), 32 * sizeof(float), cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaMemsetAsync(v.X, 0, (size_t)n * sizeof(double), s));                        // x0 = 0
+        MP_CUDA(cudaStreamSynchronize(s));                                                    // h1 / h1s lifetime
+    }
+    int nhist = 0;
+    double hist[MP_HIST_MAX] = {0};
+    *iters = -31;
+    const int t_setup = tm.mark();
+    for (int it = 0; it <= itermax; ++it) {
+        // ---- r = b - A x_i (eps_d), beta = ||r||, ||x||; the check
+        prof_begin(KC_RESIDUAL, s);
+        launch_residual_products(v.A, v.lda, n, n, 1, v.X, n, ax, rs, sms, s);
+        MP_CUDA(cudaMemcpyAsync(r, v.B, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        launch_combine<double>(r, ax, n, 1, ones, 1.0, -1.0, n, s);
+        prof_end(KC_RESIDUAL, 8.0 * n * n, s);
+        launch_multidot<double>(r, n, 1, r, n, pd, sc + 0, false, s);
+        launch_multidot<double>(v.X, n, 1, v.X, n, pd, sc + 1, false, s);
+        double hsc[2];
+        MP_CUDA(cudaMemcpyAsync(hsc, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        const double beta = std::sqrt(hsc[0]), xn = std::sqrt(hsc[1]);
+        if (!std::isfinite(beta) || !std::isfinite(xn)) break;
+        hist[nhist++] = beta == 0.0 ? 0.0 : beta / (xn * cte);
+        if (beta < xn * cte || beta == 0.0) { *iters = it; break; }                          // G-1
+        if (it == itermax) break;
+        // ---- one FGMRES(m_out) cycle
+        launch_cycle_start<double>(sc + 0, g, m_out, sc + 2, s);                            // g = beta e_1
+        for (int k = 0; k < m_out; ++k) {
+            double *vk = V + (size_t)k * ldv, *zk = Z + (size_t)k * ldv;
+            // v_k = r / h_{k,k-1} (eps_d), and its binary32 demotion for the inner solver
+            launch_scale_copy<double, float>(r, k == 0 ? sc + 2 : hn + (k - 1), true, vk, vs, n, s);
+            // ---- one GMRES_SP(m_in) cycle: A z = v_k, z = 0 initially (eps_s)
+            prof_begin(KC_SOLVE, s);
+            launch_multidot<float>(vs, n, 1, vs, n, ps, scs + 0, false, s);
+            launch_cycle_start<float>(scs + 0, gs, m_in, scs + 1, s);
+            launch_scale_copy<float, float>(vs, scs + 1, true, Vs, nullptr, n, s);
+            for (int j = 0; j < m_in; ++j) {
+                float *wj = Vs + (size_t)(j + 1) * ldv;
+                launch_gemv_rows_f32(W, ldw, n, Vs + (size_t)j * ldv, wj, s);
+                launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs, false, s);              // CGS, pass 1
+                launch_combine<float>(wj, Vs, ldv, j + 1, hs, 1.f, -1.f, n, s);
+                launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs2, false, s);             // pass 2 (G-6)
+                launch_combine<float>(wj, Vs, ldv, j + 1, hs2, 1.f, -1.f, n, s);
+                launch_combine<float>(hs, hs2, 32, 1, oness, 1.f, 1.f, j + 1, s);          // h += pass-2 h
+                launch_multidot<float>(wj, n, 1, wj, n, ps, scs + 2, false, s);
+                launch_givens_step<float>(hs, scs + 2, j, m_in, Rs, css, sns, gs, hns + j, s);
+                launch_scale_copy<float, float>(wj, hns + j, true, wj, nullptr, n, s);
+            }
+            launch_backsolve<float>(Rs, m_in, m_in, gs, ys, hns, s);
+            launch_combine<float>(zs, Vs, ldv, m_in, ys, 0.f, 1.f, n, s);                     // z = V y
+            prof_end(KC_SOLVE, 4.0 * n * n * m_in, s);
+            launch_convert_f32_f64(zs, zk, n, s);
+            // ---- r = A z_k (eps_d); modified Gram-Schmidt against v_1..v_k (eps_d); h_{k+1,k}
+            prof_begin(KC_RESIDUAL, s);
+            launch_residual_products(v.A, v.lda, n, n, 1, zk, n, r, rs, sms, s);
+            prof_end(KC_RESIDUAL, 8.0 * n * n, s);
+            for (int j = 0; j <= k; ++j) {
+                launch_multidot<double>(V + (size_t)j * ldv, ldv, 1, r, n, pd, hcol + j, false, s);
+                launch_combine<double>(r, V + (size_t)j * ldv, ldv, 1, hcol + j, 1.0, -1.0, n, s);
+            }
+            launch_multidot<double>(r, n, 1, r, n, pd, sc + 3, false, s);
+            launch_givens_step<double>(hcol, sc + 3, k, m_out, R, cs, sn, g, hn + k, s);
+        }
+        // ---- y = argmin ||beta e_1 - H y||, x += Z y (eps_d)
+        launch_backsolve<double>(R, m_out, m_out, g, y, hn, s);
+        launch_combine<double>(v.X, Z, ldv, m_out, y, 1.0, 1.0, n, s);
+    }
+    const int t_ref = tm.mark();
+    finish_copy_out(a, v, s);
+    const int t_end = tm.mark();
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+        rep->iters = *iters; rep->info = *info; rep->nhist = nhist; rep->variant = -2;
+        rep->anrm = anrm;
+        for (int i = 0; i < nhist; ++i) rep->hist[i] = hist[i];
+        rep->t_total_ms = tm.ms(t0, t_end);
+        rep->t_demote_ms = tm.ms(t0, t_setup);
+        rep->t_refine_ms = tm.ms(t_setup, t_ref);
+        rep->workspace_bytes = pool.bytes;
+        rep->kernel_launches = g_launches;
+        if (!g_prof.deferred) prof_collect(rep);
+    }
+    if (!g_prof.deferred) g_prof.reset(false, false);
+    else g_prof.on = false;
+    return MP_OK;
+}
+
 // ------------------------------------------------------------------ 1D block-cyclic multi-GPU path
 // SURVEY 8(e) / B:5: global column block j (nb columns) lives on rank j mod P at local slot
 // j / P; A (binary64, caller's) and the working copy use the same distribution; B, X, r, z,
@@ -2169,6 +2325,20 @@ int mp_qdgesv_ex(int64_t n, int64_t nrhs, const double *A, int64_t lda, const do
 {
     if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
     return guarded([&] { return qdgesv_impl(Args{n, nrhs, lda, A, B, Xhi}, Xlo, iters, info, opts, rep); });
+}
+
+int mp_fgmres(int64_t n, const double *A, int64_t lda, const double *b, double *x, int m_out, int m_in, int *iters,
+              int *info)
+{
+    if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return fgmres_impl(n, A, lda, b, x, m_out, m_in, iters, info, nullptr, nullptr); });
+}
+
+int mp_fgmres_ex(int64_t n, const double *A, int64_t lda, const double *b, double *x, int m_out, int m_in,
+                 int *iters, int *info, const mp_opts *opts, mp_report *rep)
+{
+    if (!iters || !info) { g_err = "iters/info must not be NULL"; return MP_ERR_INTERNAL; }
+    return guarded([&] { return fgmres_impl(n, A, lda, b, x, m_out, m_in, iters, info, opts, rep); });
 }
 
 int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,

@@ -333,3 +333,24 @@ void launch_dd_residual(const double *A, int64_t lda, int64_t n, int64_t nrhs, c
                         double *scratch, unsigned *counter, DevStatus *st, int num_sms, cudaStream_t s);
 void launch_dd_update(double *Xh, double *Xl, const double *Z, int64_t count, cudaStream_t s);
 }  // namespace mp
+
+namespace mp {
+// ---------------------------------------------------------------- NEXT-3 Algorithm 2 (k_gmres.cu)
+void launch_gemv_rows_f32(const float *W, int64_t ldw, int64_t n, const float *x, float *y, cudaStream_t s);
+size_t gmres_partial_elems(int64_t n);
+void launch_convert_f32_f64(const float *a, double *b, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_multidot(const T *V, int64_t ldv, int k, const T *w, int64_t n, T *partial, T *out, bool accumulate,
+                     cudaStream_t s);
+template <typename T>
+void launch_combine(T *w, const T *V, int64_t ldv, int k, const T *coef, T alpha, T beta, int64_t n, cudaStream_t s);
+template <typename T, typename TS>
+void launch_scale_copy(const T *w, const T *scale, bool invert, T *out, TS *outs, int64_t n, cudaStream_t s);
+template <typename T>
+void launch_givens_step(const T *hcol, const T *hnorm2, int j, int m, T *R, T *cs, T *sn, T *g, T *hout,
+                        cudaStream_t s);
+template <typename T>
+void launch_backsolve(const T *R, int m, int steps, const T *g, T *y, const T *hn, cudaStream_t s);
+template <typename T>
+void launch_cycle_start(const T *norm2, T *g, int m, T *beta, cudaStream_t s);
+}  // namespace mp
