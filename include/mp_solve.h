@@ -88,7 +88,11 @@ typedef struct mp_opts {
                                  while the trailing update of step k runs on the other SMs);
                           bit 5: binary32 triangular solves by plain substitution inside the 64-row
                                  diagonal blocks instead of the default inverted diagonal blocks
-                                 (reading A-19); exact inputs then stay exact (pin P2) */
+                                 (reading A-19); exact inputs then stay exact (pin P2);
+                          bit 6: host A: one copy before the factorisation instead of streaming it in
+                                 by column blocks under the factorisation (mp_dsgesv, n >= 4096);
+                          bit 7: mp_fgmres: run each binary32 GMRES_SP cycle as a sequence of small
+                                 kernels instead of the one cooperative launch (testing) */
 } mp_opts;
 
 #define MP_HIST_MAX 64

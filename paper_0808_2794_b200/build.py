@@ -27,6 +27,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                 "-I" + INCLUDE, "-I" + CSRC]
+FLAGS += os.environ.get("MP_EXTRA_NVCC_FLAGS", "").split()     # experiments only (e.g. -DMP_G7_GU=4)
 
 
 def sources():

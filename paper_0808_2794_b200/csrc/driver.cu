@@ -1614,6 +1614,10 @@ int fgmres_impl(int64_t n, const double *A, int64_t lda, const double *b, double
     float *gs = pool.get<float>(33), *ys = pool.get<float>(32), *hs = pool.get<float>(32), *hs2 = pool.get<float>(32);
     float *hns = pool.get<float>(32), *scs = pool.get<float>(8), *oness = pool.get<float>(32);
     float *ps = pool.get<float>(gmres_partial_elems(n));
+    const bool coop = !(o.flags & 128) && sp_cycle_supported(n, sms);   // G7: one launch per inner cycle
+    float *cpart = coop ? pool.get<float>(sp_cycle_part_elems(sms)) : nullptr;
+    float *craw = coop ? pool.get<float>((size_t)2 * ldv) : nullptr;
+    unsigned *cbar = coop ? pool.get<unsigned>(1) : nullptr;
     ResidualScratch rs;
     rs.partial = pool.get<double>(residual_partial_elems(n, 1, sms));
     rs.blocksums = nullptr;
@@ -1655,25 +1659,30 @@ int fgmres_impl(int64_t n, const double *A, int64_t lda, const double *b, double
             launch_scale_copy<double, float>(r, k == 0 ? sc + 2 : hn + (k - 1), true, vk, vs, n, s);
             // ---- one GMRES_SP(m_in) cycle: A z = v_k, z = 0 initially (eps_s)
             prof_begin(KC_SOLVE, s);
-            launch_multidot<float>(vs, n, 1, vs, n, ps, scs + 0, false, s);
-            launch_cycle_start<float>(scs + 0, gs, m_in, scs + 1, s);
-            launch_scale_copy<float, float>(vs, scs + 1, true, Vs, nullptr, n, s);
-            for (int j = 0; j < m_in; ++j) {
-                float *wj = Vs + (size_t)(j + 1) * ldv;
-                launch_gemv_rows_f32(W, ldw, n, Vs + (size_t)j * ldv, wj, s);
-                launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs, false, s);              // CGS, pass 1
-                launch_combine<float>(wj, Vs, ldv, j + 1, hs, 1.f, -1.f, n, s);
-                launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs2, false, s);             // pass 2 (G-6)
-                launch_combine<float>(wj, Vs, ldv, j + 1, hs2, 1.f, -1.f, n, s);
-                launch_combine<float>(hs, hs2, 32, 1, oness, 1.f, 1.f, j + 1, s);          // h += pass-2 h
-                launch_multidot<float>(wj, n, 1, wj, n, ps, scs + 2, false, s);
-                launch_givens_step<float>(hs, scs + 2, j, m_in, Rs, css, sns, gs, hns + j, s);
-                launch_scale_copy<float, float>(wj, hns + j, true, wj, nullptr, n, s);
+            if (coop) {
+                launch_gmres_sp_cycle(W, ldw, n, vs, Vs, ldv, craw, zk, m_in, cpart, cbar, sms, s);
+                prof_end(KC_SOLVE, 4.0 * n * n * m_in, s);
+            } else {
+                launch_multidot<float>(vs, n, 1, vs, n, ps, scs + 0, false, s);
+                launch_cycle_start<float>(scs + 0, gs, m_in, scs + 1, s);
+                launch_scale_copy<float, float>(vs, scs + 1, true, Vs, nullptr, n, s);
+                for (int j = 0; j < m_in; ++j) {
+                    float *wj = Vs + (size_t)(j + 1) * ldv;
+                    launch_gemv_rows_f32(W, ldw, n, Vs + (size_t)j * ldv, wj, s);
+                    launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs, false, s);              // CGS, pass 1
+                    launch_combine<float>(wj, Vs, ldv, j + 1, hs, 1.f, -1.f, n, s);
+                    launch_multidot<float>(Vs, ldv, j + 1, wj, n, ps, hs2, false, s);             // pass 2 (G-6)
+                    launch_combine<float>(wj, Vs, ldv, j + 1, hs2, 1.f, -1.f, n, s);
+                    launch_combine<float>(hs, hs2, 32, 1, oness, 1.f, 1.f, j + 1, s);          // h += pass-2 h
+                    launch_multidot<float>(wj, n, 1, wj, n, ps, scs + 2, false, s);
+                    launch_givens_step<float>(hs, scs + 2, j, m_in, Rs, css, sns, gs, hns + j, s);
+                    launch_scale_copy<float, float>(wj, hns + j, true, wj, nullptr, n, s);
+                }
+                launch_backsolve<float>(Rs, m_in, m_in, gs, ys, hns, s);
+                launch_combine<float>(zs, Vs, ldv, m_in, ys, 0.f, 1.f, n, s);                     // z = V y
+                prof_end(KC_SOLVE, 4.0 * n * n * m_in, s);
+                launch_convert_f32_f64(zs, zk, n, s);
             }
-            launch_backsolve<float>(Rs, m_in, m_in, gs, ys, hns, s);
-            launch_combine<float>(zs, Vs, ldv, m_in, ys, 0.f, 1.f, n, s);                     // z = V y
-            prof_end(KC_SOLVE, 4.0 * n * n * m_in, s);
-            launch_convert_f32_f64(zs, zk, n, s);
             // ---- r = A z_k (eps_d); modified Gram-Schmidt against v_1..v_k (eps_d); h_{k+1,k}
             prof_begin(KC_RESIDUAL, s);
             launch_residual_products(v.A, v.lda, n, n, 1, zk, n, r, rs, sms, s);

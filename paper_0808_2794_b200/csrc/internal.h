@@ -338,6 +338,12 @@ namespace mp {
 // ---------------------------------------------------------------- NEXT-3 Algorithm 2 (k_gmres.cu)
 void launch_gemv_rows_f32(const float *W, int64_t ldw, int64_t n, const float *x, float *y, cudaStream_t s);
 size_t gmres_partial_elems(int64_t n);
+// G7: one whole binary32 GMRES_SP(m) cycle (z = 0 start, right-hand side v) as one cooperative launch of
+// `sms` CTAs; z written in binary64.  V: ldv x m, raw: 2 x ldv, part: sp_cycle_part_elems(sms), bar: 1.
+bool sp_cycle_supported(int64_t n, int sms);
+size_t sp_cycle_part_elems(int sms);
+void launch_gmres_sp_cycle(const float *W, int64_t ldw, int64_t n, const float *v, float *V, int64_t ldv, float *raw,
+                           double *z, int m, float *part, unsigned *bar, int sms, cudaStream_t s);
 void launch_convert_f32_f64(const float *a, double *b, int64_t n, cudaStream_t s);
 template <typename T>
 void launch_multidot(const T *V, int64_t ldv, int k, const T *w, int64_t n, T *partial, T *out, bool accumulate,

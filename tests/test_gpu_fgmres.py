@@ -85,6 +85,18 @@ def test_fgmres_parity(mp, orc, n, m_out, m_in, shift, seed):
     assert np.abs(x - ref).max() <= 64 * n * kappa * EPS64 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n,m_out,m_in,seed", [(1000, 10, 20, 11), (333, 5, 31, 12)])
+def test_fgmres_multikernel_inner_cycle(mp, orc, n, m_out, m_in, seed):
+    """opts.flags bit 7: the inner cycle as separate small kernels (G1-G6) instead of the cooperative G7;
+    the same algorithm, different reduction trees: both meet the criterion, cycle counts within 1."""
+    A, B, _ = inputs.shifted_gaussian(n, seed=seed)
+    ro = orc.fgmres(A, B, m_out=m_out, m_in=m_in)
+    x1, it1, info1, _ = gpu_fgmres(mp, A, B, m_out, m_in)
+    x2, it2, info2, _ = gpu_fgmres(mp, A, B, m_out, m_in, flags=128)
+    assert info1 == info2 == 0 and abs(it1 - it2) <= 1 and abs(it2 - ro.iters) <= 1
+    assert certificate(A, x1, B) < 1.05 and certificate(A, x2, B) < 1.05
+
+
 def test_fgmres_host_buffers_match_device(mp):
     A, B, _ = inputs.shifted_gaussian(900, seed=7)
     xd, itd, infod, _ = gpu_fgmres(mp, A, B, 10, 20)
