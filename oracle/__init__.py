@@ -22,7 +22,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _SRCS = [_SRC, os.path.join(_HERE, "oracle_chol.c"), os.path.join(_HERE, "oracle_dd.c"),
-         os.path.join(_HERE, "oracle_gmres.c")]
+         os.path.join(_HERE, "oracle_gmres.c"), os.path.join(_HERE, "oracle_lp.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _CFLAGS = ["-O3", "-march=x86-64-v2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
            "-fPIC", "-shared", "-std=c11"]
@@ -80,6 +80,14 @@ def _load():
             lib.oracle_gmres_sp_cycle.restype = ctypes.c_int
             lib.oracle_fgmres_ex.argtypes = [i64, p, i64, p, p, ctypes.c_int, ctypes.c_int, pint, pint, ctypes.c_int,
                                              p, pint]
+            lib.oracle_rna_tf32.argtypes = [ctypes.c_float]
+            lib.oracle_rna_tf32.restype = ctypes.c_float
+            lib.oracle_rna_tf32_array.argtypes = [i64, p, p]
+            lib.oracle_sgetrf_tf32.argtypes = [i64, p, i64, i64, p]
+            lib.oracle_sgetrf_tf32.restype = ctypes.c_int
+            lib.oracle_dsgesv_tf32_ex.argtypes = [i64, i64, p, i64, p, p, i64, pint, pint, ctypes.c_int, p, pint]
+            lib.oracle_gmres_ir_ex.argtypes = [i64, i64, p, i64, p, p, ctypes.c_int, i64, ctypes.c_int, ctypes.c_int,
+                                               pint, pint, p, pint]
             lib.oracle_num_threads.restype = ctypes.c_int
             lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
             _lib = lib
@@ -337,3 +345,50 @@ def fgmres(A, b, m_out: int = 10, m_in: int = 20, itermax: int = ITERMAX) -> Res
     _load().oracle_fgmres_ex(n, _ptr(A), max(1, n), _ptr(bb), _ptr(x), int(m_out), int(m_in), ctypes.byref(iters),
                              ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh))
     return Result(x.reshape(n, 1), iters.value, info.value, hist[: nh.value].copy(), fro_norm(A))
+
+
+# ---------------------------------------------------------------------------- NEXT-2 (oracle_lp.c)
+# The lower-precision (TF32) factorisation and its refinement: readings T-1..T-4 in oracle_lp.c.
+def rna_tf32(x):
+    """Round binary32 values to TF32 (nearest, ties away from zero), elementwise."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    out = np.empty_like(a)
+    _load().oracle_rna_tf32_array(a.size, _ptr(a), _ptr(out))
+    return out
+
+
+def sgetrf_tf32(A, nb: int):
+    """T-1: blocked GEPP (panel nb) of fl32(A) with TF32 trailing updates: (LU packed, ipiv 0-based, info)."""
+    LU = _fortran(A, np.float32).copy(order="F")
+    n = LU.shape[0]
+    ipiv = np.zeros(n, dtype=np.int32)
+    info = _load().oracle_sgetrf_tf32(n, _ptr(LU), max(1, n), int(nb), _ptr(ipiv))
+    return LU, ipiv, int(info)
+
+
+def dsgesv_tf32(A, B, nb: int, itermax: int = ITERMAX) -> Result:
+    """T-2: Algorithm 1 with the T-1 factors."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F").copy(order="F")
+    X = np.zeros_like(Bm, order="F")
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(itermax + 1)
+    _load().oracle_dsgesv_tf32_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), int(nb), ctypes.byref(iters),
+                                  ctypes.byref(info), int(itermax), _ptr(hist), ctypes.byref(nh))
+    return Result(X, iters.value, info.value, hist[: nh.value].copy(), fro_norm(A))
+
+
+def gmres_ir(A, B, nb: int = 0, m: int = 20, itermax: int = ITERMAX, tf32: bool = True) -> Result:
+    """T-3/T-4: binary32 LU (TF32 updates with panel nb when tf32, else sgetf2), x0, GMRES-IR(m) per column.
+    Result.iters = LU applications (max over columns) or -31 / -3 (X then from the binary64 solver)."""
+    A = _fortran(A, np.float64)
+    n = A.shape[0]
+    Bm = _fortran(B, np.float64).reshape(n, -1, order="F").copy(order="F")
+    X = np.zeros_like(Bm, order="F")
+    iters, info, nh = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    hist = np.zeros(64)
+    _load().oracle_gmres_ir_ex(n, Bm.shape[1], _ptr(A), max(1, n), _ptr(Bm), _ptr(X), 1 if tf32 else 0, int(nb),
+                               int(m), int(itermax), ctypes.byref(iters), ctypes.byref(info), _ptr(hist),
+                               ctypes.byref(nh))
+    return Result(X, iters.value, info.value, hist[: nh.value].copy(), fro_norm(A))
