@@ -521,6 +521,39 @@ def other_configs(mp, args, dev):
                         "kernels_ms": {k: [round(v["ms"], 3), v["launches"]] for k, v in kg.items()}}
     del Ag, bg, xg
     torch.cuda.empty_cache()
+    # NEXT-2: the 1xTF32 factorisation (MP_VARIANT_TF32) with Algorithm 1 on a well-conditioned C3-sized
+    # system (3 I + G / sqrt(n), kappa ~ 2), and with GMRES-IR (flags bit 8) on C3's Gaussian A itself
+    log("TF32")
+    g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED + 21)
+    At = (torch.randn((ns, ns), dtype=torch.float64, device=dev, generator=g) / math.sqrt(ns)).t()
+    At.diagonal().add_(3.0)
+    xt = (torch.rand((1, ns), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+    bt = (At @ xt).t().contiguous().t()
+    tf = {}
+    for name, o in (("3xtf32", mp.make_opts()), ("tf32", mp.make_opts(variant=mp.MP_VARIANT_TF32))):
+        ms_v, its_v = time_solves(mp, At, bt, o, 3)
+        _, _, _, rep_v = mp.mp_dsgesv_ex(At, bt, None, o)
+        torch.cuda.synchronize()
+        tf[name] = {"ms": round(ms_v, 3), "iters": its_v, "factor_ms": round(rep_v.t_factor_ms, 3),
+                    "refine_ms": round(rep_v.t_refine_ms, 3)}
+    del At, bt, xt
+    g = torch.Generator(device=dev).manual_seed(inputs.BASE_SEED)
+    Ag = torch.randn((ns, ns), dtype=torch.float64, device=dev, generator=g).t()
+    xg = (torch.rand((1, ns), dtype=torch.float64, device=dev, generator=g) * 2 - 1).t()
+    bg = (Ag @ xg).t().contiguous().t()
+    gir = {}
+    for name, o in (("tf32_alg1", mp.make_opts(variant=mp.MP_VARIANT_TF32)),
+                    ("tf32_gmres_ir", mp.make_opts(variant=mp.MP_VARIANT_TF32, flags=256, itermax=63)),
+                    ("3xtf32_gmres_ir", mp.make_opts(flags=256))):
+        ms_v, its_v = time_solves(mp, Ag, bg, o, 1)
+        _, _, _, rep_v = mp.mp_dsgesv_ex(Ag, bg, None, o)
+        torch.cuda.synchronize()
+        gir[name] = {"ms": round(ms_v, 3), "iters": its_v, "factor_ms": round(rep_v.t_factor_ms, 3),
+                     "refine_ms": round(rep_v.t_refine_ms, 3), "fallback_ms": round(rep_v.t_fallback_ms, 3)}
+    res["TF32_C3"] = {"n": ns, "well_conditioned": {"matrix": "3 I + G/sqrt(n) (kappa ~ 2)", **tf},
+                      "gaussian": {"matrix": "C3's N(0,1) A", **gir}}
+    del Ag, bg, xg
+    torch.cuda.empty_cache()
     # C4: n = 49152, nrhs = 16 (A = 19.3 GB fp64), device-generated with a seeded torch generator
     if not args.no_c4:
         n4, r4 = 49152, 16
@@ -536,6 +569,19 @@ def other_configs(mp, args, dev):
         res["C4"] = {"n": n4, "nrhs": r4, "ms": round(ms, 1), "gflops": round(flops(n4) / ms / 1e6, 1), "iters": its,
                      "factor_ms": round(rep.t_factor_ms, 1), "refine_ms": round(rep.t_refine_ms, 1),
                      "fp64_ms": round(ms64, 1), "speedup_vs_fp64": round(ms64 / ms, 3)}
+        # NEXT-2 at C4's size: 3 I + G / sqrt(n) (kappa ~ 2), 3xTF32 against the 1xTF32 factorisation
+        dA.mul_(1.0 / math.sqrt(n4))
+        dA.diagonal().add_(3.0)
+        dB = (dA @ Xt).t().contiguous().t()
+        torch.cuda.synchronize()
+        tf4 = {}
+        for name, o in (("3xtf32", mp.make_opts()), ("tf32", mp.make_opts(variant=mp.MP_VARIANT_TF32))):
+            ms_v, its_v = time_solves(mp, dA, dB, o, 1)
+            _, _, _, rep_v = mp.mp_dsgesv_ex(dA, dB, None, o)
+            torch.cuda.synchronize()
+            tf4[name] = {"ms": round(ms_v, 1), "iters": its_v, "factor_ms": round(rep_v.t_factor_ms, 1),
+                         "refine_ms": round(rep_v.t_refine_ms, 1)}
+        res["TF32_C4"] = {"n": n4, "nrhs": r4, "matrix": "3 I + G/sqrt(n) (kappa ~ 2)", **tf4}
         del dA, dB, Xt
         torch.cuda.empty_cache()
     return res

@@ -73,6 +73,12 @@ extern "C" {
  * if refinement still reaches the binary64 backward criterion. */
 #define MP_VARIANT_FFMA    0   /* FP32 FFMA SGEMM (CUDA cores) */
 #define MP_VARIANT_3XTF32  1   /* tcgen05 tensor cores, 3xTF32 split (hi*hi + hi*lo + lo*hi) */
+/* SURVEY 8(f) NEXT-2, the lower-precision tensor-core factorisation: every tensor-core Schur update
+ * takes operands rounded to TF32 (cvt.rna, 10 stored significand bits: u_f = 2^-11) with binary32
+ * accumulation, one MMA per product (3x fewer than 3xTF32).  The factors are then accurate to
+ * ~2^-11 kappa, so Algorithm 1 converges only for kappa * 2^-11 well below 1; for
+ * harder systems select the GMRES-IR refinement (opts.flags bit 8). */
+#define MP_VARIANT_TF32    2
 
 typedef struct mp_opts {
     int32_t nb;        /* panel width; 0 = default (64 for n<=1024, 128 for n<=4096, else 256) */
@@ -92,7 +98,13 @@ typedef struct mp_opts {
                           bit 6: host A: one copy before the factorisation instead of streaming it in
                                  by column blocks under the factorisation (mp_dsgesv, n >= 4096);
                           bit 7: mp_fgmres: run each binary32 GMRES_SP cycle as a sequence of small
-                                 kernels instead of the one cooperative launch (testing) */
+                                 kernels instead of the one cooperative launch (testing);
+                          bit 8: mp_dsgesv: refine by GMRES-IR instead of Algorithm 1's loop (SURVEY
+                                 8(f) NEXT-2): restarted FGMRES(20) in binary64 on A x = b from x0
+                                 (each right-hand side on its own), every Krylov direction preconditioned by the
+                                 binary32 LU factors (one forward/backward sweep pair); B:5's test at
+                                 every restart, each cycle ends early once its Givens residual
+                                 estimate meets the test; *iters = LU-solve applications */
 } mp_opts;
 
 #define MP_HIST_MAX 64

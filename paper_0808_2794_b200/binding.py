@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpsolve.so")
 
 MP_OK, MP_ERR_CUDA, MP_ERR_NOMEM, MP_ERR_INTERNAL, MP_ERR_NCCL, MP_ERR_UNSUPPORTED = 0, 1, 2, 3, 4, 5
-MP_VARIANT_FFMA, MP_VARIANT_3XTF32 = 0, 1
+MP_VARIANT_FFMA, MP_VARIANT_3XTF32, MP_VARIANT_TF32 = 0, 1, 2
 MP_HIST_MAX = 64
 KCLASSES = ("demote", "panel", "laswp", "trsm", "gemm", "solve", "residual", "trail")
 

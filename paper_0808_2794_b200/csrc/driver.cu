@@ -435,6 +435,11 @@ cudaStream_t copy_stream()
 // columns — recursive panel factorisation (cluster leaves K2 + in-panel K3/K4/K5),
 // the panel's interchanges applied once to every other column (K3), U12 (K4),
 // Schur update of the trailing matrix (K5).
+
+// tensor-core trailing-update variants: 3xTF32 (binary32-accurate, the default) and 1xTF32 (SURVEY 8(f)
+// NEXT-2: operands rounded to TF32, ~2^-11; refinement then needs kappa * 2^-11 < 1 or GMRES-IR)
+inline bool tc_variant(int v) { return v == MP_VARIANT_3XTF32 || v == MP_VARIANT_TF32; }
+
 template <typename T>
 struct Factor {
     T *W;
@@ -485,8 +490,9 @@ struct Factor {
               int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3, bool reuse_b = false) {
         prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
-            if (big && variant == MP_VARIANT_3XTF32 && M >= 256 && N >= 128)
-                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a, terms, reuse_b);
+            if (big && tc_variant(variant) && M >= 256 && N >= 128)
+                launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a,
+                                          variant == MP_VARIANT_TF32 ? 1 : terms, reuse_b);
             else
                 launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
@@ -516,7 +522,7 @@ struct Factor {
             const bool tc = tc_inpanel && w1 >= 128;
             const int64_t M = n - c0 - w1;
             const int kp = (int)round_up(w1, 4);
-            const bool bsplit = sizeof(T) == 4 && tc && variant == MP_VARIANT_3XTF32 && tf32[1] && M >= 256 &&
+            const bool bsplit = sizeof(T) == 4 && tc && tc_variant(variant) && tf32[1] && M >= 256 &&
                                 w - w1 >= 128 && w1 <= 256;
             float *bh = bsplit ? tf32[1] + 2 * (size_t)M * kp : nullptr;
             trsm(q, c0, w1, c0 + w1, c0 + w, bh, bsplit ? bh + (size_t)(w - w1) * kp : nullptr, kp);
@@ -598,7 +604,7 @@ struct Factor {
         // L21 of panel j (rows [j + w, n) x its columns) split hi/lo on the panel stream right after
         // the panel, into the update scratch of that step's parity: the update stream's interchanges
         // and TRSM of the next panel's columns run meanwhile (the split is off its critical path)
-        const bool presplit = sizeof(T) == 4 && variant == MP_VARIANT_3XTF32 && tfU[1] != nullptr;
+        const bool presplit = sizeof(T) == 4 && tc_variant(variant) && tfU[1] != nullptr;
         auto split_l21 = [&](int64_t kp0, int wp, int bb) -> bool {
             const int64_t M = n - kp0 - wp;
             if (!presplit || M < 256) return false;
@@ -694,7 +700,7 @@ void make_factor(Factor<T> &f, T *W, int64_t n, int64_t ldw, int nb, int32_t *ip
     f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
     f.sms = num_sms();
     f.variant = variant;
-    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) {
+    if (sizeof(T) == 4 && tc_variant(variant)) {
         f.tf32[0] = pool.get<float>(tf32_scratch_floats(n, nb));
         f.tf32[1] = pool.get<float>(tf32_scratch_floats(n, nb));
         f.tfU[0] = f.tf32[0];
@@ -744,7 +750,7 @@ void run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n,
 {
     Factor<float> f;
     make_factor<float>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant);
-    if (variant == MP_VARIANT_3XTF32) f.tfC = pool.get<float>(tf32_scratch_floats(n, nb));
+    if (tc_variant(variant)) f.tfC = pool.get<float>(tf32_scratch_floats(n, nb));
     const int64_t nbk = ceil_div(n, (int64_t)nb);
     const int64_t per = ceil_div(nbk, (int64_t)nblocks) * nb;                 // block width (multiple of nb)
     float *S = pool.get<float>((size_t)n * round_up(per, 64));
@@ -894,6 +900,89 @@ void finish_copy_out(const Args &a, const Views &v, cudaStream_t s)
     MP_CUDA(cudaStreamSynchronize(s));
 }
 
+// GMRES-IR refinement (opts.flags bit 8; readings T-3/T-4): per right-hand side,
+// restarted FGMRES(kGirM) in binary64 on A x = b from the x0 already in X, every Krylov direction
+// preconditioned by the binary32 LU (z_k = LUsolve(fl32(P v_k)), the K6 + K7 kernels), the A products by
+// K8, modified Gram-Schmidt / Givens / y / x += Z y by the k_gmres kernels.  B:5's test at every restart;
+// a cycle ends early once |g_{k+1}| < ||x|| cte / 2.  Returns the LU applications (max over columns),
+// or -31 when a column reaches `itermax` applications unconverged or its norms are not finite.
+constexpr int kGirM = 20;
+int gmres_ir_refine(const Views &v, int64_t n, int64_t nrhs, const float *W, int64_t ldw, const int32_t *pinv,
+                    float *Y, const float *inv, SolveScratch &ss, ResidualScratch &rs, StatusIO &sio, double cte,
+                    int itermax, double *hist, int &nhist, Pool &pool, cudaStream_t s, int sms)
+{
+    const int m = kGirM;
+    const int64_t ldv = round_up(n, 32);
+    double *V = pool.get<double>((size_t)ldv * (m + 1)), *Z = pool.get<double>((size_t)ldv * m);
+    double *r = pool.get<double>(n), *ax = pool.get<double>(n);
+    double *Rm = pool.get<double>((size_t)(m + 1) * m), *cs = pool.get<double>(32), *sn = pool.get<double>(32);
+    double *g = pool.get<double>(33), *y = pool.get<double>(32), *hcol = pool.get<double>(32);
+    double *hn = pool.get<double>(32), *sc = pool.get<double>(8), *ones = pool.get<double>(32);
+    double *pd = pool.get<double>(gmres_partial_elems(n));
+    {
+        std::vector<double> h1(32, 1.0);
+        MP_CUDA(cudaMemcpyAsync(ones, h1.data(), 32 * sizeof(double), cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+    }
+    int worst = 0;
+    for (int64_t c = 0; c < nrhs; ++c) {
+        double *x = v.X + c * n;
+        const double *b = v.B + c * n;
+        int apps = 0;
+        bool done = false;
+        for (;;) {
+            // r = b - A x (eps_d), beta, ||x||, the check
+            prof_begin(KC_RESIDUAL, s);
+            launch_residual_products(v.A, v.lda, n, n, 1, x, n, ax, rs, sms, s);
+            MP_CUDA(cudaMemcpyAsync(r, b, (size_t)n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+            launch_combine<double>(r, ax, n, 1, ones, 1.0, -1.0, n, s);
+            prof_end(KC_RESIDUAL, 8.0 * n * n, s);
+            launch_multidot<double>(r, n, 1, r, n, pd, sc + 0, false, s);
+            launch_multidot<double>(x, n, 1, x, n, pd, sc + 1, false, s);
+            double hsc[2];
+            MP_CUDA(cudaMemcpyAsync(hsc, sc, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+            const double beta = std::sqrt(hsc[0]), xn = std::sqrt(hsc[1]);
+            if (!std::isfinite(beta) || !std::isfinite(xn)) break;
+            if (c == 0 && nhist < MP_HIST_MAX) hist[nhist++] = beta == 0.0 ? 0.0 : beta / (xn * cte);
+            if (beta < xn * cte || beta == 0.0) { done = true; break; }
+            if (apps >= itermax) break;
+            launch_cycle_start<double>(sc + 0, g, m, sc + 2, s);
+            int kk = 0;
+            for (int k = 0; k < m; ++k) {
+                double *vk = V + (size_t)k * ldv, *zk = Z + (size_t)k * ldv;
+                launch_scale_copy<double, double>(r, k == 0 ? sc + 2 : hn + (k - 1), true, vk, nullptr, n, s);
+                // z_k = LUsolve(fl32(P v_k)) (eps_s)
+                prof_begin(KC_SOLVE, s);
+                launch_permute_demote_rhs<float>(vk, n, 1, pinv, Y, sio.d, s);
+                launch_lu_solve<float>(W, ldw, n, 1, Y, zk, 0, ss, s, inv);
+                prof_end(KC_SOLVE, 4.0 * n * n, s);
+                ++apps;
+                prof_begin(KC_RESIDUAL, s);
+                launch_residual_products(v.A, v.lda, n, n, 1, zk, n, r, rs, sms, s);
+                prof_end(KC_RESIDUAL, 8.0 * n * n, s);
+                for (int j = 0; j <= k; ++j) {                                   // MGS (eps_d)
+                    launch_multidot<double>(V + (size_t)j * ldv, ldv, 1, r, n, pd, hcol + j, false, s);
+                    launch_combine<double>(r, V + (size_t)j * ldv, ldv, 1, hcol + j, 1.0, -1.0, n, s);
+                }
+                launch_multidot<double>(r, n, 1, r, n, pd, sc + 3, false, s);
+                launch_givens_step<double>(hcol, sc + 3, k, m, Rm, cs, sn, g, hn + k, s);
+                kk = k + 1;
+                double est[2];
+                MP_CUDA(cudaMemcpyAsync(est, g + k + 1, sizeof(double), cudaMemcpyDeviceToHost, s));
+                MP_CUDA(cudaMemcpyAsync(est + 1, hn + k, sizeof(double), cudaMemcpyDeviceToHost, s));
+                MP_CUDA(cudaStreamSynchronize(s));
+                if (est[1] == 0.0 || !(std::fabs(est[0]) >= 0.5 * xn * cte) || apps >= itermax) break;
+            }
+            launch_backsolve<double>(Rm, m, kk, g, y, hn, s);
+            launch_combine<double>(x, Z, ldv, kk, y, 1.0, 1.0, n, s);
+        }
+        if (!done) return -31;
+        worst = std::max(worst, apps);
+    }
+    return worst;
+}
+
 int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_report *rep)
 {
     *info = 0; *iters = 0;
@@ -906,7 +995,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     if (opts) o = *opts;
     const int nb = o.nb > 0 ? o.nb : default_nb(a.n);
     const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
-    if (o.variant != MP_VARIANT_FFMA && o.variant != MP_VARIANT_3XTF32) throw std::runtime_error("unknown variant");
+    if (o.variant != MP_VARIANT_FFMA && !tc_variant(o.variant)) throw std::runtime_error("unknown variant");
     const int64_t n = a.n, nrhs = a.nrhs;
     check_size_limits(n);
     cudaStream_t s = g_stream;
@@ -1010,7 +1099,12 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         launch_lu_solve<float>(W, ldw, n, nrhs, Y, v.X, 0, ss, s, inv);
         prof_end(KC_SOLVE, 4.0 * n * n, s);
         code = -31;
-        for (int it = 0; it <= itermax; ++it) {
+        if (o.flags & 256) {                                      // GMRES-IR (NEXT-2)
+            const int apps = gmres_ir_refine(v, n, nrhs, W, ldw, pinv, Y, inv, ss, rs, sio, cte, itermax, hist, nhist,
+                                             pool, s, sms);
+            if (apps >= 0) { *iters = apps; code = 0; }
+        }
+        for (int it = 0; it <= itermax && !(o.flags & 256); ++it) {
             // ---- step 4 + check: r = b - A x (binary64), norms, verdict; y = fl32(P r)
             prof_begin(KC_RESIDUAL, s);
             launch_residual<float>(v.A, v.lda, n, nrhs, v.B, v.X, R, pinv, Y, cte, rs, sio.d, sms, s);
@@ -1168,7 +1262,7 @@ template <typename T>
 void run_chol(T *W, int64_t n, int64_t ldw, int nb, DevStatus *st, Pool &pool, cudaStream_t s, int variant)
 {
     float *scratch = nullptr;
-    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32 && n > nb)
+    if (sizeof(T) == 4 && tc_variant(variant) && n > nb)
         scratch = pool.get<float>(tf32_scratch_floats(n, nb));
     const int sms = num_sms();
     for (int64_t k = 0; k < n; k += nb) {
@@ -1185,7 +1279,7 @@ void run_chol(T *W, int64_t n, int64_t ldw, int nb, DevStatus *st, Pool &pool, c
         T *A21 = W + (k + w) * ldw + k, *A22 = W + (k + w) * ldw + k + w;
         if constexpr (sizeof(T) == 4) {
             if (scratch && m >= 256)
-                launch_syrk_lower_3xtf32(A21, ldw, A22, ldw, m, w, scratch, sms, s);
+                launch_syrk_lower_3xtf32(A21, ldw, A22, ldw, m, w, scratch, sms, s, variant == MP_VARIANT_TF32 ? 1 : 3);
             else
                 launch_gemm_update<T>(W, ldw, k + w, k + w, k, m, m, w, s);
         } else {
@@ -1235,7 +1329,7 @@ int dsposv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     const int64_t n = a.n, nrhs = a.nrhs;
     const int nb = chol_nb(4, n, o.nb);
     const int itermax = o.itermax > 0 ? std::min(o.itermax, MP_HIST_MAX - 1) : MP_ITERMAX_DEFAULT;
-    if (o.variant != MP_VARIANT_FFMA && o.variant != MP_VARIANT_3XTF32) throw std::runtime_error("unknown variant");
+    if (o.variant != MP_VARIANT_FFMA && !tc_variant(o.variant)) throw std::runtime_error("unknown variant");
     check_size_limits(n);
     cudaStream_t s = g_stream;
     g_launches = 0;
@@ -1843,7 +1937,7 @@ void dist_factor(Comm &cm, const Dist &d, T *Wl, int64_t ldw, int32_t *ipiv, int
     f.ps.ppairs = f.ppairs[0];
     f.ps.nppairs = f.nppairs[0];
     float *tf = nullptr, *tfp = nullptr;
-    if (sizeof(T) == 4 && variant == MP_VARIANT_3XTF32) {
+    if (sizeof(T) == 4 && tc_variant(variant)) {
         tf = pool.get<float>(tf32_scratch_floats(n, (int)nb));
         tfp = pool.get<float>(tf32_scratch_floats(n, (int)nb));
     }
@@ -2355,11 +2449,12 @@ int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_
 {
     return guarded([&] {
         cudaStream_t s = g_stream;
-        if (variant == MP_VARIANT_3XTF32) {
+        if (tc_variant(variant)) {
             float *scratch = nullptr;
             const size_t bytes = ((size_t)2 * M * round_up(K, 4) + (size_t)2 * N * round_up(K, 4) + 4096) * 4;
             MP_CUDA(cudaMallocFromPoolAsync((void **)&scratch, bytes, library_pool(), s));
-            launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, num_sms(), s);
+            launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, num_sms(), s, false,
+                                      variant == MP_VARIANT_TF32 ? 1 : 3);
             MP_CUDA(cudaFreeAsync(scratch, s));
         } else {
             launch_gemm_update<float>(W, ldw, r0, c0, k0, M, N, K, s);

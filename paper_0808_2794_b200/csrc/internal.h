@@ -322,7 +322,7 @@ void launch_symv_products(const double *A, int64_t lda, int64_t n, int64_t nrhs,
                           double *partials, cudaStream_t s);
 // C[M x M] lower tiles -= L21 L21^T, L21 = A[M x K] row-major (3xTF32 tcgen05)
 void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc, int64_t M, int64_t K, float *scratch,
-                              int num_sms, cudaStream_t s);
+                              int num_sms, cudaStream_t s, int terms = 3);
 }  // namespace mp
 
 namespace mp {

@@ -204,11 +204,17 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
                 for (int kc = 0; kc < nk; ++kc) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     unsigned char *st = smem + stage * STAGE_BYTES;
-                    mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
-                    tma_load_2d(st, &tmUh, &full_bar[stage], kc * KC, tn * TM_COLS);
-                    tma_load_2d(st + A_BYTES, &tmUl, &full_bar[stage], kc * KC, tn * TM_COLS);
-                    tma_load_2d(st + 2 * A_BYTES, &tmLh, &full_bar[stage], kc * KC, tm * TM_ROWS);
-                    tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmLl, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                    if (terms == 1) {                                 // 1xTF32 (NEXT-2): the hi boxes only
+                        mbar_expect_tx(&full_bar[stage], A_BYTES + B_BYTES);
+                        tma_load_2d(st, &tmUh, &full_bar[stage], kc * KC, tn * TM_COLS);
+                        tma_load_2d(st + 2 * A_BYTES, &tmLh, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                    } else {
+                        mbar_expect_tx(&full_bar[stage], STAGE_BYTES);
+                        tma_load_2d(st, &tmUh, &full_bar[stage], kc * KC, tn * TM_COLS);
+                        tma_load_2d(st + A_BYTES, &tmUl, &full_bar[stage], kc * KC, tn * TM_COLS);
+                        tma_load_2d(st + 2 * A_BYTES, &tmLh, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                        tma_load_2d(st + 2 * A_BYTES + B_BYTES, &tmLl, &full_bar[stage], kc * KC, tm * TM_ROWS);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -235,6 +241,10 @@ gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_consta
                         const uint32_t off = ks * 32;                  // 8 tf32 = 32 B along the swizzled row
                         const uint64_t dAh = umma_desc_sw128(sAh + off), dAl = umma_desc_sw128(sAl + off);
                         const uint64_t dBh = umma_desc_sw128(sBh + off), dBl = umma_desc_sw128(sBl + off);
+                        if (terms == 1) {                                 // 1xTF32: hi*hi only
+                            umma_tf32(tacc, dAh, dBh, (kc | ks) ? 1u : 0u);
+                            continue;
+                        }
                         if (MP_TF32_TERMS == 4 || terms == 4) {
                             umma_tf32(tacc, dAl, dBl, (kc | ks) ? 1u : 0u);  // lo*lo (4xTF32)
                             umma_tf32(tacc, dAl, dBh, 1u);
@@ -413,7 +423,7 @@ void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t
 // SPD path: C[M x M] (lower tiles) -= L21 L21^T with L21 = A[M x K] (row-major, lda).  The B operand of
 // the 3xTF32 kernel is K-major U^T = L21 itself, so one hi/lo split of L21 serves as both operands.
 void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc, int64_t M, int64_t K, float *scratch,
-                              int num_sms, cudaStream_t s)
+                              int num_sms, cudaStream_t s, int terms)
 {
     if (M <= 0 || K <= 0) return;
     const int kp = (int)round_up(K, 4);
@@ -431,7 +441,7 @@ void launch_syrk_lower_3xtf32(const float *A, int64_t lda, float *C, int64_t ldc
     const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024;
     func_smem_once((const void *)gemm_3xtf32_kernel<true>, smem);
     launch_ex(gemm_3xtf32_kernel<true>, dim3(grid), dim3(GT), smem, s, nullptr, mUh, mUl, mLh, mLl, C, ldc, (int)M,
-              (int)M, (int)K, 3);
+              (int)M, (int)K, terms);
 }
 
 // The hi/lo split of the A operand alone (M x K rows at A, lda) into scratch, in the layout
