@@ -245,6 +245,12 @@ template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
                      SolveScratch &ss, cudaStream_t s, const float *inv = nullptr);
 size_t solve_flag_words(int64_t n);
+// K7 for 2..16+ right-hand sides (k_solve_mr.cu): right-looking blocked sweeps with fixed row
+// ownership and the inverted diagonal blocks (inv required); flags: the 4 nblk words of
+// SolveScratch, epoch: its counter.  launch_lu_solve takes this path when mr_solve_supported().
+bool mr_solve_supported(int64_t n, int64_t nrhs);
+void launch_lu_solve_mr(const float *W, int64_t ldw, int64_t n, int64_t nrhs, float *Y, double *X, int accumulate,
+                        unsigned *flags, unsigned &epoch, const float *inv, cudaStream_t s);
 size_t solve_inv_floats(int64_t n);      // [D_L | M_L | D_U | M_U], each ceil(n/64) 64x64 blocks
 void launch_solve_inverses(const float *W, int64_t ldw, int64_t n, float *inv, cudaStream_t s);
 // max over the diagonal blocks of kappa_inf (L and U) computed by launch_solve_inverses (synchronises s)

@@ -32,7 +32,7 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
                         const double *__restrict__ X, int64_t ldx, double *__restrict__ partial,
                         int64_t cols_per_split, int c_off, int nrhs_total)
 {
-    extern __shared__ __align__(16) double xs[];        // [cols_per_split][MAXR]
+    extern __shared__ __align__(16) double xs[];        // [cols_per_split][R]
     const int s = blockIdx.y;
     const int64_t j0 = (int64_t)s * cols_per_split;
     const int64_t j1 = (ncols < j0 + cols_per_split) ? ncols : j0 + cols_per_split;
@@ -161,12 +161,15 @@ residual_finalize_kernel(int64_t n, int nrhs, int splits, const double *__restri
 
 }  // namespace
 
+// right-hand sides per partial-kernel instantiation (1, 2, 4, 8, 16): the smallest that holds nc
+static int rbucket(int64_t nc) { return nc <= 1 ? 1 : nc <= 2 ? 2 : nc <= 4 ? 4 : nc <= 8 ? 8 : MAXR; }
+
 int64_t residual_splits(int64_t n, int64_t nrhs, int num_sms)
 {
     const int64_t tiles = ceil_div(n, ROWS);
     int64_t s = ceil_div((int64_t)num_sms * 8, tiles);
     // the x slice of a split lives in shared memory: at most 64 KB per CTA
-    const int64_t r = nrhs <= 1 ? 1 : MAXR;
+    const int64_t r = rbucket(std::min<int64_t>(nrhs, MAXR));
     s = std::max<int64_t>(s, ceil_div(n * r * (int64_t)sizeof(double), 64 * 1024));
     s = std::max<int64_t>(1, std::min<int64_t>(s, ceil_div(n, 64)));
     return s;
@@ -189,9 +192,18 @@ static int64_t launch_partials(const double *A, int64_t lda, int64_t rows, int64
     const bool vec = (lda % 2 == 0) && (((uintptr_t)A & 15) == 0);
     for (int c0 = 0; c0 < nr; c0 += MAXR) {
         const int nc = std::min(MAXR, nr - c0);
-        const size_t smem = (size_t)cps * (nc == 1 ? 1 : MAXR) * sizeof(double);
-        auto kern = vec ? (nc == 1 ? residual_partial_kernel<true, 1> : residual_partial_kernel<true, MAXR>)
-                        : (nc == 1 ? residual_partial_kernel<false, 1> : residual_partial_kernel<false, MAXR>);
+        const int rb = rbucket(nc);
+        const size_t smem = (size_t)cps * rb * sizeof(double);
+        using KF = void (*)(const double *, int64_t, int64_t, int64_t, int, const double *, int64_t, double *, int64_t,
+                            int, int);
+        const KF kv[5] = {residual_partial_kernel<true, 1>, residual_partial_kernel<true, 2>,
+                          residual_partial_kernel<true, 4>, residual_partial_kernel<true, 8>,
+                          residual_partial_kernel<true, MAXR>};
+        const KF ks[5] = {residual_partial_kernel<false, 1>, residual_partial_kernel<false, 2>,
+                          residual_partial_kernel<false, 4>, residual_partial_kernel<false, 8>,
+                          residual_partial_kernel<false, MAXR>};
+        const int bi = rb == 1 ? 0 : rb == 2 ? 1 : rb == 4 ? 2 : rb == 8 ? 3 : 4;
+        auto kern = vec ? kv[bi] : ks[bi];
         if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
         kern<<<g1, RT, smem, s>>>(A, lda, rows, cols, nc, X + c0 * ldx, ldx, rs.partial, cps, c0, nr);
     }

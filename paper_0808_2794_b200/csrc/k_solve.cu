@@ -1212,6 +1212,13 @@ template <typename T>
 void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, double *X, int accumulate,
                      SolveScratch &ss, cudaStream_t s, const float *inv)
 {
+    if constexpr (sizeof(T) == 4) {
+        if (inv != nullptr && nrhs >= 2 && mr_solve_supported(n, nrhs)) {
+            launch_lu_solve_mr(reinterpret_cast<const float *>(W), ldw, n, nrhs, reinterpret_cast<float *>(Y), X,
+                               accumulate, ss.flags, ss.epoch, inv, s);
+            return;
+        }
+    }
     const int nblk = (int)ceil_div(n, BS);
     CUtensorMap tm, tDL, tML, tDU, tMU;
     encode_map<T>(&tm, W, ldw, ldw, n);
