@@ -14,6 +14,7 @@
 // over `splits` CTAs per row tile (split-K) and the partial sums are reduced
 // in a fixed order by the finalize kernel (deterministic).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -83,6 +84,55 @@ residual_partial_kernel(const double *__restrict__ A, int64_t lda, int64_t n, in
             if (r0) ps[c * n + i] = acc0[c];
             if (r1) ps[c * n + i + 1] = acc1[c];
         }
+}
+
+// The same partial products with ONE row per thread (ROWS threads per CTA) for 9..16 right-hand
+// sides: the two-row kernel's 2 x 16 binary64 accumulators kept occupancy at 2 CTAs (16 warps) per SM
+// and left it latency-bound (ncu: long-scoreboard stalls, 0.3 of HBM); this one runs 32 warps.
+template <int R>
+__global__ void __launch_bounds__(ROWS)
+residual_partial_r1_kernel(const double *__restrict__ A, int64_t lda, int64_t n, int64_t ncols, int nrhs,
+                           const double *__restrict__ X, int64_t ldx, double *__restrict__ partial,
+                           int64_t cols_per_split, int c_off, int nrhs_total)
+{
+    extern __shared__ __align__(16) double xs[];        // [cols_per_split][R]
+    const int s = blockIdx.y;
+    const int64_t j0 = (int64_t)s * cols_per_split;
+    const int64_t j1 = (ncols < j0 + cols_per_split) ? ncols : j0 + cols_per_split;
+    const int64_t i = (int64_t)blockIdx.x * ROWS + threadIdx.x;
+    for (int64_t idx = threadIdx.x; idx < (j1 - j0) * R; idx += ROWS) {
+        const int64_t jj = idx / R;
+        const int c = (int)(idx - jj * R);
+        xs[idx] = c < nrhs ? X[c * ldx + j0 + jj] : 0.0;
+    }
+    __syncthreads();
+    double acc[R];
+#pragma unroll
+    for (int c = 0; c < R; ++c) acc[c] = 0.0;
+    if (i < n) {
+        int64_t j = j0;
+        for (; j + JU <= j1; j += JU) {
+            double a[JU];
+#pragma unroll
+            for (int u = 0; u < JU; ++u) a[u] = __ldcs(A + (j + u) * lda + i);
+#pragma unroll
+            for (int u = 0; u < JU; ++u) {
+                const double *xj = xs + (j + u - j0) * R;
+#pragma unroll
+                for (int c = 0; c < R; ++c) acc[c] = fma(a[u], xj[c], acc[c]);
+            }
+        }
+        for (; j < j1; ++j) {
+            const double a0 = __ldcs(A + j * lda + i);
+            const double *xj = xs + (j - j0) * R;
+#pragma unroll
+            for (int c = 0; c < R; ++c) acc[c] = fma(a0, xj[c], acc[c]);
+        }
+        double *ps = partial + ((int64_t)s * nrhs_total + c_off) * n;
+#pragma unroll
+        for (int c = 0; c < R; ++c)
+            if (c < nrhs) ps[c * n + i] = acc[c];
+    }
 }
 
 template <typename T>
@@ -204,6 +254,13 @@ static int64_t launch_partials(const double *A, int64_t lda, int64_t rows, int64
                           residual_partial_kernel<false, MAXR>};
         const int bi = rb == 1 ? 0 : rb == 2 ? 1 : rb == 4 ? 2 : rb == 8 ? 3 : 4;
         auto kern = vec ? kv[bi] : ks[bi];
+        static const bool r1_off = std::getenv("MP_RESIDUAL_R1_OFF") != nullptr;
+        if (rb == MAXR && !r1_off) {                 // 9..16 right-hand sides: one row per thread
+            auto k1 = residual_partial_r1_kernel<MAXR>;
+            if (smem > 48 * 1024) func_smem_once((const void *)k1, smem);
+            k1<<<g1, ROWS, smem, s>>>(A, lda, rows, cols, nc, X + c0 * ldx, ldx, rs.partial, cps, c0, nr);
+            continue;
+        }
         if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
         kern<<<g1, RT, smem, s>>>(A, lda, rows, cols, nc, X + c0 * ldx, ldx, rs.partial, cps, c0, nr);
     }

@@ -265,9 +265,10 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
             for (int i = 0; i < RQ; ++i) Rk[i] -= acc[i];
             __syncthreads();                                 // slot consumed
             slot = slot + 1 == NSLOT ? 0 : slot + 1;
+            // the chain block of step t + 1 (this CTA's next solve): its R' is complete now — form
+            // P before the step's other tiles (it is the one thing the next hand-off waits for here)
+            if (k == dk && posof(owned(dk)) == t + 2) make_p(dk);
         }
-        // the next block this CTA solves becomes the chain block at step t + 1: its R' is complete
-        if (dk < nown && posof(owned(dk)) == t + 2) make_p(dk);
         if (have) yb ^= 1;
     }
     cp_wait<0>();
