@@ -14,8 +14,8 @@
 //     the inverses (reading A-19) and P_J = D_J R'_J was computed while waiting (R'_J: every update
 //     but step I's).  The dependent chain per step is one flag hand-off and ONE 64 x 64 x R product
 //     on one SM.
-// Tiles T(J, I) stream HBM -> shared memory with cp.async through a 3-slot ring, prefetched two work
-// items ahead (they never depend on the chain); D tiles are prefetched one solve ahead.
+// Tiles T(J, I) stream HBM -> shared memory with cp.async through a 6-slot ring, prefetched five work
+// items ahead (they never depend on the chain); D / M tiles are loaded one solve ahead.
 // HBM traffic per sweep: n^2/2 * 4 bytes of the factor (each tile once) + the D blocks + O(n R).
 #include <algorithm>
 #include <cstdlib>
@@ -29,7 +29,10 @@ namespace {
 constexpr int MB = 64;            // block rows (= the A-19 inverse blocks)
 constexpr int MNT = 256;          // threads: 64 rows x 4 right-hand-side groups
 constexpr int TLD = MB + 4;       // padded shared row (conflict-free 16-byte row reads)
-constexpr int NSLOT = 3;
+#ifndef MP_MR_SLOTS
+#define MP_MR_SLOTS 6
+#endif
+constexpr int NSLOT = MP_MR_SLOTS;   // tile ring: NSLOT - 1 items in flight ahead of the one in use
 
 struct MrArgs {
     const float *W;
@@ -54,6 +57,12 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
 {
     unsigned v;
@@ -102,8 +111,11 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
     const int nown = (nblk - g + G - 1) / G;                 // blocks g, g + G, ...
     const int64_t n = a.n;
     float *Rs = sm;                                          // [nown][64][R]
-    float *Yb[2] = {Rs + (size_t)nown * MB * R, Rs + (size_t)nown * MB * R + MB * R};
-    float *Pb = Yb[1] + MB * R;                              // [64][R]  D R' of the next block to solve
+    // Y of the current / next step: Yb(0), Yb(1) — computed from `sm` (never through an array of
+    // pointers: the compiler then keeps shared-memory instructions instead of generic ones)
+    float *const Ybase = Rs + (size_t)nown * MB * R;         // [2][64][R]
+    auto Yb = [&](int b) { return Ybase + b * (MB * R); };
+    float *Pb = Ybase + 2 * MB * R;                          // [64][R]  D R' of the next block to solve
     float *ring = Pb + MB * R;                               // [NSLOT][64][TLD]
     float *Ds = ring + NSLOT * MB * TLD;                     // [64][TLD]
     float *Ms = Ds + MB * TLD;                               // [64][TLD]
@@ -199,19 +211,21 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
     };
     int dk = 0;                                              // ordinal of the next owned block to solve
     if (nown > 0) load_dm(0);
-    // the first two tiles (item i lives in ring slot i mod NSLOT)
+    // the first NSLOT - 1 tiles (item i lives in ring slot i mod NSLOT)
     Item pf = first_item();
     int slot = 0;
     issue(pf, 0);
-    pf = next_item(pf);
-    issue(pf, 1);
-    int yb = 0;                                              // Yb[yb] holds Y of the current step
-    bool have = false;                                       // Yb[yb] already holds Y_blk(t) (solved here)
+    for (int j = 1; j < NSLOT - 1; ++j) {
+        pf = next_item(pf);
+        issue(pf, j);
+    }
+    int yb = 0;                                              // Yb(yb) holds Y of the current step
+    bool have = false;                                       // Yb(yb) already holds Y_blk(t) (solved here)
     if (nown > 0 && posof(owned(0)) == 0) {                  // the first block: Y = D R
         make_p(0);
 #pragma unroll
-        for (int i = 0; i < RQ; ++i) Yb[0][r * R + q * RQ + i] = Pb[r * R + q * RQ + i];
-        publish(0, Yb[0]);
+        for (int i = 0; i < RQ; ++i) Yb(0)[r * R + q * RQ + i] = Pb[r * R + q * RQ + i];
+        publish(0, Yb(0));
         dk = 1;
         have = true;
         if (dk < nown) load_dm(dk);
@@ -222,13 +236,15 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
         const int k0 = first_after(t);
         if (k0 >= nown) break;                               // every owned block is solved
         if (!have) {
-            if (threadIdx.x == 0)
-                while (ld_acquire(a.flag + I) != a.epoch) { }
+            if (threadIdx.x == 0) {
+                while (ld_relaxed(a.flag + I) != a.epoch) { }   // poll without invalidating L1 each time
+                (void)ld_acquire(a.flag + I);                      // then one acquire (orders the Y reads)
+            }
             __syncthreads();
             const int64_t i0 = (int64_t)I * MB;
             for (int e = threadIdx.x; e < MB * R; e += MNT) {
                 const int c = e / MB, rr = e - c * MB;
-                Yb[yb][rr * R + c] = (c < a.nrhs && i0 + rr < n) ? __ldcg(a.Y + (int64_t)c * n + i0 + rr) : 0.f;
+                Yb(yb)[rr * R + c] = (c < a.nrhs && i0 + rr < n) ? __ldcg(a.Y + (int64_t)c * n + i0 + rr) : 0.f;
             }
         }
         __syncthreads();
@@ -238,8 +254,8 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
             float acc[RQ];
 #pragma unroll
             for (int i = 0; i < RQ; ++i) acc[i] = 0.f;
-            tile_times<R>(Ms, Yb[yb], r, q, acc);
-            float *Yn = Yb[yb ^ 1];
+            tile_times<R>(Ms, Yb(yb), r, q, acc);
+            float *Yn = Yb(yb ^ 1);
 #pragma unroll
             for (int i = 0; i < RQ; ++i) Yn[r * R + q * RQ + i] = Pb[r * R + q * RQ + i] - acc[i];
             publish(k0, Yn);
@@ -250,16 +266,16 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
             if (dk < nown) load_dm(dk);
         }
         for (int k = kt; k < nown; ++k) {
-            // item (t, k): tile T(owned(k), I) in ring slot `slot`; the item two ahead goes into the
-            // slot consumed last (free since the barrier that ended it)
+            // item (t, k): tile T(owned(k), I) in ring slot `slot`; the item NSLOT - 1 ahead goes into
+            // the slot consumed last (free since the barrier that ended it)
             pf = next_item(pf);
             issue(pf, slot == 0 ? NSLOT - 1 : slot - 1);
-            cp_wait<2>();                                    // this item's group is complete
+            cp_wait<NSLOT - 1>();                            // this item's group is complete
             __syncthreads();
             float acc[RQ];
 #pragma unroll
             for (int i = 0; i < RQ; ++i) acc[i] = 0.f;
-            tile_times<R>(ring + slot * MB * TLD, Yb[yb], r, q, acc);
+            tile_times<R>(ring + slot * MB * TLD, Yb(yb), r, q, acc);
             float *Rk = Rs + ((size_t)k * MB + r) * R + q * RQ;
 #pragma unroll
             for (int i = 0; i < RQ; ++i) Rk[i] -= acc[i];
