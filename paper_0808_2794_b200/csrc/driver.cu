@@ -545,7 +545,7 @@ struct Factor {
         emit_job = EmitJob{ps.orig, k, n, ppairs[b], nppairs[b]};
         emitted = false;
         if (ll_panel && lpos && sizeof(T) == 4 && w <= 256) {
-            const int wl = panel_leaf_width<T>(n - k);
+            const int wl = std::min(32, panel_leaf_width<T>(n - k));   // (left-looking leaves: <= 32 wide)
             if (wl <= 0) throw std::runtime_error("matrix too tall for one panel cluster");
             for (int64_t c0 = k; c0 < k + w; c0 += wl) {
                 const int ww = (int)std::min<int64_t>(wl, k + w - c0);

@@ -721,9 +721,13 @@ struct LeafCfg { int nt, rpt, w; };
 #endif
 #define MP_LEAF_C1 MP_LEAF_C1_NT, MP_LEAF_C1_RPT, 32
 #define MP_LEAF_C0 MP_LEAF_C0_NT, MP_LEAF_C0_RPT, 32
-constexpr LeafCfg kCfgF[] = {{MP_LEAF_C0}, {MP_LEAF_C1}, {512, 4, 16}, {512, 8, 8}};
-constexpr LeafCfg kCfgD[] = {{128, 4, 16}, {256, 4, 16}, {512, 4, 8}, {512, 8, 4}};
-constexpr int kNumCfg = 4;
+// {256, 3, 32} between them: the per-column update scales with the rows per thread (cycles per
+// column at m = 12288: 2113 with 4 rows, ~1720 with 2 at m = 8192; tools/bench_panel.cu).
+// (Measured and dropped: 64-column leaves for m <= 8192, {256, 2, 64}: 87-96 us per leaf against
+// 2 x 40 us + the in-panel K = 32 update and interchange they replace; C3 47.9 vs 46.4 ms.)
+constexpr LeafCfg kCfgF[] = {{MP_LEAF_C0}, {256, 3, 32}, {MP_LEAF_C1}, {512, 4, 16}, {512, 8, 8}};
+constexpr LeafCfg kCfgD[] = {{128, 4, 16}, {256, 3, 16}, {256, 4, 16}, {512, 4, 8}, {512, 8, 4}};
+constexpr int kNumCfgF = 5, kNumCfgD = 5;
 
 int g_cluster = 0;   // largest cluster size the device accepts (16, else 8)
 
@@ -737,9 +741,12 @@ void launch_cfg(const LeafArgs<T> &a, int cl, cudaStream_t s)
     static const bool fullw = [] { const char *e = std::getenv("MP_LEAF_FULLW"); return e && e[0] == '1'; }();
     auto kern = cl > 1 ? (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, true, false> : panel_leaf_kernel<T, NT, RPT, W, UG, true>)
                        : (fullw ? panel_leaf_kernel<T, NT, RPT, W, UG, false, false> : panel_leaf_kernel<T, NT, RPT, W, UG, false>);
-    if constexpr (sizeof(T) == 4)
+    if constexpr (sizeof(T) == 4 && W <= 32) {
         if (a.ll) kern = cl > 1 ? panel_leaf_kernel<T, NT, RPT, W, UG, true, true, true>
                                 : panel_leaf_kernel<T, NT, RPT, W, UG, false, true, true>;
+    } else if (a.ll) {
+        throw CudaError{cudaErrorInvalidValue, "left-looking leaves are at most 32 columns wide", __LINE__};
+    }
     if (cl > 8) func_cluster16_once((const void *)kern);
     const size_t dsm = a.ll ? ll_smem_bytes<T, W>() : 0;
     if (a.ll) func_smem_once((const void *)kern, dsm);
@@ -776,12 +783,13 @@ int cluster_size()
     return g_cluster;
 }
 
-int select_cfg(size_t elem, int64_t m, int cl)
+// narrow32: leaves of at most 32 columns (the left-looking mode)
+int select_cfg(size_t elem, int64_t m, int cl, bool narrow32 = false)
 {
     const LeafCfg *c = elem == 4 ? kCfgF : kCfgD;
     static const int first = [] { const char *e = std::getenv("MP_LEAF_MIN_CFG"); return e ? std::atoi(e) : 0; }();
-    for (int i = first; i < kNumCfg; ++i)
-        if ((int64_t)cl * c[i].nt * c[i].rpt >= m) return i;
+    for (int i = first; i < (elem == 4 ? kNumCfgF : kNumCfgD); ++i)
+        if (!(narrow32 && c[i].w > 32) && (int64_t)cl * c[i].nt * c[i].rpt >= m) return i;
     return -1;
 }
 
@@ -803,7 +811,7 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
     const int clmax = cluster_size();
     const bool ll = lpos != nullptr;
     const int64_t m = n - (ll ? ll_k : c0);
-    const int sel = select_cfg(sizeof(T), m, clmax);
+    const int sel = select_cfg(sizeof(T), m, clmax, ll);
     const LeafCfg *cfgs = sizeof(T) == 4 ? kCfgF : kCfgD;
     if (sel < 0 || w > cfgs[sel].w)
         throw CudaError{cudaErrorInvalidValue, "panel leaf does not fit one cluster", __LINE__};
@@ -817,15 +825,17 @@ void launch_panel_leaf(T *W, int64_t ldw, int64_t n, int64_t c0, int w, int32_t 
     if constexpr (sizeof(T) == 4) {
         switch (sel) {
         case 0: launch_cfg<T, MP_LEAF_C0>(a, cl, s); break;
-        case 1: launch_cfg<T, MP_LEAF_C1>(a, cl, s); break;
-        case 2: launch_cfg<T, 512, 4, 16>(a, cl, s); break;
+        case 1: launch_cfg<T, 256, 3, 32>(a, cl, s); break;
+        case 2: launch_cfg<T, MP_LEAF_C1>(a, cl, s); break;
+        case 3: launch_cfg<T, 512, 4, 16>(a, cl, s); break;
         default: launch_cfg<T, 512, 8, 8>(a, cl, s); break;
         }
     } else {
         switch (sel) {
         case 0: launch_cfg<T, 128, 4, 16>(a, cl, s); break;
-        case 1: launch_cfg<T, 256, 4, 16>(a, cl, s); break;
-        case 2: launch_cfg<T, 512, 4, 8>(a, cl, s); break;
+        case 1: launch_cfg<T, 256, 3, 16>(a, cl, s); break;
+        case 2: launch_cfg<T, 256, 4, 16>(a, cl, s); break;
+        case 3: launch_cfg<T, 512, 4, 8>(a, cl, s); break;
         default: launch_cfg<T, 512, 8, 4>(a, cl, s); break;
         }
     }

@@ -14,12 +14,12 @@ bool pdl_enabled() { return false; }
 using namespace mp;
 int main(int argc, char **argv) {
   for (int m : {512, 1024, 2048, 4096, 6144, 8192, 12288, 16384}) {
-    const int n = m, ldw = ((n + 63) / 64) * 64, w = 32;
-    std::vector<float> h((size_t)n * ldw);
+    const int n = m, ldw = ((n + 63) / 64) * 64, w = panel_leaf_width<float>(m);
+    std::vector<float> h((size_t)n * ldw);  // (pairs buffer below: 2w pairs)
     std::mt19937 rng(1); std::normal_distribution<float> nd;
     for (auto &v : h) v = nd(rng);
     float *W; int32_t *ipiv, *orig, *pairs, *np; DevStatus *st;
-    cudaMalloc(&W, h.size() * 4); cudaMalloc(&ipiv, n * 4); cudaMalloc(&orig, n * 4); cudaMalloc(&pairs, 4 * 64 * 4);
+    cudaMalloc(&W, h.size() * 4); cudaMalloc(&ipiv, n * 4); cudaMalloc(&orig, n * 4); cudaMalloc(&pairs, 4 * 128 * 4);
     cudaMalloc(&np, 4); cudaMalloc(&st, sizeof(DevStatus)); cudaMemset(st, 0, sizeof(DevStatus));
     std::vector<int> o(n); for (int i = 0; i < n; ++i) o[i] = i; cudaMemcpy(orig, o.data(), n * 4, cudaMemcpyHostToDevice);
     PanelScratch ps{orig, pairs, np, nullptr, nullptr, nullptr};
@@ -37,7 +37,7 @@ int main(int argc, char **argv) {
 #ifdef MP_PANEL_TRACE
     cudaMemcpyFromSymbol(tr, g_trace, sizeof(tr));
 #endif
-    printf("m=%d leaf w=32: %.1f us (%s)  per-column cycles [argmax, push, wait, reduce, update]:\n", m, best * 1e3, cudaGetErrorString(e));
+    printf("m=%d leaf w=%d: %.1f us (%s)  per-column cycles [argmax, push, wait, reduce, update]:\n", m, w, best * 1e3, cudaGetErrorString(e));
     double acc[5] = {0};
     for (int c = 1; c < 31; ++c) {
       acc[0] += tr[c][1] - tr[c][0]; acc[1] += tr[c][2] - tr[c][1]; acc[2] += tr[c][3] - tr[c][2]; acc[3] += tr[c][4] - tr[c][3]; acc[4] += tr[c + 1][0] - tr[c][4];
