@@ -1258,36 +1258,101 @@ int chol_nb(size_t elem, int64_t n, int requested)
     return std::max(1, std::min(nb, mx));
 }
 
+// Schur update of the SPD factorisation, C = W[r0.., c0..] (M x N) -= L21 L21^T restricted to the
+// rows / columns given, with L21 = W[r0.., k..k+w) and L21^T read from the upper block W[k.., c0..)
+// (written there by the TRSM).  lower: C square on the diagonal, only the tiles touching its
+// lower triangle (the SYRK); else a plain block (the look-ahead's next block column).
 template <typename T>
-void run_chol(T *W, int64_t n, int64_t ldw, int nb, DevStatus *st, Pool &pool, cudaStream_t s, int variant)
+void chol_update(T *W, int64_t ldw, int64_t k, int w, int64_t r0, int64_t c0, int64_t M, int64_t N, bool lower,
+                 float *scratch, int nsm, cudaStream_t q, int variant)
+{
+    if (M <= 0 || N <= 0) return;
+    prof_begin(KC_TRAIL, q);
+    T *A21 = W + r0 * ldw + k, *C = W + r0 * ldw + c0;
+    if constexpr (sizeof(T) == 4) {
+        const int terms = variant == MP_VARIANT_TF32 ? 1 : 3;
+        if (scratch && lower && M >= 256)
+            launch_syrk_lower_3xtf32(A21, ldw, C, ldw, M, w, scratch, nsm, q, terms);
+        else if (scratch && !lower && M >= 256 && N >= 128)
+            launch_gemm_update_3xtf32(W, ldw, r0, c0, k, M, N, w, scratch, nsm, q, false, terms);
+        else
+            launch_gemm_update<T>(W, ldw, r0, c0, k, M, N, w, q);
+    } else {
+        if (!launch_dgemm_dmma(A21, ldw, W + k * ldw + c0, ldw, C, ldw, M, N, w, q, lower))
+            launch_gemm_update<T>(W, ldw, r0, c0, k, M, N, w, q);
+    }
+    prof_end(KC_TRAIL, lower ? (double)M * (M + 1) * w : 2.0 * M * N * w, q);   // SYRK: lower triangle incl. diagonal
+}
+
+template <typename T>
+void chol_panel(T *W, int64_t ldw, int64_t n, int64_t k, int w, DevStatus *st, cudaStream_t q)
+{
+    prof_begin(KC_PANEL, q);
+    launch_potrf_diag<T>(W, ldw, k, w, st, q);
+    prof_end(KC_PANEL, (double)w * w * w / 3.0, q);
+    const int64_t m = n - k - w;
+    if (m <= 0) return;
+    prof_begin(KC_TRSM, q);
+    launch_trsm_chol<T>(W, ldw, k, w, n, q);
+    prof_end(KC_TRSM, (double)w * w * m, q);
+}
+
+// Right-looking blocked Cholesky (SPOTRF's structure).  With look-ahead (depth 1, the LU
+// path's streams, §7): step k's SYRK is split into the next block column [kn, kn + wn) (a plain
+// block update, first, on the update partition) and the rest (lower tiles of [kn + wn, n)^2); the
+// diagonal block and TRSM of panel kn run on the panel stream as soon as their block column is
+// up to date, beside the rest of step k's SYRK.  Concurrent work touches disjoint blocks: the
+// panel stream writes block column kn (lower) and block row kn (L21^T, upper), the SYRK only rows
+// and columns >= kn + wn.  Every entry receives the same operations in the same order.
+template <typename T>
+void run_chol(T *W, int64_t n, int64_t ldw, int nb, DevStatus *st, Pool &pool, cudaStream_t s, int variant,
+              bool lookahead = true)
 {
     float *scratch = nullptr;
     if (sizeof(T) == 4 && tc_variant(variant) && n > nb)
         scratch = pool.get<float>(tf32_scratch_floats(n, nb));
     const int sms = num_sms();
+    const ExecRes *ex = nullptr;
+    if (lookahead && n > 2 * (int64_t)nb) {
+        const ExecRes &e = exec_res();
+        if (e.ok) ex = &e;
+    }
+    if (!ex) {
+        for (int64_t k = 0; k < n; k += nb) {
+            const int w = (int)std::min<int64_t>(nb, n - k);
+            chol_panel<T>(W, ldw, n, k, w, st, s);
+            const int64_t m = n - k - w;
+            if (m <= 0) break;
+            chol_update<T>(W, ldw, k, w, k + w, k + w, m, m, true, scratch, sms, s, variant);
+        }
+        return;
+    }
+    cudaStream_t sP = ex->sP, sU = ex->sU;
+    const int nsm = ex->smsU;
+    cudaEvent_t e0 = la_event(0), eP = la_event(1), eN = la_event(3), eEndP = la_event(4), eEndU = la_event(5);
+    MP_CUDA(cudaEventRecord(e0, s));
+    MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
+    MP_CUDA(cudaStreamWaitEvent(sU, e0, 0));
+    chol_panel<T>(W, ldw, n, 0, (int)std::min<int64_t>(nb, n), st, sP);
+    MP_CUDA(cudaEventRecord(eP, sP));
     for (int64_t k = 0; k < n; k += nb) {
         const int w = (int)std::min<int64_t>(nb, n - k);
-        prof_begin(KC_PANEL, s);
-        launch_potrf_diag<T>(W, ldw, k, w, st, s);
-        prof_end(KC_PANEL, (double)w * w * w / 3.0, s);
-        const int64_t m = n - k - w;
-        if (m <= 0) break;
-        prof_begin(KC_TRSM, s);
-        launch_trsm_chol<T>(W, ldw, k, w, n, s);
-        prof_end(KC_TRSM, (double)w * w * m, s);
-        prof_begin(KC_TRAIL, s);
-        T *A21 = W + (k + w) * ldw + k, *A22 = W + (k + w) * ldw + k + w;
-        if constexpr (sizeof(T) == 4) {
-            if (scratch && m >= 256)
-                launch_syrk_lower_3xtf32(A21, ldw, A22, ldw, m, w, scratch, sms, s, variant == MP_VARIANT_TF32 ? 1 : 3);
-            else
-                launch_gemm_update<T>(W, ldw, k + w, k + w, k, m, m, w, s);
-        } else {
-            if (!launch_dgemm_dmma(A21, ldw, W + k * ldw + k + w, ldw, A22, ldw, m, m, w, s, true))
-                launch_gemm_update<T>(W, ldw, k + w, k + w, k, m, m, w, s);
-        }
-        prof_end(KC_TRAIL, (double)m * (m + 1) * w, s);        // SYRK: lower triangle incl. diagonal
+        const int64_t kn = k + w;
+        if (kn >= n) break;
+        const int wn = (int)std::min<int64_t>(nb, n - kn);
+        const int64_t m = n - kn;
+        MP_CUDA(cudaStreamWaitEvent(sU, eP, 0));
+        chol_update<T>(W, ldw, k, w, kn, kn, m, wn, false, scratch, nsm, sU, variant);     // next block column
+        MP_CUDA(cudaEventRecord(eN, sU));
+        MP_CUDA(cudaStreamWaitEvent(sP, eN, 0));
+        chol_panel<T>(W, ldw, n, kn, wn, st, sP);                                         // panel kn
+        MP_CUDA(cudaEventRecord(eP, sP));
+        chol_update<T>(W, ldw, k, w, kn + wn, kn + wn, m - wn, m - wn, true, scratch, nsm, sU, variant);  // the rest
     }
+    MP_CUDA(cudaEventRecord(eEndP, sP));
+    MP_CUDA(cudaEventRecord(eEndU, sU));
+    MP_CUDA(cudaStreamWaitEvent(s, eEndP, 0));
+    MP_CUDA(cudaStreamWaitEvent(s, eEndU, 0));
 }
 
 // binary64 SPD solve on a fresh working copy (the fallback, and mp_dposv).  Returns info:
@@ -1379,7 +1444,7 @@ int dsposv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
     double hist[MP_HIST_MAX] = {0};
     bool used_inv = false;
     if (!code) {
-        run_chol<float>(W, n, ldw, nb, sio.d, pool, s, o.variant);             // step 1 (SPOTRF)
+        run_chol<float>(W, n, ldw, nb, sio.d, pool, s, o.variant, !(o.flags & 16));   // step 1 (SPOTRF)
         t_fac = tm.mark();
         const DevStatus &st1 = sio.read();
         if (st1.flags & ST_ZERO_PIVOT) code = -3;                              // reading C-1

@@ -169,8 +169,10 @@ potrf_diag_kernel(T *__restrict__ W, int64_t ldw, int64_t k, int w, DevStatus *s
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *P = reinterpret_cast<T *>(smem_raw);                       // packed lower, w (w + 1) / 2
     T *LT = P + pk(w, 0);                                         // [w][CW] chunk rows, transposed
+    // no early trigger: the dependent TRSM's CTAs (~100 KB of shared memory each) would sit
+    // resident for the whole factorisation of this block, on SMs the look-ahead's concurrent
+    // SYRK launches need (measured: C3-size SPD 48.4 vs 42.2 ms with the trigger at the start)
     pdl_wait();
-    pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = PTHREADS / 32;
     T *Wd = W + k * ldw + k;
@@ -264,6 +266,7 @@ potrf_diag_kernel(T *__restrict__ W, int64_t ldw, int64_t k, int w, DevStatus *s
         }
         __syncthreads();
     }
+    pdl_trigger();
     // L11 into the lower block, L11^T into the upper block
     for (int i = warp; i < w; i += NW)
         for (int j = lane; j <= i; j += 32) {
