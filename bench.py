@@ -283,8 +283,8 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
 # --------------------------------------------------------------------------- our arm
 def _gemm_traffic():
     """dram bytes (read + write) of one trailing-update launch from the committed ncu --set full
-    capture (profiles/r01_gemm_full_v4.json), with its algorithmic bytes; None if absent."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01_gemm_full_v4.json")
+    capture of the current code (profiles/r02_gemm_full.json), with its algorithmic bytes; None if absent."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full.json")
     try:
         with open(p) as f:
             d = json.load(f)
