@@ -714,7 +714,7 @@ def main():
         roof = {"kernel": "trailing Schur update (K5, %s)" % args.variant,
                 "bound": "tensor" if args.variant == "3xtf32" else "alu",
                 "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-                "traffic": _gemm_traffic(),
+                "traffic": _gemm_traffic() if args.variant == "3xtf32" else None,   # (the capture is of the 3xTF32 kernel)
                 "peak_source": ("measured bf16_tflops_sustained x 1.1/2.25 (nominal tf32/bf16), " + pk_src)
                 if args.variant == "3xtf32" else
                 f"derived: 148 SM x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (sm_max_mhz, {pk_src})",

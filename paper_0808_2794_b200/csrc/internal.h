@@ -206,6 +206,10 @@ void launch_dgemm_dfma(const double *A, int64_t lda, const double *B, int64_t ld
                        int64_t M, int64_t N, int64_t K, cudaStream_t s);
 bool launch_dgemm_dmma(const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc,
                        int64_t M, int64_t N, int64_t K, cudaStream_t s, bool lower = false);
+// binary32 FFMA update with TMA-staged tiles (k_sgemm_tma.cu): C[M x N] -= A[M x K] B[K x N], row-major;
+// false = TMA alignment not met (16-byte bases, leading dimensions multiple of 4), nothing launched
+bool launch_sgemm_tma(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
+                      int64_t N, int64_t K, cudaStream_t s);
 template <typename T>
 void launch_gemm_ops(const T *A, int64_t lda, const T *B, int64_t ldb, T *C, int64_t ldc, int64_t M, int64_t N,
                      int64_t K, cudaStream_t s);

@@ -494,6 +494,8 @@ void launch_gemm_ops<float>(const float *A, int64_t lda, const float *B, int64_t
     if (K <= 128 && N <= 32) return launch_ts<float, 64, 32>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (K <= 128 && N <= 64) return launch_ts<float, 64, 64>(A, lda, B, ldb, C, ldc, M, N, K, s);
     if (K <= 128 && N <= 128) return launch_ts<float, 64, 128>(A, lda, B, ldb, C, ldc, M, N, K, s);
+    static const bool no_tma = std::getenv("MP_NO_SGEMM_TMA") != nullptr;   // A/B: the register-staged tile kernel
+    if (!no_tma && launch_sgemm_tma(A, lda, B, ldb, C, ldc, M, N, K, s)) return;
     launch_tiles<float, 128, 128, 8, 8, 8>(A, lda, B, ldb, C, ldc, M, N, K, s);
 }
 
