@@ -54,7 +54,8 @@ constexpr int MAXR = 16;               // right-hand sides per launch
 template <typename T> struct SCfg;
 template <> struct SCfg<float> {
 #ifndef MP_SOLVE_DN
-#define MP_SOLVE_DN 2                 // swept 1..5: with tagged exchanges 2 is best (0.77 vs 0.83 ms per pair at n = 16384)
+#define MP_SOLVE_DN 3                 // swept 1..5: 2 was best (0.77 vs 0.83 ms per pair at n = 16384) while the publisher's
+                                      // fence sat on every block; without it 3 is (0.612 -> 0.567 ms with YB = 4)
 #endif
 #ifndef MP_SOLVE_CHB
 #define MP_SOLVE_CHB 2
@@ -65,7 +66,7 @@ template <> struct SCfg<float> {
 #define MP_HS 8
 #endif
 #ifndef MP_YB
-#define MP_YB 8
+#define MP_YB 4                       // y blocks per helper batch (8: 0.585 vs 0.567 ms per pair at DN = 3)
 #endif
     static constexpr int HS = MP_HS;              // helper ring stages
     static constexpr int YB = MP_YB;              // y blocks fetched per helper batch
@@ -548,6 +549,8 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
     const int nblk = a.nblk, nrhs = a.nrhs;
     const int64_t n = a.n;
 
+    bool tagged_y = false;                                    // y exchanged through tagged words
+    if constexpr (sizeof(T) == 4) tagged_y = a.tY != nullptr;
     if (blockIdx.x == 0) {
         // =================================================================== chain CTA
         constexpr int NST = C::CHB * (1 + DN);
@@ -746,7 +749,9 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
 #endif
                 } else if (warp == WPUB) {
                     nbar_sync(2, 160);
-                    if (lane == 0) {
+                    // the flag exchange only: with tagged words the helpers read y itself, and the
+                    // fence (waiting for the y / x stores to reach L2) would sit on every block's step
+                    if (lane == 0 && !tagged_y) {
                         __threadfence();
                         st_release_u32(a.yflag + I, a.epoch);
                     }
@@ -847,7 +852,7 @@ __global__ void __launch_bounds__(NTH, 1) tri_sweep_kernel(const __grid_constant
                 // publish y_I for the helpers: the barrier orders the solvers' stores before the
                 // release (cumulativity), so the solvers never wait on the fence
                 nbar_sync(2, (nsolv + 1) * 32);
-                if (lane == 0) {
+                if (lane == 0 && !tagged_y) {
                     __threadfence();
                     st_release_u32(a.yflag + I, a.epoch);
                 }
