@@ -291,6 +291,11 @@ struct ExecRes {
     cudaStream_t sU3 = nullptr;
     int smsU3 = 0;
     double small_frac = 0.0;    // steps with n - k < small_frac * n use sU3
+    // and the largest one for very large trailing matrices (C4 sizes: the update, not the panel,
+    // is then the critical path at every step; the panel keeps one 16-SM cluster)
+    cudaStream_t sU4 = nullptr;
+    int smsU4 = 0;
+    int64_t huge_rows = 0;      // steps with n - k > huge_rows use sU4
 };
 
 ExecRes make_exec_res(int dev)
@@ -367,6 +372,27 @@ ExecRes make_exec_res(int dev)
             r.sU3 = (cudaStream_t)sU3;
             r.smsU3 = (int)rest3.sm.smCount;
             r.small_frac = frac;
+        }
+        cudaGetLastError();
+    }
+    {
+        unsigned psms4 = 16;                  // SMs kept free for trailing matrices > MP_HUGE_ROWS rows (MP_PANEL_SMS_HUGE)
+        if (const char *e = std::getenv("MP_PANEL_SMS_HUGE")) psms4 = (unsigned)std::max(16, std::atoi(e));
+        int64_t rows = 16384;                 // (C3, n = 16384, never qualifies; C4 at n = 49152: 819 -> 768 ms)
+        if (const char *e = std::getenv("MP_HUGE_ROWS")) rows = std::atoll(e);
+        CUdevResource grp4[1], rest4;
+        unsigned ng4 = 1;
+        CUdevResourceDesc dU4;
+        CUgreenCtx gU4;
+        CUstream sU4;
+        if (psms4 < psms && rows > 0 &&
+            split(grp4, &ng4, &all, &rest4, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, psms4) == CUDA_SUCCESS &&
+            ng4 == 1 && grp4[0].sm.smCount >= 16 && genDesc(&dU4, &rest4, 1) == CUDA_SUCCESS &&
+            mkCtx(&gU4, dU4, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS &&
+            mkStream(&sU4, gU4, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+            r.sU4 = (cudaStream_t)sU4;
+            r.smsU4 = (int)rest4.sm.smCount;
+            r.huge_rows = rows;
         }
         cudaGetLastError();
     }
@@ -628,10 +654,11 @@ struct Factor {
             const int wn = kn < ke ? (int)std::min<int64_t>(nb, ke - kn) : 0;
             const int b = idx & 1;
             // early steps (large trailing matrix): the larger update partition
-            const bool early = ex.sU2 && (double)(n - kn) > ex.big_frac * (double)n;
-            const bool late = !early && ex.sU3 && (double)(n - kn) < ex.small_frac * (double)n;
-            cudaStream_t sU = early ? ex.sU2 : (late ? ex.sU3 : ex.sU);
-            const int smsu = early ? ex.smsU2 : (late ? ex.smsU3 : ex.smsU);
+            const bool huge = ex.sU4 && n - kn > ex.huge_rows;
+            const bool early = !huge && ex.sU2 && (double)(n - kn) > ex.big_frac * (double)n;
+            const bool late = !huge && !early && ex.sU3 && (double)(n - kn) < ex.small_frac * (double)n;
+            cudaStream_t sU = huge ? ex.sU4 : early ? ex.sU2 : (late ? ex.sU3 : ex.sU);
+            const int smsu = huge ? ex.smsU4 : early ? ex.smsU2 : (late ? ex.smsU3 : ex.smsU);
             if (sU != cur) {                                   // keep the update work in order
                 MP_CUDA(cudaEventRecord(eSw, cur));
                 MP_CUDA(cudaStreamWaitEvent(sU, eSw, 0));
