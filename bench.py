@@ -294,6 +294,20 @@ def _gemm_traffic():
             "ratio": d["traffic_over_algorithmic"], "launch": "M=N=%d K=%d (%s)" % (d["M"], d["K"], os.path.basename(p))}
 
 
+def _gemm_alone(peak: float):
+    """The same kernel with the whole GPU (one trailing-update launch outside the look-ahead), from the
+    committed ncu capture (profiles/r02_gemm_full.json; ncu's own duration, so context, not the bench value)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    return {"achieved": d["achieved_tflops_3x"], "frac": round(d["achieved_tflops_3x"] / peak, 4), "sms": d["grid"],
+            "tc_pipe_active_pct": d.get("sm__pipe_tc_cycles_active_pct"),
+            "launch": "M=N=%d K=%d, %.0f us (%s)" % (d["M"], d["K"], d["duration_us"], os.path.basename(p))}
+
+
 def dtype_label(variant: str) -> str:
     """The arithmetic the path computes in: binary32 LU (its O(n^3) update on 3xTF32 tcgen05 tensor
     cores, or FP32 FFMA), binary64 residual / update / test."""
@@ -724,6 +738,9 @@ def main():
                 # panel keeps the rest): the same peak scaled to that partition
                 "sms": sms_upd, "sms_total": 148,
                 "frac_of_partition": round(ach / (peak * sms_upd / 148.0), 4)}
+        alone = _gemm_alone(peak) if args.variant == "3xtf32" else None
+        if alone:
+            roof["alone_full_gpu"] = alone
     if "residual" in kern and kern["residual"]["ms"] > 0:
         d = kern["residual"]
         ach = d["work"] / (d["ms"] / 1e3) / 1e9
