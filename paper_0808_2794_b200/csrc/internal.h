@@ -253,8 +253,10 @@ size_t solve_flag_words(int64_t n);
 // ownership and the inverted diagonal blocks (inv required); flags: the 4 nblk words of
 // SolveScratch, epoch: its counter.  launch_lu_solve takes this path when mr_solve_supported().
 bool mr_solve_supported(int64_t n, int64_t nrhs);
+// tags / tag_cols: SolveScratch's tagged words (nullptr: flag hand-off)
 void launch_lu_solve_mr(const float *W, int64_t ldw, int64_t n, int64_t nrhs, float *Y, double *X, int accumulate,
-                        unsigned *flags, unsigned &epoch, const float *inv, cudaStream_t s);
+                        unsigned *flags, unsigned &epoch, const float *inv, cudaStream_t s, uint64_t *tags = nullptr,
+                        int tag_cols = 0);
 size_t solve_inv_floats(int64_t n);      // [D_L | M_L | D_U | M_U], each ceil(n/64) 64x64 blocks
 void launch_solve_inverses(const float *W, int64_t ldw, int64_t n, float *inv, cudaStream_t s);
 // max over the diagonal blocks of kappa_inf (L and U) computed by launch_solve_inverses (synchronises s)

@@ -1220,7 +1220,7 @@ void launch_lu_solve(const T *W, int64_t ldw, int64_t n, int64_t nrhs, T *Y, dou
     if constexpr (sizeof(T) == 4) {
         if (inv != nullptr && nrhs >= 2 && mr_solve_supported(n, nrhs)) {
             launch_lu_solve_mr(reinterpret_cast<const float *>(W), ldw, n, nrhs, reinterpret_cast<float *>(Y), X,
-                               accumulate, ss.flags, ss.epoch, inv, s);
+                               accumulate, ss.flags, ss.epoch, inv, s, ss.tags, ss.tag_cols);
             return;
         }
     }

@@ -45,6 +45,11 @@ struct MrArgs {
     int nrhs, accumulate;
     unsigned *flag;               // [nblk]
     unsigned epoch;
+    // tagged exchange (nullptr: flags): Y of each solved block also written as 64-bit words {value
+    // bits, tag} [nrhs][n]; a consumer that sees the tag sees the value (single-copy atomic 64-bit
+    // access), so the hand-off needs no fence and no flag
+    uint64_t *tY;
+    unsigned tag;
 };
 
 __device__ __forceinline__ void cp16(float *dst, const float *src, bool ok)
@@ -68,6 +73,17 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p)
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ unsigned long long ld_tag(const uint64_t *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_tag(uint64_t *p, float v, unsigned tag)
+{
+    const unsigned long long w = ((unsigned long long)tag << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
 }
 __device__ __forceinline__ void st_release(unsigned *p, unsigned v)
 {
@@ -197,12 +213,14 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
             if (c < a.nrhs && i0 + r < n) {
                 const float v = Yo[r * R + c];
                 a.Y[(int64_t)c * n + i0 + r] = v;
+                if (a.tY != nullptr) st_tag(a.tY + (int64_t)c * n + i0 + r, v, a.tag);
                 if (!LOWER) {
                     double *xp = a.X + (int64_t)c * n + i0 + r;
                     *xp = a.accumulate ? *xp + (double)v : (double)v;
                 }
             }
         }
+        if (a.tY != nullptr) return;                          // (tagged: the words are the hand-off)
         __syncthreads();
         if (threadIdx.x == 0) {
             __threadfence();
@@ -236,15 +254,40 @@ __global__ void __launch_bounds__(MNT, 1) mr_sweep_kernel(const MrArgs a)
         const int k0 = first_after(t);
         if (k0 >= nown) break;                               // every owned block is solved
         if (!have) {
-            if (threadIdx.x == 0) {
-                while (ld_relaxed(a.flag + I) != a.epoch) { }   // poll without invalidating L1 each time
-                (void)ld_acquire(a.flag + I);                      // then one acquire (orders the Y reads)
-            }
-            __syncthreads();
             const int64_t i0 = (int64_t)I * MB;
-            for (int e = threadIdx.x; e < MB * R; e += MNT) {
-                const int c = e / MB, rr = e - c * MB;
-                Yb(yb)[rr * R + c] = (c < a.nrhs && i0 + rr < n) ? __ldcg(a.Y + (int64_t)c * n + i0 + rr) : 0.f;
+            if (a.tY != nullptr) {
+                // poll the block's tagged words directly: one round trip brings the values with their tags
+                constexpr int PE = MB * R / MNT;
+                float v[PE];
+                for (;;) {
+                    bool ok = true;
+#pragma unroll
+                    for (int u = 0; u < PE; ++u) {
+                        const int e = threadIdx.x + MNT * u, c = e / MB, rr = e - c * MB;
+                        v[u] = 0.f;
+                        if (c < a.nrhs && i0 + rr < n) {
+                            const unsigned long long w = ld_tag(a.tY + (int64_t)c * n + i0 + rr);
+                            v[u] = __uint_as_float((unsigned)w);
+                            ok &= (unsigned)(w >> 32) == a.tag;
+                        }
+                    }
+                    if (__syncthreads_and(ok)) break;
+                }
+#pragma unroll
+                for (int u = 0; u < PE; ++u) {
+                    const int e = threadIdx.x + MNT * u, c = e / MB, rr = e - c * MB;
+                    Yb(yb)[rr * R + c] = v[u];
+                }
+            } else {
+                if (threadIdx.x == 0) {
+                    while (ld_relaxed(a.flag + I) != a.epoch) { }   // poll without invalidating L1 each time
+                    (void)ld_acquire(a.flag + I);                      // then one acquire (orders the Y reads)
+                }
+                __syncthreads();
+                for (int e = threadIdx.x; e < MB * R; e += MNT) {
+                    const int c = e / MB, rr = e - c * MB;
+                    Yb(yb)[rr * R + c] = (c < a.nrhs && i0 + rr < n) ? __ldcg(a.Y + (int64_t)c * n + i0 + rr) : 0.f;
+                }
             }
         }
         __syncthreads();
@@ -320,8 +363,9 @@ bool mr_solve_supported(int64_t n, int64_t nrhs)
 
 // Forward (unit lower, D_L) then backward (upper, D_U) sweeps for up to 16 right-hand sides.
 void launch_lu_solve_mr(const float *W, int64_t ldw, int64_t n, int64_t nrhs, float *Y, double *X, int accumulate,
-                        unsigned *flags, unsigned &epoch, const float *inv, cudaStream_t s)
+                        unsigned *flags, unsigned &epoch, const float *inv, cudaStream_t s, uint64_t *tags, int tag_cols)
 {
+    static const bool tags_off = std::getenv("MP_SOLVE_FLAGS") != nullptr;   // A/B: flag exchange
     const int nblk = (int)ceil_div(n, (int64_t)MB);
     const size_t blk = (size_t)nblk * MB * MB;
     int dev = 0, sms = 0;
@@ -330,7 +374,11 @@ void launch_lu_solve_mr(const float *W, int64_t ldw, int64_t n, int64_t nrhs, fl
     const int grid = std::min(sms, nblk);
     for (int64_t c0 = 0; c0 < nrhs; c0 += 16) {
         const int nc = (int)std::min<int64_t>(16, nrhs - c0);
-        MrArgs a{W, ldw, n, nblk, inv, inv + blk, Y + c0 * n, X + c0 * n, nc, accumulate, flags, ++epoch};
+        MrArgs a{W, ldw, n, nblk, inv, inv + blk, Y + c0 * n, X + c0 * n, nc, accumulate, flags, ++epoch, nullptr, 0u};
+        if (tags != nullptr && nc <= tag_cols && !tags_off) {
+            a.tY = tags;
+            a.tag = 2u * a.epoch;
+        }
         auto go = [&](auto lower) {
             constexpr bool L = decltype(lower)::value;
             if (nc <= 4) launch_mr<L, 4>(a, grid, s);
@@ -342,6 +390,7 @@ void launch_lu_solve_mr(const float *W, int64_t ldw, int64_t n, int64_t nrhs, fl
         a.M = inv + 3 * blk;
         a.flag = flags + 2 * nblk;
         a.epoch = ++epoch;
+        if (a.tY != nullptr) a.tag = 2u * a.epoch + 1u;
         go(std::false_type{});
         g_launches += 2;
     }
