@@ -24,7 +24,7 @@ constexpr int LT = 256;
 template <typename T, int SW>
 __global__ void __launch_bounds__(LT)
 laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ pairs,
-                   const int32_t *__restrict__ npairs, int64_t c_lo, int64_t c_hi, int64_t x_lo,
+                   const int32_t *__restrict__ npairs, int max_pairs, int64_t c_lo, int64_t c_hi, int64_t x_lo,
                    int64_t x_hi, int32_t *__restrict__ perm, int nstrips, EmitJob ej)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -59,16 +59,19 @@ laswp_pairs_kernel(T *__restrict__ W, int64_t ldw, const int32_t *__restrict__ p
     const int cl = lane % SW, rs = lane / SW;
     const int64_t col = s0 + cl;
     const bool valid = col < c_hi && !(col >= x_lo && col < x_hi);
-    // U row groups per warp per round: all pair indices, then all row loads, in flight together
+    // U row groups per warp per round: all pair indices, then all row loads, in flight together.
+    // The pair entries below max_pairs (the list's capacity) are read without waiting for the count
+    // (one dependent round trip fewer; entries at or beyond the count are masked afterwards).
     constexpr int U = 8, NW = LT / 32, STEP = NW * RPW;
-    for (int i0 = warp * RPW + rs; i0 < np; i0 += STEP * U) {
+    for (int i0 = warp * RPW + rs; i0 < max_pairs; i0 += STEP * U) {
         int32_t src[U];
         T v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + STEP * u;
-            src[u] = i < np ? pairs[2 * i + 1] : 0;
+            src[u] = i < max_pairs ? pairs[2 * i + 1] : 0;
         }
+        if (i0 >= np) break;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = i0 + STEP * u;
@@ -129,8 +132,8 @@ void launch_laswp_pairs(T *W, int64_t ldw, const int32_t *pairs, const int32_t *
     const size_t smem = std::max<size_t>((size_t)max_pairs * sw * sizeof(T), (size_t)max_pairs * 4);
     auto kern = narrow ? laswp_pairs_kernel<T, 8> : laswp_pairs_kernel<T, 32>;
     if (smem > 48 * 1024) func_smem_once((const void *)kern, smem);
-    launch_ex(kern, dim3(grid), dim3(LT), smem, s, nullptr, W, ldw, pairs, npairs, c_lo, c_hi, x_lo, x_hi, perm,
-              nstrips, ej);
+    launch_ex(kern, dim3(grid), dim3(LT), smem, s, nullptr, W, ldw, pairs, npairs, max_pairs, c_lo, c_hi, x_lo, x_hi,
+              perm, nstrips, ej);
 }
 
 void launch_init_perm(int32_t *perm, int64_t n, cudaStream_t s)
