@@ -608,11 +608,80 @@ struct Factor {
     // panels [0, c_lo): U12 and the Schur update of every earlier step, in order (the right-looking
     // updates it missed while it was in flight; the later interchanges commute).
     float *tfC = nullptr;                  // the catch-up's own 3xTF32 scratch (it may run beside the look-ahead)
+    void catch_up_panel(int64_t k, int64_t c_lo, int64_t c_hi, cudaStream_t q, int nsm) {
+        const int w = (int)std::min<int64_t>(nb, c_lo - k);
+        trsm(q, k, w, c_lo, c_hi);
+        gemm(q, k + w, c_lo, k, n - k - w, c_hi - c_lo, w, true, KC_TRAIL, tfC ? tfC : tf32[0], nsm);
+    }
     void catch_up(int64_t c_lo, int64_t c_hi, cudaStream_t q, int nsm) {
-        for (int64_t k = 0; k < c_lo; k += nb) {
-            const int w = (int)std::min<int64_t>(nb, c_lo - k);
-            trsm(q, k, w, c_lo, c_hi);
-            gemm(q, k + w, c_lo, k, n - k - w, c_hi - c_lo, w, true, KC_TRAIL, tfC ? tfC : tf32[0], nsm);
+        for (int64_t k = 0; k < c_lo; k += nb) catch_up_panel(k, c_lo, c_hi, q, nsm);
+    }
+    // Streamed look-ahead: the column blocks of A join ONE look-ahead loop while it runs.
+    // Block j joins at step join_at (on the update stream, after that step's interchanges: demote,
+    // rows gathered into the current order, so from then on every panel's interchanges reach it), is
+    // caught up panel by panel (U12 and Schur update of each earlier panel, in order, a share per step
+    // so the work hides behind the panel chain like the ordinary trailing update), and receives the
+    // ordinary per-step updates once caught up (nc_upd).  It must be caught up before the step whose
+    // next-panel update reaches its first panel (need_at = c_lo - 2 nb).  Per entry: the same
+    // operations in the same order as the one-shot factorisation (the interchanges commute, §9b).
+    struct StreamBlock {
+        int64_t c_lo, c_hi;
+        cudaEvent_t ev;
+        int64_t join_at, need_at;
+        int64_t cu = 0;                    // caught up on the panels [0, cu)
+        bool joined = false, regular = false;
+    };
+    struct Streamer {
+        std::vector<StreamBlock> blk;
+        const double *dA = nullptr;        // device A (column-major, ld n), filled block by block
+        float *S = nullptr;                // binary32 staging of one block (row-major, ld lds)
+        double *dpart = nullptr, *anrm_parts = nullptr;
+        unsigned *dcnt = nullptr;
+        int64_t nc_swap = 0, nc_upd = 0;   // columns reached by the interchanges / by the per-step update
+        size_t next_join = 1;
+        int ahead = 3;                     // look-ahead steps the host may enqueue beyond the device
+    };
+    Streamer *str = nullptr;
+    void stream_join(StreamBlock &B, size_t j, cudaStream_t q) {
+        const int64_t wcols = B.c_hi - B.c_lo, lds = round_up(wcols, 64);
+        MP_CUDA(cudaStreamWaitEvent(q, B.ev, 0));
+        if constexpr (sizeof(T) == 4) {          // (the streamed path is the binary32 factorisation's)
+            prof_begin(KC_DEMOTE, q);
+            launch_demote_rect<float>(str->dA + B.c_lo * n, n, n, wcols, str->S, lds, str->dpart, str->dcnt, st, q);
+            MP_CUDA(cudaMemcpyAsync(str->anrm_parts + j, &st->anrm2, sizeof(double), cudaMemcpyDeviceToDevice, q));
+            launch_gather_rows(str->S, lds, round_up(wcols, 4), perm, n, W + B.c_lo, ldw, q);
+            prof_end(KC_DEMOTE, 12.0 * n * wcols, q);
+        }
+        B.joined = true;
+        str->nc_swap = B.c_hi;
+    }
+    // step k's share of the streamed work (update stream q, after the step's interchanges)
+    void stream_step(int64_t k, cudaStream_t q, int nsm) {
+        Streamer &z = *str;
+        // a block joins once its copy has landed (host-side query: the host runs at most a few steps
+        // ahead of the device, see run_lookahead), at the latest at need_at (the update stream then
+        // waits for the copy)
+        while (z.next_join < z.blk.size() &&
+               (z.blk[z.next_join].need_at <= k ||
+                (z.blk[z.next_join].join_at <= k && cudaEventQuery(z.blk[z.next_join].ev) == cudaSuccess))) {
+            stream_join(z.blk[z.next_join], z.next_join, q);
+            ++z.next_join;
+        }
+        for (size_t j = 1; j < z.blk.size(); ++j) {
+            StreamBlock &B = z.blk[j];
+            if (B.regular) continue;
+            if (!B.joined) break;
+            // spread the remaining catch-up panels evenly over the steps left before need_at
+            const int64_t left = (k - B.cu + nb - 1) / nb;
+            const int64_t steps = std::max<int64_t>(1, (B.need_at - k) / nb + 1);
+            int64_t todo = k >= B.need_at ? left : (left + steps - 1) / steps;
+            while (B.cu < k && todo-- > 0) {
+                catch_up_panel(B.cu, B.c_lo, B.c_hi, q, nsm);
+                B.cu += nb;
+            }
+            if (B.cu < k) break;           // later blocks wait (updates stay contiguous)
+            B.regular = true;              // caught up on [0, k): step k's own update is the ordinary one
+            z.nc_upd = B.c_hi;
         }
     }
     // Look-ahead (depth 1).  Step k:
@@ -649,6 +718,10 @@ struct Factor {
         split_ok[0] = split_l21(kb, (int)std::min<int64_t>(nb, ke - kb), 0);
         int idx = 0;
         for (int64_t k = kb; k < ke; k += nb, ++idx) {
+            if (str && idx >= str->ahead) {   // streamed: the host enqueues at most `ahead` steps ahead
+                const cudaError_t e = cudaEventSynchronize(la_event(70 + (idx - str->ahead) % 8));
+                if (e != cudaSuccess) MP_CUDA(e);
+            }
             const int w = (int)std::min<int64_t>(nb, ke - k);
             const int64_t kn = k + w;
             const int wn = kn < ke ? (int)std::min<int64_t>(nb, ke - kn) : 0;
@@ -688,21 +761,26 @@ struct Factor {
                 split_ok[b ^ 1] = split_l21(kn, wn, b ^ 1);
             }
             // ... then every other column (left factors, rest of the trailing matrix), off it
+            // (streamed: the columns that have joined so far; their catch-up share of this step)
+            const int64_t ncs = str ? str->nc_swap : nc;
             prof_begin(KC_LASWP, sU);
-            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, nc, k, kn + wn, perm, sU);
-            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(nc - w - wn) * sizeof(T), sU);
-            if (kn < nc && kn + wn < nc) {
+            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, ncs, k, kn + wn, perm, sU);
+            prof_end(KC_LASWP, 2.0 * 2 * w * (double)(ncs - w - wn) * sizeof(T), sU);
+            if (str) stream_step(k, sU, smsu);
+            const int64_t ncu = str ? str->nc_upd : nc;
+            if (kn < ncu && kn + wn < ncu) {
                 const int kp = (int)round_up(w, 4);
-                const int64_t nr = nc - kn - wn;
+                const int64_t nr = ncu - kn - wn;
                 const bool bsplit = split_ok[b] && nr >= 128 && w <= 256;
                 float *bh = bsplit ? tfU[b] + 2 * (size_t)(n - kn) * kp : nullptr;
-                trsm(sU, k, w, kn + wn, nc, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
+                trsm(sU, k, w, kn + wn, ncu, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
                 const bool reuse = split_ok[b] || (kn < n && n - kn >= 256 && wn >= 128);
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
-                gemm(sU, kn, kn + wn, k, n - kn, nc - kn - wn, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
+                gemm(sU, kn, kn + wn, k, n - kn, nr, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
                      reuse, terms, bsplit);
             }
+            if (str) MP_CUDA(cudaEventRecord(la_event(70 + idx % 8), sU));
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
         MP_CUDA(cudaEventRecord(eEndU, cur));
@@ -771,36 +849,121 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
 // (perm) and brought up to date with the panels [0, c_lo) (catch_up), then its own panels are
 // factored with every update restricted to the columns that have arrived.  Same operations per
 // entry as the one-shot factorisation, reordered (the exact-LU family stays bitwise).
-void run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n, float *W, int64_t ldw, int nb,
-                         int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool, cudaStream_t s, int variant,
-                         bool lookahead, int nblocks, double *anrm_parts, cudaStream_t cs)
+// Column-block plan of the streamed path, in panels: with the look-ahead (one loop, blocks joining
+// it), blocks of ~nbk/8 panels (at least 3), the last ones halving down to one panel, so that little
+// work is left once the last bytes land; without it (blocks factored one after the other) nblocks
+// equal blocks.  MP_STREAM_PLAN="w0,w1,..." (panels) overrides the look-ahead plan.
+std::vector<int64_t> stream_plan(int64_t nbk, bool joined, int nblocks)
+{
+    std::vector<int64_t> p;
+    if (!joined) {
+        const int64_t per = ceil_div(nbk, (int64_t)nblocks);
+        for (int64_t r = nbk; r > 0; r -= per) p.push_back(std::min(per, r));
+        return p;
+    }
+    if (const char *e = std::getenv("MP_STREAM_PLAN")) {
+        int64_t r = nbk;
+        for (const char *c = e; *c && r > 0;) {
+            const int64_t v = std::max<int64_t>(1, std::atoll(c));
+            p.push_back(std::min(v, r));
+            r -= p.back();
+            while (*c && *c != ',') ++c;
+            if (*c == ',') ++c;
+        }
+        if (r > 0) p.push_back(r);
+        if (p[0] < 2 && p.size() > 1) { p[0] += p[1]; p.erase(p.begin() + 1); }
+        return p;
+    }
+    const int64_t B = std::max<int64_t>(3, ceil_div(nbk, (int64_t)8));
+    int64_t r = nbk;
+    while (r > B) { p.push_back(B); r -= B; }
+    while (r > 1) { const int64_t h = ceil_div(r, (int64_t)2); p.push_back(h); r -= h; }
+    if (r > 0) p.push_back(r);
+    if (p[0] < 2 && p.size() > 1) { p[0] += p[1]; p.erase(p.begin() + 1); }
+    return p;
+}
+
+// returns the number of column blocks (anrm_parts[0 .. blocks) hold their ||A||_F^2 shares)
+int run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n, float *W, int64_t ldw, int nb,
+                        int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool, cudaStream_t s, int variant,
+                        bool lookahead, int nblocks, double *anrm_parts, cudaStream_t cs)
 {
     Factor<float> f;
     make_factor<float>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant);
     if (tc_variant(variant)) f.tfC = pool.get<float>(tf32_scratch_floats(n, nb));
     const int64_t nbk = ceil_div(n, (int64_t)nb);
-    const int64_t per = ceil_div(nbk, (int64_t)nblocks) * nb;                 // block width (multiple of nb)
+    // MP_STREAM_JOINED=1: one look-ahead loop the blocks join (measured slower at C3: 66.6-70 vs 64.2 ms,
+    // DESIGN §9b); default: the blocks factored one after another, each caught up at full width
+    static const bool joined_env = [] { const char *e = std::getenv("MP_STREAM_JOINED"); return e && e[0] == '1'; }();
+    const bool joined = lookahead && joined_env && nbk > 4 && exec_res().ok;
+    std::vector<int64_t> plan = stream_plan(nbk, joined, nblocks);
+    if (plan.size() > 40) throw std::runtime_error("streamed path: more than 40 column blocks");
+    int64_t per = 0;
+    for (int64_t b : plan) per = std::max(per, b * nb);
     float *S = pool.get<float>((size_t)n * round_up(per, 64));
     double *dpart = pool.get<double>((size_t)num_sms() * 8);
     unsigned *dcnt = pool.get<unsigned>(1);
     MP_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(unsigned), s));
     std::vector<cudaEvent_t> ev;
+    std::vector<std::pair<int64_t, int64_t>> cols;
     {   // dA was allocated stream-ordered on s: the copy stream starts after that point of s
         cudaEvent_t e0 = la_event(19);
         MP_CUDA(cudaEventRecord(e0, s));
         MP_CUDA(cudaStreamWaitEvent(cs, e0, 0));
     }
-    for (int64_t c_lo = 0, j = 0; c_lo < n; c_lo += per, ++j) {
-        const int64_t c_hi = std::min(n, c_lo + per);
+    // copy-engine DMA (one linear transfer per block when A's columns are contiguous); MP_H2D_SM=1: SM
+    // loads of the pinned block with evict-first stores (k_h2d.cu; measured slower: 75 vs 64.2 ms)
+    static const bool dma_env = [] { const char *e = std::getenv("MP_H2D_SM"); return !(e && e[0] == '1'); }();
+    static const int h2d_ctas = [] { const char *e = std::getenv("MP_H2D_CTAS"); return e ? std::max(1, std::atoi(e)) : 8; }();
+    const double *hA_dev = dma_env ? nullptr : h2d_device_view(hA);
+    for (int64_t c_lo = 0, j = 0; c_lo < n; ++j) {
+        const int64_t c_hi = std::min(n, c_lo + plan[j] * nb);
         cudaEvent_t e = la_event(20 + (int)j);
-        MP_CUDA(cudaMemcpy2DAsync(dA + c_lo * n, n * sizeof(double), hA + c_lo * lda_h, lda_h * sizeof(double),
-                                  n * sizeof(double), c_hi - c_lo, cudaMemcpyHostToDevice, cs));
+        if (hA_dev && launch_h2d_cols(hA_dev + c_lo * lda_h, lda_h, dA + c_lo * n, n, c_hi - c_lo, h2d_ctas, cs)) {
+        } else if (lda_h == n) {           // contiguous columns: one linear copy-engine transfer
+            MP_CUDA(cudaMemcpyAsync(dA + c_lo * n, hA + c_lo * lda_h, (size_t)(c_hi - c_lo) * n * sizeof(double),
+                                    cudaMemcpyHostToDevice, cs));
+        } else
+            MP_CUDA(cudaMemcpy2DAsync(dA + c_lo * n, n * sizeof(double), hA + c_lo * lda_h, lda_h * sizeof(double),
+                                      n * sizeof(double), c_hi - c_lo, cudaMemcpyHostToDevice, cs));
         MP_CUDA(cudaEventRecord(e, cs));
         ev.push_back(e);
+        cols.emplace_back(c_lo, c_hi);
+        c_lo = c_hi;
+    }
+    if (joined) {
+        // block 0 demoted straight into W (rows in their original order); the others join the loop
+        const int64_t c_hi0 = cols[0].second;
+        MP_CUDA(cudaStreamWaitEvent(s, ev[0], 0));
+        prof_begin(KC_DEMOTE, s);
+        launch_demote_rect<float>(dA, n, n, c_hi0, W, ldw, dpart, dcnt, st, s);
+        prof_end(KC_DEMOTE, 12.0 * n * c_hi0, s);
+        MP_CUDA(cudaMemcpyAsync(anrm_parts, &st->anrm2, sizeof(double), cudaMemcpyDeviceToDevice, s));
+        static const int64_t dist = [] { const char *e = std::getenv("MP_STREAM_JOIN"); return e ? std::atoll(e) : 64; }();
+        static const int ahead = [] { const char *e = std::getenv("MP_STREAM_AHEAD"); return e ? std::max(1, std::atoi(e)) : 3; }();
+        Factor<float>::Streamer z;
+        z.dA = dA; z.S = S; z.dpart = dpart; z.anrm_parts = anrm_parts; z.dcnt = dcnt;
+        z.nc_swap = z.nc_upd = c_hi0;
+        z.ahead = ahead;
+        for (size_t j = 0; j < cols.size(); ++j) {
+            Factor<float>::StreamBlock B;
+            B.c_lo = cols[j].first; B.c_hi = cols[j].second; B.ev = ev[j];
+            B.need_at = B.c_lo - 2 * nb;
+            B.join_at = std::max<int64_t>(0, std::min(B.need_at, B.c_lo - dist * nb));
+            B.joined = B.regular = j == 0;
+            z.blk.push_back(B);
+        }
+        f.str = &z;
+        f.kb = 0; f.ke = n; f.nc = n;
+        f.run(true);
+        f.str = nullptr;
+        for (const auto &B : z.blk)
+            if (!B.regular) throw std::runtime_error("streamed path: a column block was never caught up");
+        return (int)cols.size();
     }
     const int sms = num_sms();
-    for (int64_t c_lo = 0, j = 0; c_lo < n; c_lo += per, ++j) {
-        const int64_t c_hi = std::min(n, c_lo + per), wcols = c_hi - c_lo;
+    for (int64_t j = 0; j < (int64_t)cols.size(); ++j) {
+        const int64_t c_lo = cols[j].first, c_hi = cols[j].second, wcols = c_hi - c_lo;
         MP_CUDA(cudaStreamWaitEvent(s, ev[j], 0));
         prof_begin(KC_DEMOTE, s);
         if (c_lo == 0) {
@@ -816,6 +979,7 @@ void run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n,
         f.kb = c_lo; f.ke = c_hi; f.nc = c_hi;
         f.run(lookahead);
     }
+    return (int)cols.size();
 }
 
 struct Args {
@@ -1069,15 +1233,15 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         launch_init_perm(ident, n, s);
         launch_permute_demote_rhs<float>(v.B, n, nrhs, ident, Y, sio.d, s);
         static const int kBlocks = [] { const char *e = std::getenv("MP_STREAM_BLOCKS"); return e ? std::max(1, std::min(16, std::atoi(e))) : 4; }();
-        double *parts = pool.get<double>(17);
-        run_factor_streamed(a.A, a.lda, const_cast<double *>(v.A), n, W, ldw, nb, ipiv, perm, sio.d, pool, s,
-                            o.variant, (o.flags & 16) == 0, kBlocks, parts, copy_stream());
-        double hp[17] = {0};
+        double *parts = pool.get<double>(40);
+        const int nparts = run_factor_streamed(a.A, a.lda, const_cast<double *>(v.A), n, W, ldw, nb, ipiv, perm,
+                                               sio.d, pool, s, o.variant, (o.flags & 16) == 0, kBlocks, parts,
+                                               copy_stream());
+        double hp[40] = {0};
         MP_CUDA(cudaMemcpyAsync(hp, parts, sizeof(hp), cudaMemcpyDeviceToHost, s));
         MP_CUDA(cudaStreamSynchronize(s));
         anrm2_streamed = 0.0;
-        for (int j = 0; j < (int)ceil_div(ceil_div(n, (int64_t)nb), (int64_t)ceil_div(ceil_div(n, (int64_t)nb), kBlocks)); ++j)
-            anrm2_streamed += hp[j];
+        for (int j = 0; j < nparts; ++j) anrm2_streamed += hp[j];
     } else {
         prof_begin(KC_DEMOTE, s);
         launch_demote_transpose<float>(v.A, v.lda, n, W, ldw, dpart, dcnt, sio.d, s);

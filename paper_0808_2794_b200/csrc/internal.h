@@ -124,6 +124,13 @@ template <typename T>
 void launch_demote_rect(const double *A, int64_t lda, int64_t n, int64_t ncols, T *W, int64_t ldw,
                         double *partials, unsigned *counter, DevStatus *st, cudaStream_t s);
 
+// Streamed e2e path (k_h2d.cu): device view of a pinned host pointer (nullptr if not device-accessible);
+// copy ncols columns (host ld lda_h) into dA (ld n) with nctas CTAs of SM loads over PCIe and
+// L2 evict-first stores.  Returns false (nothing launched) when n / alignment do not allow it.
+const double *h2d_device_view(const double *hA);
+bool launch_h2d_cols(const double *hA_dev, int64_t lda_h, double *dA, int64_t n, int64_t ncols, int nctas,
+                     cudaStream_t s);
+
 // W[i][c] = S[perm[i]][c] (i < n, c < ncols; S row-major with ld lds; 16-byte aligned rows)
 void launch_gather_rows(const float *S, int64_t lds, int64_t ncols, const int32_t *perm, int64_t n, float *W,
                         int64_t ldw, cudaStream_t s);

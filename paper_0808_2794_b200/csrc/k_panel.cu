@@ -401,6 +401,9 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
     static_assert(sizeof(SlotT) % 16 == 0, "slot must be 16-byte chunks");
     constexpr int CH = (int)(sizeof(SlotT) / 16);
     constexpr int EPC = 16 / (int)sizeof(T);     // elements per 16-byte chunk
+    // the staged candidate row keeps its dead slots; the leader zeroes them chunk by chunk while
+    // pushing (live is a multiple of UG): one select per chunk instead of one per element per warp
+    constexpr bool kLeadZero = MULTI && (UG % EPC == 0);
     pdl_wait();
     pdl_trigger();
     cg::cluster_group cluster = cg::this_cluster();
@@ -516,7 +519,8 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                                     uint4 v;
                                     T *pv = reinterpret_cast<T *>(&v);
 #pragma unroll
-                                    for (int e = 0; e < EPC; ++e) pv[e] = s + e < live ? x[q][s + e] : T(0);
+                                    for (int e = 0; e < EPC; ++e)
+                                        pv[e] = (kLeadZero || s + e < live) ? x[q][s + e] : T(0);
                                     *reinterpret_cast<uint4 *>(&wstage[par][warp].row[s]) = v;
                                 }
                             }
@@ -561,7 +565,11 @@ __global__ void __launch_bounds__(NT, 1) panel_leaf_kernel(LeafArgs<T> a)
                         uint4 pv[PJ];
 #pragma unroll
                         for (int j = 0; j < PJ; ++j)
-                            if (pch[j] >= 0) pv[j] = s4[pch[j]];
+                            if (pch[j] >= 0) {
+                                pv[j] = s4[pch[j]];
+                                // dead slots (multipliers) go out as zeros: whole 16-byte chunks
+                                if (kLeadZero && pch[j] >= 1 && (pch[j] - 1) * EPC >= live) pv[j] = make_uint4(0u, 0u, 0u, 0u);
+                            }
 #pragma unroll
                         for (int j = 0; j < PJ; ++j)
                             if (pch[j] >= 0) st_async16(pdst[par][j], pv[j], pbar[par][j]);

@@ -288,3 +288,37 @@ def test_streamed_host_path_exact_and_criterion(mp, orc):
     assert infoh == infod == 0 and abs(ith - ro.iters) <= 1
     assert certificate(A2, Xh2, B2) < 1.05
     assert abs(reph.anrm - ro.anrm) <= 1e-12 * ro.anrm
+
+
+_STREAM_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_0808_2794_b200 import binding as mp, inputs
+n = int(sys.argv[2])
+A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n)
+Xh, it, info, _ = mp.mp_dsgesv_ex(A, B)
+ok = int(it == 0 and info == 0 and np.array_equal(Xh, X))
+A2, B2, _ = inputs.gaussian(n, nrhs=2, seed=77)
+Xh2, ith, infoh, _ = mp.mp_dsgesv_ex(A2, B2)
+Xd2, itd, infod, _ = mp.mp_dsgesv_ex(mp.colmajor_cuda(A2), mp.colmajor_cuda(B2))
+torch.cuda.synchronize()
+same = int(infoh == infod == 0 and ith == itd and np.array_equal(Xh2, Xd2.cpu().numpy()))
+print(ok, same)
+"""
+
+
+@pytest.mark.parametrize("env", [{"MP_STREAM_JOINED": "1"}, {"MP_STREAM_JOINED": "1", "MP_STREAM_PLAN": "2,3,1,4,2,1"},
+                                 {"MP_H2D_SM": "1"}])
+def test_streamed_host_path_options(env):
+    """The streamed e2e path's experimental options (read once per process: run in a child): blocks
+    joining one look-ahead loop (interchanges reach a block from its join on, catch-up spread over the
+    steps) and the SM-load copy of the host blocks.  Exact-LU stays bitwise and the Gaussian solve
+    equals the device-resident path bitwise (the same operations per entry)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _STREAM_CHILD, root, "4608"], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    ok, same = map(int, r.stdout.split()[-2:])
+    assert ok == 1 and same == 1
