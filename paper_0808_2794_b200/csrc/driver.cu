@@ -282,6 +282,8 @@ struct ExecRes {
     bool ok = false;
     cudaStream_t sP = nullptr, sU = nullptr;
     int smsP = 0, smsU = 0;
+    // a second stream on the update partition (the streamed e2e path's concurrent catch-up)
+    cudaStream_t sC = nullptr;
     // a second, larger update partition for the early steps (the trailing update is then the
     // critical path); sU2 == nullptr: not available
     cudaStream_t sU2 = nullptr;
@@ -333,6 +335,11 @@ ExecRes make_exec_res(int dev)
     if (mkCtx(&gP, dP, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
     if (mkCtx(&gU, dU, (CUdevice)dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return r;
     if (mkStream(&sU, gU, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return r;
+    {
+        CUstream sC;
+        if (mkStream(&sC, gU, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) r.sC = (cudaStream_t)sC;
+        cudaGetLastError();
+    }
     {
         unsigned psms2 = 32;                  // SMs kept free during the early steps (MP_PANEL_SMS_EARLY)
         if (const char *e = std::getenv("MP_PANEL_SMS_EARLY")) psms2 = (unsigned)std::max(16, std::atoi(e));
@@ -473,6 +480,10 @@ struct Factor {
     int32_t *ipiv, *perm;
     PanelScratch ps;
     int32_t *ppairs[2], *nppairs[2];   // panel-level pairs, double-buffered for the look-ahead
+    // streamed path: every panel's pairs kept (slot k / nb), and the interchanges of the steps applied
+    // to the columns [swap_lo, nc) only (the left factors get them later)
+    int32_t *pairs_all = nullptr, *npairs_all = nullptr;
+    int64_t swap_lo = 0;
     DevStatus *st;
     int nb;
     int variant = MP_VARIANT_FFMA;
@@ -567,6 +578,10 @@ struct Factor {
     // panels k in [kb, ke), interchanges / U12 / Schur updates on columns [0, nc); rows always [0, n)
     int64_t kb = 0, ke = -1, nc = -1;
     void factor_panel(cudaStream_t q, int64_t k, int w, int b) {
+        if (pairs_all) {
+            ppairs[b] = pairs_all + (k / nb) * 4 * (int64_t)nb;
+            nppairs[b] = npairs_all + k / nb;
+        }
         cur_np = nppairs[b];                 // the first leaf zeroes it and starts orig[] as the identity
         emit_job = EmitJob{ps.orig, k, n, ppairs[b], nppairs[b]};
         emitted = false;
@@ -596,7 +611,7 @@ struct Factor {
             factor_panel(s, k, w, 0);
             // the panel's interchanges on every other column (left factors + trailing matrix)
             prof_begin(KC_LASWP, s);
-            launch_laswp_pairs<T>(W, ldw, ppairs[0], nppairs[0], 2 * w, 0, nc, k, k + w, perm, s);
+            launch_laswp_pairs<T>(W, ldw, ppairs[0], nppairs[0], 2 * w, swap_lo, nc, k, k + w, perm, s);
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(nc - w) * sizeof(T), s);
             if (k + w < nc) {
                 trsm(s, k, w, k + w, nc);                                                  // U12 <- L11^-1 A12
@@ -764,7 +779,7 @@ struct Factor {
             // (streamed: the columns that have joined so far; their catch-up share of this step)
             const int64_t ncs = str ? str->nc_swap : nc;
             prof_begin(KC_LASWP, sU);
-            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, 0, ncs, k, kn + wn, perm, sU);
+            launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, swap_lo, ncs, k, kn + wn, perm, sU);
             prof_end(KC_LASWP, 2.0 * 2 * w * (double)(ncs - w - wn) * sizeof(T), sU);
             if (str) stream_step(k, sU, smsu);
             const int64_t ncu = str ? str->nc_upd : nc;
@@ -856,7 +871,7 @@ void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *pe
 std::vector<int64_t> stream_plan(int64_t nbk, bool joined, int nblocks)
 {
     std::vector<int64_t> p;
-    if (!joined) {
+    if (!joined && !std::getenv("MP_STREAM_PLAN")) {
         const int64_t per = ceil_div(nbk, (int64_t)nblocks);
         for (int64_t r = nbk; r > 0; r -= per) p.push_back(std::min(per, r));
         return p;
@@ -931,6 +946,11 @@ int run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n, 
         cols.emplace_back(c_lo, c_hi);
         c_lo = c_hi;
     }
+    // diagnostic (MP_STREAM_PRECOPY=1): every block lands before the factorisation starts (the same
+    // schedule with no copy in flight: per-launch timelines are distorted by a concurrent copy)
+    static const bool precopy = [] { const char *e = std::getenv("MP_STREAM_PRECOPY"); return e && e[0] == '1'; }();
+    if (precopy)
+        for (cudaEvent_t e : ev) MP_CUDA(cudaStreamWaitEvent(s, e, 0));
     if (joined) {
         // block 0 demoted straight into W (rows in their original order); the others join the loop
         const int64_t c_hi0 = cols[0].second;
@@ -962,6 +982,73 @@ int run_factor_streamed(const double *hA, int64_t lda_h, double *dA, int64_t n, 
         return (int)cols.size();
     }
     const int sms = num_sms();
+    // Overlapped blocks (default with the look-ahead): while block j is factored, block j+1 is demoted,
+    // put in the row order of block j's start and caught up with the panels before block j, on a second
+    // stream of the update partition.  Block j's interchanges are therefore kept off the columns left of
+    // it (its L columns stay as the concurrent catch-up reads them, swap_lo) and applied afterwards to
+    // those columns and to block j+1 at once; block j+1 then gets the catch-up of block j's panels
+    // only.  Per entry the same operations in the same order (the interchanges commute, §9b).
+    static const bool no_overlap = [] { const char *e = std::getenv("MP_STREAM_NO_OVERLAP"); return e && e[0] == '1'; }();
+    const ExecRes *exr = lookahead && !no_overlap && cols.size() > 1 ? &exec_res() : nullptr;
+    if (exr && exr->ok && exr->sC) {
+        cudaStream_t sC = exr->sC;
+        f.pairs_all = pool.get<int32_t>((size_t)nbk * 4 * nb);
+        f.npairs_all = pool.get<int32_t>((size_t)nbk);
+        int32_t *perm_snap = pool.get<int32_t>(n);
+        std::vector<cudaEvent_t> eC(cols.size(), nullptr);
+        for (size_t j = 0; j < cols.size(); ++j) {
+            const int64_t c_lo = cols[j].first, c_hi = cols[j].second;
+            if (j == 0) {
+                MP_CUDA(cudaStreamWaitEvent(s, ev[0], 0));
+                prof_begin(KC_DEMOTE, s);
+                launch_demote_rect<float>(dA, n, n, c_hi, W, ldw, dpart, dcnt, st, s);
+                prof_end(KC_DEMOTE, 12.0 * n * c_hi, s);
+                MP_CUDA(cudaMemcpyAsync(anrm_parts, &st->anrm2, sizeof(double), cudaMemcpyDeviceToDevice, s));
+            } else {
+                const int64_t p_lo = cols[j - 1].first, p_hi = cols[j - 1].second;
+                MP_CUDA(cudaStreamWaitEvent(s, eC[j], 0));
+                // block j-1's interchanges on the columns that have not seen them: the left factors and block j
+                for (int64_t k = p_lo; k < p_hi; k += nb) {
+                    const int w = (int)std::min<int64_t>(nb, p_hi - k);
+                    prof_begin(KC_LASWP, s);
+                    launch_laswp_pairs<float>(W, ldw, f.pairs_all + (k / nb) * 4 * (int64_t)nb, f.npairs_all + k / nb,
+                                              2 * w, 0, c_hi, p_lo, p_hi, nullptr, s);
+                    prof_end(KC_LASWP, 2.0 * 2 * w * (double)(c_hi - (p_hi - p_lo)) * sizeof(float), s);
+                }
+                for (int64_t k = p_lo; k < c_lo; k += nb) f.catch_up_panel(k, c_lo, c_hi, s, sms);
+            }
+            if (j + 1 < cols.size()) {
+                // block j+1 on the catch-up stream, in the row order of block j's start
+                const int64_t q_lo = cols[j + 1].first, q_hi = cols[j + 1].second, wq = q_hi - q_lo;
+                if (j == 0) launch_init_perm(perm_snap, n, s);
+                else MP_CUDA(cudaMemcpyAsync(perm_snap, perm, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+                cudaEvent_t eSnap = la_event(80 + (int)(j % 2));
+                MP_CUDA(cudaEventRecord(eSnap, s));
+                MP_CUDA(cudaStreamWaitEvent(sC, eSnap, 0));
+                MP_CUDA(cudaStreamWaitEvent(sC, ev[j + 1], 0));
+                const int64_t lds = round_up(wq, 64);
+                prof_begin(KC_DEMOTE, sC);
+                launch_demote_rect<float>(dA + q_lo * n, n, n, wq, S, lds, dpart, dcnt, st, sC);
+                MP_CUDA(cudaMemcpyAsync(anrm_parts + j + 1, &st->anrm2, sizeof(double), cudaMemcpyDeviceToDevice, sC));
+                launch_gather_rows(S, lds, round_up(wq, 4), perm_snap, n, W + q_lo, ldw, sC);
+                prof_end(KC_DEMOTE, 12.0 * n * wq, sC);
+                for (int64_t k = 0; k < c_lo; k += nb) f.catch_up_panel(k, q_lo, q_hi, sC, exr->smsU);
+                eC[j + 1] = la_event(82 + (int)j);
+                MP_CUDA(cudaEventRecord(eC[j + 1], sC));
+            }
+            f.swap_lo = c_lo; f.kb = c_lo; f.ke = c_hi; f.nc = c_hi;
+            f.run(true);
+        }
+        // the last block's interchanges on the left factors
+        const int64_t p_lo = cols.back().first, p_hi = cols.back().second;
+        for (int64_t k = p_lo; k < p_hi && p_lo > 0; k += nb) {
+            const int w = (int)std::min<int64_t>(nb, p_hi - k);
+            launch_laswp_pairs<float>(W, ldw, f.pairs_all + (k / nb) * 4 * (int64_t)nb, f.npairs_all + k / nb, 2 * w, 0,
+                                      p_lo, 0, 0, nullptr, s);
+        }
+        f.swap_lo = 0;
+        return (int)cols.size();
+    }
     for (int64_t j = 0; j < (int64_t)cols.size(); ++j) {
         const int64_t c_lo = cols[j].first, c_hi = cols[j].second, wcols = c_hi - c_lo;
         MP_CUDA(cudaStreamWaitEvent(s, ev[j], 0));
@@ -1232,7 +1319,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         int32_t *ident = pool.get<int32_t>(n);
         launch_init_perm(ident, n, s);
         launch_permute_demote_rhs<float>(v.B, n, nrhs, ident, Y, sio.d, s);
-        static const int kBlocks = [] { const char *e = std::getenv("MP_STREAM_BLOCKS"); return e ? std::max(1, std::min(16, std::atoi(e))) : 4; }();
+        static const int kBlocks = [] { const char *e = std::getenv("MP_STREAM_BLOCKS"); return e ? std::max(1, std::min(16, std::atoi(e))) : 7; }();
         double *parts = pool.get<double>(40);
         const int nparts = run_factor_streamed(a.A, a.lda, const_cast<double *>(v.A), n, W, ldw, nb, ipiv, perm,
                                                sio.d, pool, s, o.variant, (o.flags & 16) == 0, kBlocks, parts,
