@@ -7,7 +7,10 @@
  * (device pointer, leading dimension ldw, the library's working-copy layout)
  *     W[r0+i][c0+j] -= sum_k W[r0+i][k0+k] * W[k0+k][c0+j],  i < M, j < N, k < K.
  * variant: MP_VARIANT_FFMA (CUDA-core FFMA) or MP_VARIANT_3XTF32 (tcgen05 tensor
- * cores, hi/lo TF32 split).  Runs on the library stream (mp_set_stream) and is
+ * cores, hi/lo TF32 split) or MP_VARIANT_TF32, in bits 0-7; bits 8-11: cluster size (1, 2
+ * or 4) of the tcgen05 kernel — CTAs of a cluster take neighbouring tiles of a tile row and
+ * share the L21 boxes by TMA multicast — 0 = the library's policy (MP_GEMM_CLUSTER, clusters
+ * only for launches of several waves of tiles).  Runs on the library stream (mp_set_stream) and is
  * synchronous.  Returns MP_OK or MP_ERR_* (see mp_solve.h).
  *
  * mp_kernel_schur_update_f64: the same update on a row-major binary64 W — DGETRF's

@@ -486,6 +486,12 @@ struct Factor {
     int64_t swap_lo = 0;
     DevStatus *st;
     int nb;
+    // wider panels while the trailing matrix is large (update-bound steps: the update's intensity on
+    // the trailing matrix's HBM traffic doubles): steps with n - k > big_rows
+    // take nb_big columns; 0 = every panel nb wide
+    int nb_big = 0;
+    int64_t big_rows = 0;
+    int width_at(int64_t k) const { return (nb_big > nb && n - k > big_rows) ? nb_big : nb; }
     int variant = MP_VARIANT_FFMA;
     bool fuse_trsm = true;                 // MP_NO_FUSED_TRSM=1: separate K4 + K5 in the panel
     bool tc_inpanel = true;                // MP_NO_TC_INPANEL=1: FFMA tall-skinny GEMM for every in-panel level
@@ -606,8 +612,8 @@ struct Factor {
     void run_sequential() {
         psms = sms;
         if (kb == 0) launch_init_perm(perm, n, s);
-        for (int64_t k = kb; k < ke; k += nb) {
-            const int w = (int)std::min<int64_t>(nb, ke - k);
+        for (int64_t k = kb; k < ke;) {
+            const int w = (int)std::min<int64_t>(width_at(k), ke - k);
             factor_panel(s, k, w, 0);
             // the panel's interchanges on every other column (left factors + trailing matrix)
             prof_begin(KC_LASWP, s);
@@ -617,6 +623,7 @@ struct Factor {
                 trsm(s, k, w, k + w, nc);                                                  // U12 <- L11^-1 A12
                 gemm(s, k + w, k + w, k, n - k - w, nc - k - w, w, true, KC_TRAIL, tf32[0], sms);   // A22 -= L21 U12
             }
+            k += w;
         }
     }
     // Bring the column block [c_lo, c_hi) (its rows already permuted by perm) up to date with the
@@ -728,18 +735,19 @@ struct Factor {
         MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
         MP_CUDA(cudaStreamWaitEvent(cur, e0, 0));
         if (kb == 0) launch_init_perm(perm, n, cur);
-        factor_panel(sP, kb, (int)std::min<int64_t>(nb, ke - kb), 0);
+        factor_panel(sP, kb, (int)std::min<int64_t>(width_at(kb), ke - kb), 0);
         MP_CUDA(cudaEventRecord(eP[0], sP));
-        split_ok[0] = split_l21(kb, (int)std::min<int64_t>(nb, ke - kb), 0);
+        split_ok[0] = split_l21(kb, (int)std::min<int64_t>(width_at(kb), ke - kb), 0);
         int idx = 0;
-        for (int64_t k = kb; k < ke; k += nb, ++idx) {
+        for (int64_t k = kb, knext = kb; k < ke; k = knext, ++idx) {
             if (str && idx >= str->ahead) {   // streamed: the host enqueues at most `ahead` steps ahead
                 const cudaError_t e = cudaEventSynchronize(la_event(70 + (idx - str->ahead) % 8));
                 if (e != cudaSuccess) MP_CUDA(e);
             }
-            const int w = (int)std::min<int64_t>(nb, ke - k);
+            const int w = (int)std::min<int64_t>(width_at(k), ke - k);
             const int64_t kn = k + w;
-            const int wn = kn < ke ? (int)std::min<int64_t>(nb, ke - kn) : 0;
+            knext = kn;
+            const int wn = kn < ke ? (int)std::min<int64_t>(width_at(kn), ke - kn) : 0;
             const int b = idx & 1;
             // early steps (large trailing matrix): the larger update partition
             const bool huge = ex.sU4 && n - kn > ex.huge_rows;
@@ -815,26 +823,34 @@ struct Factor {
 
 template <typename T>
 void make_factor(Factor<T> &f, T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st,
-                 Pool &pool, cudaStream_t s, int variant)
+                 Pool &pool, cudaStream_t s, int variant, bool auto_nb = false)
 {
     f.W = W; f.n = n; f.ldw = ldw; f.ipiv = ipiv; f.perm = perm; f.st = st; f.nb = nb; f.s = s;
     f.sms = num_sms();
     f.variant = variant;
+    // the library's own panel width (opts.nb = 0) on the tensor-core path: nb_big-wide panels while
+    // more than big_rows rows remain (MP_NB_BIG, MP_NB_BIG_ROWS; 0 disables)
+    if (auto_nb && sizeof(T) == 4 && tc_variant(variant)) {
+        static const int env_big = [] { const char *e = std::getenv("MP_NB_BIG"); return e ? std::atoi(e) : 512; }();
+        static const long long env_rows = [] { const char *e = std::getenv("MP_NB_BIG_ROWS"); return e ? std::atoll(e) : 16384LL; }();
+        if (env_big > nb && env_big % nb == 0 && env_rows > 0 && n > env_rows) { f.nb_big = env_big; f.big_rows = env_rows; }
+    }
+    const int nbmax = std::max(nb, f.nb_big);
     if (sizeof(T) == 4 && tc_variant(variant)) {
-        f.tf32[0] = pool.get<float>(tf32_scratch_floats(n, nb));
-        f.tf32[1] = pool.get<float>(tf32_scratch_floats(n, nb));
+        f.tf32[0] = pool.get<float>(tf32_scratch_floats(n, nbmax));
+        f.tf32[1] = pool.get<float>(tf32_scratch_floats(n, nbmax));
         f.tfU[0] = f.tf32[0];
-        f.tfU[1] = pool.get<float>(tf32_scratch_floats(n, nb));
+        f.tfU[1] = pool.get<float>(tf32_scratch_floats(n, nbmax));
     }
     f.ps.orig = pool.get<int32_t>(n);
     // left-looking leaves (MP_PANEL_LL=1, experimental: bitwise-correct but slower than the recursive
     // panel on B200)
     static const bool ll_env = [] { const char *e = std::getenv("MP_PANEL_LL"); return e && e[0] == '1'; }();
-    if (sizeof(T) == 4 && ll_env && nb <= 256 && nb % 8 == 0) {   // (16-byte loads of the multipliers)
+    if (sizeof(T) == 4 && ll_env && nbmax <= 256 && nb % 8 == 0) {   // (16-byte loads of the multipliers)
         f.lpos = pool.get<int32_t>(n);
         f.ll_panel = true;
     }
-    f.ps.pairs = pool.get<int32_t>(4 * (size_t)nb);
+    f.ps.pairs = pool.get<int32_t>(4 * (size_t)nbmax);
     f.ps.npairs = pool.get<int32_t>(1);
     f.ps.ticket = pool.get<int32_t>(1);
     MP_CUDA(cudaMemsetAsync(f.ps.ticket, 0, sizeof(int32_t), s));
@@ -842,7 +858,7 @@ void make_factor(Factor<T> &f, T *W, int64_t n, int64_t ldw, int nb, int32_t *ip
     if (const char *e = std::getenv("MP_NO_TC_INPANEL")) f.tc_inpanel = e[0] != '1';
     if (const char *e = std::getenv("MP_TF32_TERMS4_FRAC")) f.terms4_frac = std::atof(e);
     for (int b = 0; b < 2; ++b) {
-        f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nb);
+        f.ppairs[b] = pool.get<int32_t>(4 * (size_t)nbmax);
         f.nppairs[b] = pool.get<int32_t>(1);
     }
     f.ps.ppairs = f.ppairs[0];
@@ -851,10 +867,10 @@ void make_factor(Factor<T> &f, T *W, int64_t n, int64_t ldw, int nb, int32_t *ip
 
 template <typename T>
 void run_factor(T *W, int64_t n, int64_t ldw, int nb, int32_t *ipiv, int32_t *perm, DevStatus *st, Pool &pool,
-                cudaStream_t s, int variant = MP_VARIANT_FFMA, bool lookahead = true)
+                cudaStream_t s, int variant = MP_VARIANT_FFMA, bool lookahead = true, bool auto_nb = false)
 {
     Factor<T> f;
-    make_factor<T>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant);
+    make_factor<T>(f, W, n, ldw, nb, ipiv, perm, st, pool, s, variant, auto_nb);
     f.run(lookahead);
 }
 
@@ -1353,7 +1369,7 @@ int dsgesv_impl(const Args &a, int *iters, int *info, const mp_opts *opts, mp_re
         if (st0.flags & ST_ZERO_PIVOT) code = -3;                   // (step 1 already ran)
     } else if (!code) {
         // ---- step 1: binary32 blocked GEPP
-        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant, (o.flags & 16) == 0);
+        run_factor<float>(W, n, ldw, nb, ipiv, perm, sio.d, pool, s, o.variant, (o.flags & 16) == 0, o.nb <= 0);
         t_fac = tm.mark();
         const DevStatus &st1 = sio.read();
         if (st1.flags & ST_ZERO_PIVOT) code = -3;
@@ -2790,9 +2806,12 @@ int mp_fgmres_ex(int64_t n, const double *A, int64_t lda, const double *b, doubl
 int mp_kernel_schur_update(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                            int64_t K, int variant)
 {
+    const int cluster = (variant >> 8) & 0xf;      // bits 8-11: cluster size of the tcgen05 kernel (0: default policy)
+    variant &= 0xff;
     return guarded([&] {
         cudaStream_t s = g_stream;
         if (tc_variant(variant)) {
+            struct Force { explicit Force(int c) { set_gemm_tf32_cluster(c); } ~Force() { set_gemm_tf32_cluster(0); } } force(cluster);
             float *scratch = nullptr;
             const size_t bytes = ((size_t)2 * M * round_up(K, 4) + (size_t)2 * N * round_up(K, 4) + 4096) * 4;
             MP_CUDA(cudaMallocFromPoolAsync((void **)&scratch, bytes, library_pool(), s));

@@ -230,6 +230,8 @@ size_t tf32_scratch_floats(int64_t n, int nbmax);
 template <typename T>
 bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K,
                             int32_t *ticket, cudaStream_t s);
+// cluster size of the tensor-core update for the calling thread's launches (0: the default policy)
+void set_gemm_tf32_cluster(int cs);
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                                int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false);
 // split of the A operand only (see launch_gemm_ops_3xtf32's reuse_a)

@@ -71,6 +71,33 @@ def test_schur_update_gaussian_accuracy(mp, variant):
     assert np.array_equal(got[:r0], W0[:r0]) and np.array_equal(got[:, :c0], W0[:, :c0])
 
 
+CLUSTER_SHAPES = [(300, 200, 7, 512, 333, 32), (1000, 700, 16, 1400, 1200, 256), (513, 129, 40, 700, 700, 200),
+                  (256, 1300, 0, 600, 1700, 256), (2048, 2048, 256, 2304, 2304, 256)]
+
+
+@pytest.mark.parametrize("cluster", [1, 2, 4, 8])
+@pytest.mark.parametrize("shape", CLUSTER_SHAPES)
+def test_schur_update_clusters_exact_and_bitwise(mp, cluster, shape):
+    """The tcgen05 update with its L boxes multicast over clusters of 2 / 4 CTAs (variant bits 8-11):
+    exact on small integers (odd tile counts: a cluster's surplus CTA stores nothing) and, on
+    Gaussian data, bitwise equal to the single-CTA kernel (same MMA order per tile).  cluster = 8
+    selects the CTA-pair kernel (tcgen05 cta_group::2: one 256 x 256 instruction tile per pair)."""
+    M, N, k0, rows, cols, K = shape
+    rng = np.random.default_rng(M + N + K + cluster)
+    ldw = ((cols + 63) // 64) * 64
+    W0 = rng.integers(-8, 9, size=(rows, ldw)).astype(np.float32)
+    r0, c0 = k0 + K, k0 + K
+    M, N = min(M, rows - r0), min(N, cols - c0)
+    got = run(mp, W0, r0, c0, k0, M, N, K, 1 | (cluster << 8))
+    assert np.array_equal(got.astype(np.float64), reference(W0, r0, c0, k0, M, N, K))
+    G0 = rng.standard_normal((rows, ldw)).astype(np.float32)
+    one = run(mp, G0, r0, c0, k0, M, N, K, 1 | (1 << 8))
+    got = run(mp, G0, r0, c0, k0, M, N, K, 1 | (cluster << 8))
+    assert np.array_equal(got, one)
+    got1 = run(mp, G0, r0, c0, k0, M, N, K, 2 | (cluster << 8))     # 1xTF32 (hi boxes only)
+    assert np.array_equal(got1, run(mp, G0, r0, c0, k0, M, N, K, 2 | (1 << 8)))
+
+
 # --------------------------------------------------------------------------- binary64 update (FP64 path)
 def run64(mp, W0, r0, c0, k0, M, N, K, pipe):
     import torch

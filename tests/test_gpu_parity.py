@@ -466,3 +466,57 @@ def test_left_looking_panel_option(mp, n):
     assert r.returncode == 0, r.stderr[-2000:]
     ok, it, it_or, info = map(int, r.stdout.split()[-4:])
     assert ok == 1 and info == 0 and abs(it - it_or) <= 1
+
+
+_CLUSTER_CHILD = """
+import hashlib, sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from paper_0808_2794_b200 import binding as mp, inputs
+n = int(sys.argv[2])
+A, B, X, perm, L, U = inputs.exact_lu(n, nrhs=1, seed=n)
+LU, ipiv, info = mp.mp_sgetrf(A, mp.make_opts(nb=256))
+p = np.arange(n)
+for k, q in enumerate(ipiv):
+    p[k], p[q] = p[q], p[k]
+ok = info == 0 and np.array_equal(p, perm) and np.array_equal(np.tril(LU, -1).astype(float), np.tril(L, -1)) \
+     and np.array_equal(np.triu(LU).astype(float), U)
+Ac, Bc, Xc, Lc = inputs.exact_chol(n, nrhs=1, seed=n + 17)
+Lg, infoc = mp.mp_spotrf(Ac, mp.make_opts(nb=256))
+ok = ok and infoc == 0 and np.array_equal(np.tril(Lg).astype(np.float64), Lc)
+h = hashlib.sha1()
+A2, B2, _ = inputs.gaussian(n, nrhs=2, seed=n + 1)
+Xg, it, info2, _ = mp.mp_dsgesv_ex(mp.colmajor_cuda(A2), mp.colmajor_cuda(B2))
+torch.cuda.synchronize()
+h.update(Xg.cpu().numpy().tobytes())
+LU2, ipiv2, info3 = mp.mp_sgetrf(A2, mp.make_opts(nb=128))
+h.update(np.ascontiguousarray(LU2).tobytes()); h.update(np.ascontiguousarray(ipiv2).tobytes())
+A3, B3, _ = inputs.spd_wishart(n, nrhs=1, seed=n + 2)
+X3, it3, info4, _ = mp.mp_dsposv_ex(mp.colmajor_cuda(A3), mp.colmajor_cuda(B3))
+torch.cuda.synchronize()
+h.update(X3.cpu().numpy().tobytes())
+print(int(ok), it, it3, info2 + info3 + info4, h.hexdigest())
+"""
+
+
+@pytest.mark.parametrize("n", [1300, 2600])
+def test_update_cluster_modes_bitwise(mp, n):
+    """The tensor-core update's cluster modes (MP_GEMM_CLUSTER, read once per process: run in children
+    with MP_GEMM_CLUSTER_WAVES=0 so that every tcgen05 launch takes the mode, whatever its size): CTA
+    pairs (8, tcgen05 cta_group::2, the default for large launches) and multicast clusters (2, 4) give
+    the exact-LU / exact-Cholesky factors bitwise and the same bits as single CTAs (1) for Gaussian
+    LU factors, the refined solution and the SPD solve (LOWER tiles: a pair's tile above the diagonal
+    stores nothing)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = {}
+    for cs in (1, 2, 4, 8):
+        r = subprocess.run([sys.executable, "-c", _CLUSTER_CHILD, root, str(n)],
+                           env=dict(os.environ, MP_GEMM_CLUSTER=str(cs), MP_GEMM_CLUSTER_WAVES="0"),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[cs] = r.stdout.split()[-5:]
+        assert res[cs][0] == "1" and res[cs][3] == "0", (cs, res[cs])
+    assert res[2] == res[1] and res[4] == res[1] and res[8] == res[1], res
