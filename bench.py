@@ -283,8 +283,8 @@ def run_distributed(args, rank, world, dev, dist, mp, variant):
 # --------------------------------------------------------------------------- our arm
 def _gemm_traffic():
     """dram bytes (read + write) of one trailing-update launch from the committed ncu --set full
-    capture of the current code (profiles/r02_gemm_full.json), with its algorithmic bytes; None if absent."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full.json")
+    capture of the current code (profiles/r02_gemm_full_pair.json), with its algorithmic bytes; None if absent."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full_pair.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -296,8 +296,8 @@ def _gemm_traffic():
 
 def _gemm_alone(peak: float):
     """The same kernel with the whole GPU (one trailing-update launch outside the look-ahead), from the
-    committed ncu capture (profiles/r02_gemm_full.json; ncu's own duration, so context, not the bench value)."""
-    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full.json")
+    committed ncu capture (profiles/r02_gemm_full_pair.json; ncu's own duration, so context, not the bench value)."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_gemm_full_pair.json")
     try:
         with open(p) as f:
             d = json.load(f)
