@@ -323,7 +323,7 @@ ExecRes make_exec_res(int dev)
     CUdevResource all, grp[1], rest;
     unsigned ng = 1;
     if (getRes((CUdevice)dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return r;
-    unsigned psms = 48;                       // SMs kept free of the trailing update (MP_PANEL_SMS)
+    unsigned psms = 40;                       // SMs kept free of the trailing update (MP_PANEL_SMS)
     if (const char *e = std::getenv("MP_PANEL_SMS")) psms = (unsigned)std::max(16, std::atoi(e));
     if (split(grp, &ng, &all, &rest, CU_DEV_SM_RESOURCE_SPLIT_MAX_POTENTIAL_CLUSTER_SIZE, psms) != CUDA_SUCCESS || ng != 1)
         return r;
@@ -530,12 +530,13 @@ struct Factor {
     // Schur update C -= L U.  big: the trailing update or the next panel's columns
     // (tensor-core variant when selected); scratch / nsm: the launching stream's.
     void gemm(cudaStream_t q, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N, int64_t K, bool big,
-              int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3, bool reuse_b = false) {
+              int cls, float *scratch, int nsm, bool reuse_a = false, int terms = 3, bool reuse_b = false,
+              float *bscratch = nullptr) {
         prof_begin(cls, q);
         if constexpr (sizeof(T) == 4) {
             if (big && tc_variant(variant) && M >= 256 && N >= 128)
                 launch_gemm_update_3xtf32(W, ldw, r0, c0, k0, M, N, K, scratch, nsm, q, reuse_a,
-                                          variant == MP_VARIANT_TF32 ? 1 : terms, reuse_b);
+                                          variant == MP_VARIANT_TF32 ? 1 : terms, reuse_b, bscratch);
             else
                 launch_gemm_update<T>(W, ldw, r0, c0, k0, M, N, K, q);
         } else {
@@ -718,26 +719,40 @@ struct Factor {
         psms = std::max(8, sms - ex.smsU);
         cudaEvent_t e0 = la_event(0), eP[2] = {la_event(1), la_event(2)}, eN = la_event(3);
         cudaEvent_t eEndP = la_event(4), eEndU = la_event(5), eSw = la_event(6), eS[2] = {la_event(7), la_event(8)};
+        cudaEvent_t eR[2] = {la_event(9), la_event(10)};
+        static const bool next_on_panel_env = [] { const char *e = std::getenv("MP_LA_NEXT_ON_PANEL"); return !e || e[0] != '0'; }();
+        const bool next_on_panel = next_on_panel_env && sizeof(T) == 4;
         // L21 of panel j (rows [j + w, n) x its columns) split hi/lo on the panel stream right after
         // the panel, into the update scratch of that step's parity: the update stream's interchanges
         // and TRSM of the next panel's columns run meanwhile (the split is off its critical path)
         const bool presplit = sizeof(T) == 4 && tc_variant(variant) && tfU[1] != nullptr;
-        auto split_l21 = [&](int64_t kp0, int wp, int bb) -> bool {
+        auto split_l21 = [&](int64_t kp0, int wp, int bb, cudaStream_t q) -> bool {
             const int64_t M = n - kp0 - wp;
             if (!presplit || M < 256) return false;
             if constexpr (sizeof(T) == 4)
-                launch_split_a_3xtf32(W + (kp0 + wp) * ldw + kp0, ldw, M, wp, tfU[bb], sP);
-            MP_CUDA(cudaEventRecord(eS[bb], sP));
+                launch_split_a_3xtf32(W + (kp0 + wp) * ldw + kp0, ldw, M, wp, tfU[bb], q);
+            MP_CUDA(cudaEventRecord(eS[bb], q));
             return true;
         };
         bool split_ok[2] = {false, false};
+        // steps that bring the next panel's columns up to date on the panel stream (see below); their
+        // L21 split runs on the (then idle) update stream at the start of the step instead (pending)
+        auto on_panel_step = [&](int64_t kk) {
+            if (!next_on_panel || str || kk >= ke) return false;
+            const int64_t kn_ = kk + std::min<int64_t>(width_at(kk), ke - kk);
+            const bool huge_ = ex.sU4 && n - kn_ > ex.huge_rows;
+            const bool early_ = !huge_ && ex.sU2 && (double)(n - kn_) > ex.big_frac * (double)n;
+            return !huge_ && !early_ && kn_ < ke;
+        };
+        bool pending[2] = {false, false};
         MP_CUDA(cudaEventRecord(e0, s));
         MP_CUDA(cudaStreamWaitEvent(sP, e0, 0));
         MP_CUDA(cudaStreamWaitEvent(cur, e0, 0));
         if (kb == 0) launch_init_perm(perm, n, cur);
         factor_panel(sP, kb, (int)std::min<int64_t>(width_at(kb), ke - kb), 0);
         MP_CUDA(cudaEventRecord(eP[0], sP));
-        split_ok[0] = split_l21(kb, (int)std::min<int64_t>(width_at(kb), ke - kb), 0);
+        if (on_panel_step(kb)) pending[0] = true;
+        else split_ok[0] = split_l21(kb, (int)std::min<int64_t>(width_at(kb), ke - kb), 0, sP);
         int idx = 0;
         for (int64_t k = kb, knext = kb; k < ke; k = knext, ++idx) {
             if (str && idx >= str->ahead) {   // streamed: the host enqueues at most `ahead` steps ahead
@@ -761,6 +776,34 @@ struct Factor {
                 cur = sU;
             }
             MP_CUDA(cudaStreamWaitEvent(sU, eP[b], 0));
+            // (default; MP_LA_NEXT_ON_PANEL=0 disables) steps whose update is hidden (neither the early nor the huge phase):
+            // the next panel's columns are brought up to date on the PANEL stream itself (no hop to the
+            // update stream and back on the critical path); it waits for the previous step's trailing
+            // update (eR), shares the L21 split with the update stream and keeps U12's split of those
+            // columns in the panel stream's own scratch
+            const bool on_panel = on_panel_step(k);
+            if (on_panel) {
+                if (pending[b]) { split_ok[b] = split_l21(k, w, b, sU); pending[b] = false; }
+                if (idx > 0) MP_CUDA(cudaStreamWaitEvent(sP, eR[b ^ 1], 0));
+                prof_begin(KC_LASWP, sP);
+                launch_laswp_pairs<T>(W, ldw, ppairs[b], nppairs[b], 2 * w, kn, kn + wn, 0, 0, nullptr, sP);
+                prof_end(KC_LASWP, 2.0 * 2 * w * (double)wn * sizeof(T), sP);
+                const int kp = (int)round_up(w, 4);
+                // A split: the shared one in tfU[b] when it exists; B split: always the panel stream's
+                // own (second half of tf32[1]; the update stream writes its U12 split into tfU[b])
+                float *bs = split_ok[b] && tf32[1] ? tf32[1] + 2 * (size_t)n * kp : nullptr;
+                const bool bsplit = bs && wn >= 128 && w <= 256;
+                trsm(sP, k, w, kn, kn + wn, bsplit ? bs : nullptr, bsplit ? bs + (size_t)wn * kp : nullptr, kp);
+                const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
+                if (split_ok[b]) MP_CUDA(cudaStreamWaitEvent(sP, eS[b], 0));
+                gemm(sP, kn, kn, k, n - kn, wn, w, true, KC_TRAIL, bs ? tfU[b] : tf32[1], sms, bs != nullptr, terms, bsplit, bs);
+                psms = std::max(8, sms - smsu);
+                factor_panel(sP, kn, wn, b ^ 1);
+                MP_CUDA(cudaEventRecord(eP[b ^ 1], sP));
+                if (on_panel_step(kn)) { pending[b ^ 1] = true; split_ok[b ^ 1] = false; }
+                else split_ok[b ^ 1] = split_l21(kn, wn, b ^ 1, sP);
+                if (split_ok[b]) MP_CUDA(cudaStreamWaitEvent(sU, eS[b], 0));
+            } else
             if (kn < ke) {
                 // the next panel's columns first (on the panel's critical path) ...
                 prof_begin(KC_LASWP, sU);
@@ -781,7 +824,8 @@ struct Factor {
                 psms = std::max(8, sms - smsu);
                 factor_panel(sP, kn, wn, b ^ 1);
                 MP_CUDA(cudaEventRecord(eP[b ^ 1], sP));
-                split_ok[b ^ 1] = split_l21(kn, wn, b ^ 1);
+                if (on_panel_step(kn)) { pending[b ^ 1] = true; split_ok[b ^ 1] = false; }
+                else split_ok[b ^ 1] = split_l21(kn, wn, b ^ 1, sP);
             }
             // ... then every other column (left factors, rest of the trailing matrix), off it
             // (streamed: the columns that have joined so far; their catch-up share of this step)
@@ -798,12 +842,13 @@ struct Factor {
                 float *bh = bsplit ? tfU[b] + 2 * (size_t)(n - kn) * kp : nullptr;
                 trsm(sU, k, w, kn + wn, ncu, bh, bsplit ? bh + (size_t)nr * kp : nullptr, kp);
                 // same L21 as the next panel's update just before: its hi/lo split is reused
-                const bool reuse = split_ok[b] || (kn < n && n - kn >= 256 && wn >= 128);
+                const bool reuse = split_ok[b] || (!on_panel && kn < n && n - kn >= 256 && wn >= 128);
                 const int terms = (double)(n - kn) < terms4_frac * (double)n ? 4 : 3;
                 gemm(sU, kn, kn + wn, k, n - kn, nr, w, true, KC_TRAIL, split_ok[b] ? tfU[b] : tf32[0], smsu,
                      reuse, terms, bsplit);
             }
             if (str) MP_CUDA(cudaEventRecord(la_event(70 + idx % 8), sU));
+            if (next_on_panel) MP_CUDA(cudaEventRecord(eR[b], sU));
         }
         MP_CUDA(cudaEventRecord(eEndP, sP));
         MP_CUDA(cudaEventRecord(eEndU, cur));

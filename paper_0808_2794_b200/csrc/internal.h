@@ -233,11 +233,13 @@ bool launch_trsm_gemm_fused(T *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k
 // cluster size of the tensor-core update for the calling thread's launches (0: the default policy)
 void set_gemm_tf32_cluster(int cs);
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
-                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false);
+                               int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false,
+                               float *bscratch = nullptr);
 // split of the A operand only (see launch_gemm_ops_3xtf32's reuse_a)
 void launch_split_a_3xtf32(const float *A, int64_t lda, int64_t M, int64_t K, float *scratch, cudaStream_t s);
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
-                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false);
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a = false, int terms = 3, bool reuse_b = false,
+                            float *bscratch = nullptr);
 
 // ---------------------------------------------------------------- K7/K9 triangular solves (k_solve.cu)
 struct SolveScratch {

@@ -809,12 +809,15 @@ size_t tf32_scratch_floats(int64_t n, int nbmax)
 }
 
 void launch_gemm_ops_3xtf32(const float *A, int64_t lda, const float *B, int64_t ldb, float *C, int64_t ldc, int64_t M,
-                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms, bool reuse_b)
+                            int64_t N, int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms, bool reuse_b,
+                            float *bscratch)
 {
     if (M <= 0 || N <= 0 || K <= 0) return;
     const int kp = (int)round_up(K, 4);
     float *Lh = scratch, *Ll = Lh + (size_t)M * kp;
-    float *Uh = Ll + (size_t)M * kp, *Ul = Uh + (size_t)N * kp;
+    // bscratch: the B operand's split lives in its own buffer (the look-ahead's next-panel update on
+    // the panel stream shares the A split with the update stream but not the B split)
+    float *Uh = bscratch ? bscratch : Ll + (size_t)M * kp, *Ul = Uh + (size_t)N * kp;
     {
         const int64_t tot = M * kp;
         if (!reuse_a)                       // reuse_a: Lh/Ll already hold this A (same M, K, scratch)
@@ -854,10 +857,10 @@ void launch_split_a_3xtf32(const float *A, int64_t lda, int64_t M, int64_t K, fl
 
 void launch_gemm_update_3xtf32(float *W, int64_t ldw, int64_t r0, int64_t c0, int64_t k0, int64_t M, int64_t N,
                                int64_t K, float *scratch, int num_sms, cudaStream_t s, bool reuse_a, int terms,
-                               bool reuse_b)
+                               bool reuse_b, float *bscratch)
 {
     launch_gemm_ops_3xtf32(W + r0 * ldw + k0, ldw, W + k0 * ldw + c0, ldw, W + r0 * ldw + c0, ldw, M, N, K, scratch,
-                           num_sms, s, reuse_a, terms, reuse_b);
+                           num_sms, s, reuse_a, terms, reuse_b, bscratch);
 }
 
 }  // namespace mp
