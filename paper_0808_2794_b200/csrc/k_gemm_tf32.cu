@@ -449,7 +449,25 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_c
         if constexpr (!LOWER) return false;
         return tm * TM_ROWS + TM_ROWS - 1 < tn * TM_COLS;
     };
-    auto skip = [&](int t) { return skip_tile(t / tiles_ng, (t % tiles_ng) * 2); };
+    // Tile order: column bands of bw tile pairs, swept row by row, so that a band's U boxes
+    // (bw x 256 columns x K x 8 B, kept to ~32 MB: half of L2 is what one die's SMs see) stay in L2
+    // while the trailing matrix streams through once.  (Row-major order over all tile columns
+    // re-reads U from HBM on every tile row once 2 N K 4 B exceeds that: ncu at M = N = 48128,
+    // K = 512 showed 38.4 GB of DRAM reads against 9.7 GB algorithmic.)
+    const int bw = max(1, min(step, (32 << 20) / (2 * TM_COLS * 8 * max(K, 1))));
+    const int nfull = tiles_ng / bw, rem = tiles_ng - nfull * bw, per_band = bw * tiles_m;
+    auto tile_of = [&](int t, int &tm, int &g) {
+        if (t < nfull * per_band) {
+            const int band = t / per_band, r = t - band * per_band;
+            tm = r / bw;
+            g = band * bw + (r - tm * bw);
+        } else {
+            const int r = t - nfull * per_band;
+            tm = r / rem;
+            g = nfull * bw + (r - tm * rem);
+        }
+    };
+    auto skip = [&](int t) { int tm, g; tile_of(t, tm, g); return skip_tile(tm, g * 2); };
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < P_STAGES; ++s) { mbar_init(&full_bar[s], 1); mbar_init(&empty_bar[s], 1); }
@@ -476,7 +494,9 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_c
             const int lr0 = crank * (TM_ROWS / 2);
             for (int t = first; t < ntiles; t += step) {
                 if (skip(t)) continue;
-                const int tn = (t % tiles_ng) * 2 + crank, tm = t / tiles_ng;
+                int tm, g;
+                tile_of(t, tm, g);
+                const int tn = g * 2 + crank;
                 for (int kc = 0; kc < nk; ++kc) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     unsigned char *st = smem + stage * P_STAGE_BYTES;
@@ -547,7 +567,9 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_c
         const uint32_t lempty[2] = {mapa_u32(smem_u32(&acc_empty[0]), 0), mapa_u32(smem_u32(&acc_empty[1]), 0)};
         for (int t = first; t < ntiles; t += step) {
             if (skip(t)) continue;
-            const int tn = (t % tiles_ng) * 2 + crank, tm = t / tiles_ng;
+            int tm, g;
+            tile_of(t, tm, g);
+            const int tn = g * 2 + crank;
             const int j = tn * TM_COLS + q * 32 + lane;
             const int i0 = tm * TM_ROWS + h * (TM_ROWS / 2);
             const bool jv = j < N && !skip_tile(tm, tn);
