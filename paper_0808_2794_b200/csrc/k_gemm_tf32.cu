@@ -454,7 +454,10 @@ gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmUh, const __grid_c
     // while the trailing matrix streams through once.  (Row-major order over all tile columns
     // re-reads U from HBM on every tile row once 2 N K 4 B exceeds that: ncu at M = N = 48128,
     // K = 512 showed 38.4 GB of DRAM reads against 9.7 GB algorithmic.)
-    const int bw = max(1, min(step, (32 << 20) / (2 * TM_COLS * 8 * max(K, 1))));
+    // (LOWER keeps row-major order, bw = all tile pairs of a row: with a fixed tile column per cluster
+    // the clusters left of the diagonal would do all the rows and those on the right almost none —
+    // SPD n = 16384 37.3 -> 40.1 ms with bands)
+    const int bw = LOWER ? max(1, tiles_ng) : max(1, min(step, (32 << 20) / (2 * TM_COLS * 8 * max(K, 1))));
     const int nfull = tiles_ng / bw, rem = tiles_ng - nfull * bw, per_band = bw * tiles_m;
     auto tile_of = [&](int t, int &tm, int &g) {
         if (t < nfull * per_band) {
